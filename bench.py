@@ -1,0 +1,362 @@
+"""Benchmark of the serving-time ranking path (BASELINE.json metric:
+candidates scored/sec at 16k lifelong seq; p50/p99 request ms).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--mode bf16|fp32] [--config c2|c1|c3]
+
+One step = one request of BASELINE configs[1] (1 user, 1,000 candidates,
+L=16,384, NNConfig(32, 96, 32, 32) -> S=192) through stage -> NN select ->
+SKUT -> head.  N>1 (torchrun, one rank per GPU): every rank scores its own
+independent requests (weak scaling, no data-path collective); ``value`` is
+the aggregate over ranks / the max-over-ranks device time.
+
+``value``: device-resident inputs (staged once per pool request), CUDA events
+around each step on the launch stream, L2 flushed between timed steps.
+``e2e``: the public API ``Engine.rank_requests`` from host numpy buffers,
+host->device and device->host copies inside the timed region.
+``--impl reference`` times the CPU oracle port of the reference path on all
+host cores (rank 0 only) and prints the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "candidates scored/sec at 16k lifelong seq (1/2/4/8 B200); p50/p99 request ms"
+UNIT = "candidates/s"
+CONFIGS = {
+    # name: (requests per step, candidates per request, LL tokens, NNConfig)
+    "c2": (1, 1000, 16384, (32, 96, 32, 32)),
+    "c1": (1, 64, 1024, (32, 32, 0, 0)),
+    "c3": (32, 500, 16384, (32, 96, 32, 32)),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained"), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def flops_per_candidate(L, nn, d=64, f=32, layers=2, E=32, ctx=8, h=64, H=4):
+    """SURVEY.md §8(d) algorithmic FLOPs per candidate."""
+    r, kl, kr, ki = nn
+    S = r + kl + kr + ki
+    rt, imp = 256, 256
+    nn_f = 2 * E * (L + max(0, rt - r) + imp)
+    tf = layers * (8 * S * d * d + 2 * d * S * (S + 1) + 4 * S * d * f)
+    pool = 2 * S * d * d
+    head = 2 * (d + E + ctx) * h + 2 * h * H
+    return dict(nn=nn_f, transformer=tf, pool=pool, head=head, total=nn_f + tf + pool + head)
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (oracle port of the reference path), one process per core
+# ---------------------------------------------------------------------------
+
+def _cpu_worker(args):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    seed, n_cand, L, nn, reps = args
+    import paper_2506_02267_b200 as P
+    from oracle import seqrank_oracle as orc
+    r = P.generate_requests(1, n_cand, ll_tokens=L, seed=seed)[0]
+    user = {f"{s}_{c}": getattr(b, a) for s, b in zip(("ll", "rt", "imp"), r.user.blocks())
+            for c, a in (("emb", "embeddings"), ("action", "actions"), ("surface", "surfaces"),
+                         ("ts", "timestamps"))}
+    Pd = orc.model_init(0, seq_len=sum(nn))
+    lat = []
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        t = time.perf_counter()
+        orc.rank_request(user, r.candidates, r.ctx, Pd, nn)
+        lat.append(time.perf_counter() - t)
+    return n_cand * reps, time.perf_counter() - t0, lat
+
+
+def cpu_baseline(cfg_name, seconds_budget=12.0, procs=None):
+    """Bounded sample: each process scores `n` candidates of a full-length
+    request (L as configured) `reps` times; aggregate cand/s over all cores."""
+    reqs, n_cand, L, nn = CONFIGS[cfg_name]
+    procs = procs or os.cpu_count() or 1
+    n = min(n_cand, 250)  # ~1 s per process per rep at ~250 cand/s/core
+    env_old = os.environ.get("OPENBLAS_NUM_THREADS")
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(procs) as pool:
+        # calibrate one rep on one process first (bounded), then size reps
+        done, secs, _ = pool.apply(_cpu_worker, ((0, n, L, nn, 1),))
+        per = secs / 1
+        reps = max(1, int(seconds_budget / max(per, 1e-3)))
+        reps = min(reps, 8)
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_worker, [(i, n, L, nn, reps) for i in range(procs)])
+        wall = time.perf_counter() - t0
+    if env_old is None:
+        os.environ.pop("OPENBLAS_NUM_THREADS", None)
+    else:
+        os.environ["OPENBLAS_NUM_THREADS"] = env_old
+    total = sum(r[0] for r in res)
+    lats = [x for r in res for x in r[2]]
+    return {
+        "value": total / wall, "unit": UNIT, "cores": procs, "kind": "port",
+        "sample": (f"{procs} processes x {reps} reps x {n} candidates of one L={L} request "
+                   f"(oracle port of build_dedup_batch->fused_assemble->encode_batch->forward_fused"
+                   f"->pool->head, OPENBLAS_NUM_THREADS=1); {wall:.1f}s wall"),
+        "per_process_cand_s": n / statistics.median(lats),
+        "request_ms_p50_for_sample": 1e3 * sorted(lats)[len(lats) // 2],
+    }
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2506_02267_b200 as P
+    from paper_2506_02267_b200.runtime import Capacity, Engine
+    from paper_2506_02267_b200.serving import nearest_rank
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n_req, n_cand, L, nn_t = CONFIGS[args.config]
+    nn = P.NNConfig(*nn_t)
+    model = P.RankingModel.init(P.ModelConfig.for_nn(nn), seed=0)
+    cap = Capacity(n_req, n_req * n_cand, n_req * (L + 512))
+    eng = Engine(model, capacity=cap, device=local_rank)
+    # a pool of distinct requests per rank (different seeds per rank)
+    pool_n = max(2, args.pool)
+    pool = [P.generate_requests(n_req, n_cand, ll_tokens=L, seed=1000 * rank + i) for i in range(pool_n)]
+    packed = [[(r.user, r.candidates, r.ctx) for r in reqs] for reqs in pool]
+    mode = args.mode
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    logits = torch.empty((n_req * n_cand, 4), dtype=torch.float32, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- device-resident throughput (value) ----
+    eng.stage(packed[0])
+    for _ in range(args.warmup):
+        eng.run_staged(mode, logits)
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    eng.set_profiling(True)
+    barrier()
+    torch.cuda.synchronize()
+    with Clocks(local_rank) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))  # evict the previous step's working set from L2 (untimed)
+            starts[i].record()
+            eng.run_staged(mode, logits)
+            ends[i].record()
+        torch.cuda.synchronize()
+    barrier()
+    launches_per_step = eng.last_launch_count()
+    kt = eng.kernel_times()
+    eng.set_profiling(False)
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    dev_ms = sum(step_ms)
+    t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    cand_step = n_req * n_cand
+    value = world * cand_step * args.steps / (max_ms / 1e3)
+
+    # ---- end-to-end through the public API (host buffers, H2D + D2H inside) ----
+    for i in range(args.warmup):
+        eng.rank_requests(packed[i % pool_n], mode=mode)
+    barrier()
+    torch.cuda.synchronize()
+    lat = []
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        ts = time.perf_counter()
+        eng.rank_requests(packed[i % pool_n], mode=mode)
+        lat.append(time.perf_counter() - ts)
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * cand_step * args.steps / float(te.item())
+    h2d = _staged_bytes(packed[0])
+    d2h = cand_step * 4 * 4
+
+    # ---- roofline of the dominant kernel ----
+    fl = flops_per_candidate(L, nn_t)
+    hbm, tflops, tflops_sus, src = peaks()
+    dom = max(kt.items(), key=lambda kv: kv[1][0]) if kt else None
+    roof = None
+    if dom:
+        name, (ms, n) = dom
+        per_launch_ms = ms / max(n, 1)
+        if name.startswith("skut"):
+            work = cand_step * (fl["transformer"] + fl["pool"] + fl["head"])
+        elif name.startswith("nn_"):
+            work = cand_step * fl["nn"]
+        else:
+            work = None
+        if work is not None:
+            ach = work / (per_launch_ms / 1e3) / 1e12
+            roof = {"kernel": name, "bound": "tensor", "achieved": round(ach, 3),
+                    "peak": tflops, "unit": "TFLOP/s", "frac": round(ach / tflops, 5),
+                    "peak_source": f"{src} bf16_tflops (burst)", "traffic": None,
+                    "kernel_ms_per_launch": round(per_launch_ms, 4),
+                    "share_of_step": round(ms / max(dev_ms, 1e-9), 3)}
+    out = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16x3 (fp32-accurate split) tensor + i8 NN" if mode == "bf16" else "fp32",
+        "mode": mode, "data": "synthetic (generate_requests, seqrank.dataset distribution), random-init weights seed 0",
+        "config": {"workload": f"{args.config}: {n_req} request(s) x {n_cand} candidates, L={L}, "
+                               f"RT=256, IMP=256, NNConfig{nn_t} -> S={nn.seq_len}, 2 layers d=64",
+                   "requests_per_step_per_gpu": n_req, "candidates_per_step_per_gpu": cand_step,
+                   "parallelism": f"request-sharded x{world} (no collective)",
+                   "l2": "flushed between timed steps (256 MB write, untimed)"},
+        "p50_request_ms": round(nearest_rank(step_ms, 50), 4),
+        "p99_request_ms": round(nearest_rank(step_ms, 99), 4),
+        "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "p50_request_ms": round(1e3 * nearest_rank(lat, 50), 4),
+                "p99_request_ms": round(1e3 * nearest_rank(lat, 99), 4)},
+        "gpu_launches": launches_per_step * args.steps,
+        "kernels": {k: {"ms_per_launch": round(v[0] / max(v[1], 1), 4), "launches": v[1]} for k, v in kt.items()},
+        "roofline": roof,
+        "clocks": clk.summary(),
+    }
+    return out
+
+
+def _staged_bytes(reqs):
+    """Bytes of the one H2D copy per step (token columns + candidates + ctx + plan)."""
+    tok = sum(r[0].total_tokens() for r in reqs)
+    n = sum(len(r[1]) for r in reqs)
+    return tok * (32 + 2 + 1) + n * (32 * 4 + 4) + len(reqs) * (8 * 4 + 40)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--pool", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        steps_rates = []
+        cb = None
+        for i in range(args.warmup + args.steps):
+            if i < args.warmup:
+                continue
+            cb = cpu_baseline(args.config, seconds_budget=4.0)
+            steps_rates.append(cb["value"])
+        value = statistics.median(steps_rates)
+        n_req, n_cand, L, nn_t = CONFIGS[args.config]
+        print(json.dumps({
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "impl": "reference",
+            "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32/f64 (numpy)", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {n_req} request(s) x {n_cand} candidates, L={L}, NNConfig{nn_t}"},
+            "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cb["cores"], "kind": "port",
+                             "sample": cb["sample"]},
+            "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }))
+        return
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    out = run_gpu(args, rank, world, local_rank)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            cb = cpu_baseline(args.config)
+            out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,621 @@
+// C ABI (include/tav2.h): worker context, pinned staging arena, parameter
+// upload, batch planning and the launch sequence of the ranking path.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "tav2_common.cuh"
+
+using namespace tav2;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(TAV2_ECUDA, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                               \
+  } while (0)
+
+constexpr int kTile = 128;        // candidates per NN tile (tcgen05 M)
+constexpr int kTargetWork = 296;  // ~2 NN work units per SM
+constexpr int kMinChunk = 256;    // minimum LL tokens per work unit
+constexpr int kCaps[3] = {16384, 256, 256};  // LIFELONG/REALTIME/IMPRESSION_CAP (core.py:31-33)
+
+inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+struct tav2_ctx {
+  tav2_config cfg;
+  tav2_capacity cap;
+  int device = 0;
+  NNCfg nn{};
+  int kmax = 1;
+  int max_tiles = 0, max_work = 0;
+  // pinned host arena + device mirror of the staged region
+  unsigned char* h_arena = nullptr;
+  unsigned char* d_staged = nullptr;
+  int64_t staged_cap = 0;
+  cudaEvent_t ev_staged = nullptr;
+  // derived device buffers
+  float* tok_unit = nullptr;
+  double* tok_rnorm = nullptr;
+  float* cand_unit = nullptr;
+  uint64_t* part = nullptr;
+  int32_t* idx = nullptr;
+  float* logits = nullptr;
+  float* skut_scratch = nullptr;
+  // params
+  float* d_params = nullptr;
+  Params params{};
+  bool params_ok = false;
+  // current batch
+  Plan plan{};
+  bool staged = false;
+  int launches = 0;
+  // per-kernel profiling (CUDA events on the launch stream)
+  struct Slot {
+    const char* name = nullptr;
+    cudaEvent_t a = nullptr, b = nullptr;
+    bool pending = false;
+    double ms = 0.0;
+    int n = 0;
+  };
+  static constexpr int kSlots = 8;
+  Slot slots[kSlots];
+  bool profiling = false;
+};
+
+namespace {
+
+Staged staged_view(tav2_ctx* c) {
+  Staged s{};
+  const Plan& p = c->plan;
+  unsigned char* b = c->d_staged;
+  s.req = reinterpret_cast<const ReqInfo*>(b + p.off_req);
+  s.tiles = reinterpret_cast<const NNTile*>(b + p.off_tiles);
+  s.work = reinterpret_cast<const NNWork*>(b + p.off_work);
+  s.item_req = reinterpret_cast<const int32_t*>(b + p.off_item_req);
+  s.ctx = reinterpret_cast<const float*>(b + p.off_ctx);
+  s.cand = reinterpret_cast<const float*>(b + p.off_cand);
+  s.action = reinterpret_cast<const uint16_t*>(b + p.off_action);
+  s.surface = reinterpret_cast<const uint8_t*>(b + p.off_surface);
+  s.emb = reinterpret_cast<const int8_t*>(b + p.off_emb);
+  s.tok_unit = c->tok_unit;
+  s.tok_rnorm = c->tok_rnorm;
+  s.cand_unit = c->cand_unit;
+  s.n_req = p.n_req;
+  s.n_items = p.n_items;
+  s.n_tok = p.n_tok;
+  s.n_tiles = p.n_tiles;
+  s.n_work = p.n_work;
+  return s;
+}
+
+int64_t staged_bytes(int R, int N, int64_t T, int tiles, int work) {
+  int64_t o = 0;
+  o = align256(o + (int64_t)R * sizeof(ReqInfo));
+  o = align256(o + (int64_t)tiles * sizeof(NNTile));
+  o = align256(o + (int64_t)work * sizeof(NNWork));
+  o = align256(o + (int64_t)N * 4);
+  o = align256(o + (int64_t)R * kCtx * 4);
+  o = align256(o + (int64_t)N * kEmbed * 4);
+  o = align256(o + T * 2);
+  o = align256(o + T);
+  o = align256(o + T * kEmbed);
+  return o;
+}
+
+int free_all(tav2_ctx* c) {
+  cudaFreeHost(c->h_arena);
+  cudaFree(c->d_staged);
+  cudaFree(c->tok_unit);
+  cudaFree(c->tok_rnorm);
+  cudaFree(c->cand_unit);
+  cudaFree(c->part);
+  cudaFree(c->idx);
+  cudaFree(c->logits);
+  cudaFree(c->skut_scratch);
+  cudaFree(c->d_params);
+  if (c->ev_staged) cudaEventDestroy(c->ev_staged);
+  for (auto& sl : c->slots) {
+    if (sl.a) cudaEventDestroy(sl.a);
+    if (sl.b) cudaEventDestroy(sl.b);
+  }
+  return 0;
+}
+
+void settle(tav2_ctx::Slot& sl) {
+  if (!sl.pending) return;
+  cudaEventSynchronize(sl.b);
+  float t = 0.f;
+  if (cudaEventElapsedTime(&t, sl.a, sl.b) == cudaSuccess) sl.ms += t;
+  sl.n++;
+  sl.pending = false;
+}
+
+// Launch `fn` (returning cudaError_t); when profiling, bracket it with events.
+template <class F>
+cudaError_t timed(tav2_ctx* c, const char* name, cudaStream_t s, F&& fn) {
+  c->launches++;
+  if (!c->profiling) return fn();
+  tav2_ctx::Slot* sl = nullptr;
+  for (auto& x : c->slots) {
+    if (x.name == name || (x.name && strcmp(x.name, name) == 0)) { sl = &x; break; }
+    if (!x.name) { x.name = name; sl = &x; break; }
+  }
+  if (!sl) return fn();
+  if (!sl->a) {
+    cudaEventCreate(&sl->a);
+    cudaEventCreate(&sl->b);
+  }
+  settle(*sl);
+  cudaEventRecord(sl->a, s);
+  cudaError_t e = fn();
+  cudaEventRecord(sl->b, s);
+  sl->pending = true;
+  return e;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tav2_last_error(void) { return g_err.c_str(); }
+
+const char* tav2_build_info(void) {
+  return "tav2 0.1.0; kernels sm_100a (tcgen05/TMA) + SIMT fp32 parity mode; C ABI include/tav2.h";
+}
+
+int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, tav2_ctx** out) {
+  if (!cfg || !cap || !out) return fail(TAV2_EINVAL, "null argument");
+  *out = nullptr;
+  const tav2_config& m = *cfg;
+  if (m.embed_dim != kEmbed || m.ffn_dim != kFfn || m.ctx_dim != kCtx || m.hidden_dim != kHidden)
+    return fail(TAV2_EINVAL,
+                "unsupported model shape on the B200 path: embed_dim=%d ffn_dim=%d ctx_dim=%d "
+                "hidden_dim=%d (need 32/32/8/64)",
+                m.embed_dim, m.ffn_dim, m.ctx_dim, m.hidden_dim);
+  if (m.num_layers < 1 || m.num_layers > kMaxLayers)
+    return fail(TAV2_EINVAL, "num_layers %d outside [1, %d]", m.num_layers, kMaxLayers);
+  if (m.action_rows < 1 || m.action_rows > 16 || m.surface_rows < 4)
+    return fail(TAV2_EINVAL, "action_rows must be 1..16 and surface_rows >= 4");
+  if (m.recent < 0 || m.k_lifelong < 0 || m.k_realtime < 0 || m.k_impression < 0)
+    return fail(TAV2_EINVAL, "segment lengths must be non-negative");  // nnsearch.py:42-44
+  int S = m.recent + m.k_lifelong + m.k_realtime + m.k_impression;
+  if (S == 0) return fail(TAV2_EINVAL, "assembled sequence length must be positive");
+  if (S != m.seq_len)
+    return fail(TAV2_EINVAL, "encoder seq_len %d must equal the assembly length %d", m.seq_len, S);
+  if (S > kMaxSeq) return fail(TAV2_EINVAL, "seq_len %d exceeds %d", S, kMaxSeq);
+  if (m.k_lifelong > kMaxK || m.k_realtime > kMaxK || m.k_impression > kMaxK)
+    return fail(TAV2_EINVAL, "per-segment k exceeds %d", kMaxK);
+  if (cap->max_requests < 1 || cap->max_items < 1 || cap->max_tokens < 0)
+    return fail(TAV2_EINVAL, "invalid capacity");
+
+  tav2_ctx* c = new tav2_ctx();
+  c->cfg = m;
+  c->cap = *cap;
+  c->device = device;
+  c->nn.recent = m.recent;
+  c->nn.k[0] = m.k_lifelong;
+  c->nn.k[1] = m.k_realtime;
+  c->nn.k[2] = m.k_impression;
+  c->nn.seg_start[0] = 0;
+  c->nn.seg_start[1] = m.k_lifelong;
+  c->nn.seg_start[2] = m.k_lifelong + m.recent;
+  c->nn.seg_start[3] = m.k_lifelong + m.recent + m.k_realtime;
+  c->nn.seq_len = S;
+  c->kmax = std::max(1, std::max(m.k_lifelong, std::max(m.k_realtime, m.k_impression)));
+  const int R = cap->max_requests, N = cap->max_items;
+  const int64_t T = cap->max_tokens;
+  c->max_tiles = R + cdiv(N, kTile);
+  c->max_work = 3 * c->max_tiles + kTargetWork;
+  c->staged_cap = staged_bytes(R, N, T, c->max_tiles, c->max_work);
+
+  auto bad = [&](cudaError_t e, const char* what) {
+    fail(TAV2_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+    free_all(c);
+    delete c;
+    return TAV2_ECUDA;
+  };
+  cudaError_t e;
+  if ((e = cudaSetDevice(device)) != cudaSuccess) return bad(e, "cudaSetDevice");
+  if ((e = cudaMallocHost(&c->h_arena, c->staged_cap)) != cudaSuccess) return bad(e, "pinned arena");
+  if ((e = cudaMalloc(&c->d_staged, c->staged_cap)) != cudaSuccess) return bad(e, "staged region");
+  if ((e = cudaMalloc(&c->tok_unit, std::max<int64_t>(T, 1) * kEmbed * 4)) != cudaSuccess)
+    return bad(e, "tok_unit");
+  if ((e = cudaMalloc(&c->tok_rnorm, std::max<int64_t>(T, 1) * 8)) != cudaSuccess) return bad(e, "tok_rnorm");
+  if ((e = cudaMalloc(&c->cand_unit, (size_t)N * kEmbed * 4)) != cudaSuccess) return bad(e, "cand_unit");
+  if ((e = cudaMalloc(&c->part, (size_t)c->max_work * c->kmax * kTile * 8)) != cudaSuccess)
+    return bad(e, "partial top-k");
+  if ((e = cudaMalloc(&c->idx, (size_t)N * S * 4)) != cudaSuccess) return bad(e, "idx");
+  if ((e = cudaMalloc(&c->logits, (size_t)N * kHeads * 4)) != cudaSuccess) return bad(e, "logits");
+  {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    size_t n = (size_t)sms * skut_simt_scratch_floats(S);
+    if ((e = cudaMalloc(&c->skut_scratch, n * 4)) != cudaSuccess) return bad(e, "skut scratch");
+  }
+  if ((e = cudaEventCreateWithFlags(&c->ev_staged, cudaEventDisableTiming)) != cudaSuccess)
+    return bad(e, "event");
+  *out = c;
+  return TAV2_OK;
+}
+
+int tav2_destroy(tav2_ctx* c) {
+  if (!c) return TAV2_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  free_all(c);
+  delete c;
+  return TAV2_OK;
+}
+
+int tav2_load_params(tav2_ctx* c, int n, const char* const* names, const float* const* data,
+                     const int64_t* numel) {
+  if (!c || (n > 0 && (!names || !data || !numel))) return fail(TAV2_EINVAL, "null argument");
+  const tav2_config& m = c->cfg;
+  const int d = kDModel;
+  struct Want {
+    std::string name;
+    int64_t numel;
+    const float** slot;
+  };
+  Params P{};
+  P.num_layers = m.num_layers;
+  P.seq_len = m.seq_len;
+  P.action_rows = m.action_rows;
+  P.surface_rows = m.surface_rows;
+  std::vector<Want> want = {
+      {"encoder.action_table", (int64_t)m.action_rows * d, &P.action_table},
+      {"encoder.surface_table", (int64_t)m.surface_rows * d, &P.surface_table},
+      {"encoder.position_table", (int64_t)m.seq_len * d, &P.position_table},
+      {"encoder.out_linear", (int64_t)d * d, &P.out_linear},
+      {"head.w1", (int64_t)(d + kEmbed + kCtx) * kHidden, &P.head_w1},
+      {"head.b1", kHidden, &P.head_b1},
+      {"head.w2", (int64_t)kHidden * kHeads, &P.head_w2},
+      {"head.b2", kHeads, &P.head_b2},
+  };
+  for (int L = 0; L < m.num_layers; ++L) {
+    std::string p = "encoder.layer" + std::to_string(L) + ".";
+    want.push_back({p + "wq", d * d, &P.wq[L]});
+    want.push_back({p + "wk", d * d, &P.wk[L]});
+    want.push_back({p + "wv", d * d, &P.wv[L]});
+    want.push_back({p + "wo", d * d, &P.wo[L]});
+    want.push_back({p + "w1", d * kFfn, &P.w1[L]});
+    want.push_back({p + "w2", kFfn * d, &P.w2[L]});
+    want.push_back({p + "ln1_scale", d, &P.ln1_scale[L]});
+    want.push_back({p + "ln1_shift", d, &P.ln1_shift[L]});
+    want.push_back({p + "ln2_scale", d, &P.ln2_scale[L]});
+    want.push_back({p + "ln2_shift", d, &P.ln2_shift[L]});
+  }
+  int64_t total = 0;
+  std::vector<int> src(want.size(), -1);
+  std::vector<int64_t> off(want.size());
+  for (size_t w = 0; w < want.size(); ++w) {
+    for (int i = 0; i < n; ++i)
+      if (names[i] && want[w].name == names[i]) src[w] = i;
+    if (src[w] < 0) return fail(TAV2_EINVAL, "missing parameter tensor '%s'", want[w].name.c_str());
+    if (numel[src[w]] != want[w].numel)
+      return fail(TAV2_EINVAL, "parameter '%s' has %lld elements, expected %lld",
+                  want[w].name.c_str(), (long long)numel[src[w]], (long long)want[w].numel);
+    off[w] = total;
+    total += (want[w].numel + 63) & ~int64_t(63);  // 256-byte aligned tensors
+  }
+  CU(cudaSetDevice(c->device));
+  if (c->d_params) {
+    CU(cudaDeviceSynchronize());
+    cudaFree(c->d_params);
+    c->d_params = nullptr;
+  }
+  CU(cudaMalloc(&c->d_params, total * 4));
+  std::vector<float> host(total, 0.0f);
+  for (size_t w = 0; w < want.size(); ++w) {
+    memcpy(host.data() + off[w], data[src[w]], want[w].numel * 4);
+    *want[w].slot = c->d_params + off[w];
+  }
+  CU(cudaMemcpy(c->d_params, host.data(), total * 4, cudaMemcpyHostToDevice));
+  c->params = P;
+  c->params_ok = true;
+  return TAV2_OK;
+}
+
+int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, int32_t* n_items) {
+  if (!c || !reqs) return fail(TAV2_EINVAL, "null argument");
+  if (n_req < 1) return fail(TAV2_EINVAL, "at least one request required");  // nnsearch.py:221
+  if (n_req > c->cap.max_requests)
+    return fail(TAV2_ECAP, "%d requests exceed capacity %d", n_req, c->cap.max_requests);
+  cudaStream_t s = (cudaStream_t)stream;
+  const NNCfg& nn = c->nn;
+  int N = 0;
+  int64_t T = 0;
+  int tiles = 0;
+  for (int r = 0; r < n_req; ++r) {
+    const tav2_request& q = reqs[r];
+    if (q.n_cand < 1 || !q.candidates)
+      return fail(TAV2_EINVAL, "each request needs a non-empty (M, E) candidate array");
+    for (int k = 0; k < 3; ++k) {
+      if (q.len[k] < 0 || q.len[k] > kCaps[k])
+        return fail(TAV2_EINVAL, "request %d source %d length %d outside [0, %d]", r, k, q.len[k],
+                    kCaps[k]);
+      if (q.len[k] > 0 && (!q.emb[k] || !q.action[k] || !q.surface[k]))
+        return fail(TAV2_EINVAL, "request %d source %d has null columns", r, k);
+    }
+    N += q.n_cand;
+    T += (int64_t)q.len[0] + q.len[1] + q.len[2];
+    tiles += cdiv(q.n_cand, kTile);
+  }
+  if (N > c->cap.max_items) return fail(TAV2_ECAP, "%d items exceed capacity %d", N, c->cap.max_items);
+  if (T > c->cap.max_tokens)
+    return fail(TAV2_ECAP, "%lld tokens exceed capacity %lld", (long long)T, (long long)c->cap.max_tokens);
+
+  // ---- NN work decomposition: LL chunks sized so the grid fills the GPU ----
+  const int ll_chunks_target = std::max(1, cdiv(kTargetWork, std::max(tiles, 1)));
+  std::vector<NNTile> vt;
+  std::vector<NNWork> vw;
+  vt.reserve(tiles);
+  {
+    int item = 0;
+    for (int r = 0; r < n_req; ++r) {
+      const tav2_request& q = reqs[r];
+      for (int i0 = 0; i0 < q.n_cand; i0 += kTile) {
+        NNTile t{};
+        t.req = r;
+        t.item0 = item + i0;
+        t.n = std::min(kTile, q.n_cand - i0);
+        const int tid = (int)vt.size();
+        for (int s = 0; s < 3; ++s) {
+          int lo = s == 1 ? nn.recent : 0;
+          int hi = q.len[s];
+          t.work0[s] = (int)vw.size();
+          t.nwork[s] = 0;
+          if (nn.k[s] == 0 || hi <= lo) continue;
+          int nch = s == 0 ? std::min(ll_chunks_target, std::max(1, cdiv(hi - lo, kMinChunk))) : 1;
+          int step = cdiv(hi - lo, nch);
+          for (int a = lo; a < hi; a += step) {
+            vw.push_back(NNWork{tid, s, a, std::min(hi, a + step)});
+            t.nwork[s]++;
+          }
+        }
+        vt.push_back(t);
+      }
+      item += q.n_cand;
+    }
+  }
+  if ((int)vt.size() > c->max_tiles || (int)vw.size() > c->max_work)
+    return fail(TAV2_ECAP, "NN plan (%zu tiles, %zu work) exceeds capacity", vt.size(), vw.size());
+
+  Plan p{};
+  p.n_req = n_req;
+  p.n_items = N;
+  p.n_tok = (int32_t)T;
+  p.n_tiles = (int)vt.size();
+  p.n_work = (int)vw.size();
+  p.tile_size = kTile;
+  int64_t o = 0;
+  p.off_req = o; o = align256(o + (int64_t)n_req * sizeof(ReqInfo));
+  p.off_tiles = o; o = align256(o + (int64_t)p.n_tiles * sizeof(NNTile));
+  p.off_work = o; o = align256(o + (int64_t)p.n_work * sizeof(NNWork));
+  p.off_item_req = o; o = align256(o + (int64_t)N * 4);
+  p.off_ctx = o; o = align256(o + (int64_t)n_req * kCtx * 4);
+  p.off_cand = o; o = align256(o + (int64_t)N * kEmbed * 4);
+  p.off_action = o; o = align256(o + T * 2);
+  p.off_surface = o; o = align256(o + T);
+  p.off_emb = o; o = align256(o + T * kEmbed);
+  p.bytes = o;
+
+  // The arena is reused: the previous batch's H2D copy must have drained
+  // before we overwrite it (arena reset contract, arena.py:49-55).
+  CU(cudaEventSynchronize(c->ev_staged));
+  unsigned char* h = c->h_arena;
+  ReqInfo* ri = reinterpret_cast<ReqInfo*>(h + p.off_req);
+  int32_t* item_req = reinterpret_cast<int32_t*>(h + p.off_item_req);
+  float* ctx = reinterpret_cast<float*>(h + p.off_ctx);
+  float* cand = reinterpret_cast<float*>(h + p.off_cand);
+  uint16_t* act = reinterpret_cast<uint16_t*>(h + p.off_action);
+  uint8_t* surf = h + p.off_surface;
+  int8_t* emb = reinterpret_cast<int8_t*>(h + p.off_emb);
+  int item = 0;
+  int64_t tok = 0;
+  for (int r = 0; r < n_req; ++r) {
+    const tav2_request& q = reqs[r];
+    ri[r].item_off = item;
+    ri[r].n_items = q.n_cand;
+    for (int s = 0; s < 3; ++s) {
+      ri[r].tok_off[s] = (int32_t)tok;
+      ri[r].len[s] = q.len[s];
+      if (q.len[s]) {
+        memcpy(emb + tok * kEmbed, q.emb[s], (size_t)q.len[s] * kEmbed);
+        memcpy(act + tok, q.action[s], (size_t)q.len[s] * 2);
+        memcpy(surf + tok, q.surface[s], (size_t)q.len[s]);
+      }
+      tok += q.len[s];
+    }
+    memcpy(cand + (int64_t)item * kEmbed, q.candidates, (size_t)q.n_cand * kEmbed * 4);
+    for (int i = 0; i < q.n_cand; ++i) item_req[item + i] = r;
+    if (q.ctx)
+      memcpy(ctx + r * kCtx, q.ctx, kCtx * 4);
+    else
+      memset(ctx + r * kCtx, 0, kCtx * 4);
+    item += q.n_cand;
+  }
+  if (!vt.empty()) memcpy(h + p.off_tiles, vt.data(), vt.size() * sizeof(NNTile));
+  if (!vw.empty()) memcpy(h + p.off_work, vw.data(), vw.size() * sizeof(NNWork));
+
+  CU(cudaSetDevice(c->device));
+  CU(cudaMemcpyAsync(c->d_staged, h, p.bytes, cudaMemcpyHostToDevice, s));
+  CU(cudaEventRecord(c->ev_staged, s));
+  c->plan = p;
+  c->staged = true;
+  if (n_items) *n_items = N;
+  return TAV2_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int check_ready(tav2_ctx* c, int mode) {
+  if (!c) return fail(TAV2_EINVAL, "null context");
+  if (!c->staged) return fail(TAV2_ESTATE, "no staged batch: call tav2_stage first");
+  if (mode != TAV2_MODE_FP32 && mode != TAV2_MODE_BF16)
+    return fail(TAV2_EINVAL, "unknown precision mode %d", mode);
+  return TAV2_OK;
+}
+
+int run_nn(tav2_ctx* c, int mode, int32_t* idx, float* scores, cudaStream_t s) {
+  Staged st = staged_view(c);
+  CU(timed(c, "prep", s, [&] { return launch_prep(st, s); }));
+  if (mode == TAV2_MODE_FP32) {
+    CU(timed(c, "nn_simt", s, [&] { return launch_nn_simt(st, c->nn, c->part, c->kmax, kTile, s); }));
+  } else {
+    CU(timed(c, "nn_tc", s, [&] { return launch_nn_tc(st, c->nn, c->part, c->kmax, s); }));
+  }
+  CU(timed(c, "nn_merge", s,
+           [&] { return launch_nn_merge(st, c->nn, c->part, c->kmax, kTile, idx, scores, s); }));
+  return TAV2_OK;
+}
+
+int run_score(tav2_ctx* c, int mode, const int32_t* idx, float* logits, float* pooled,
+              cudaStream_t s) {
+  if (!c->params_ok) return fail(TAV2_ESTATE, "parameters not loaded");
+  Staged st = staged_view(c);
+  (void)mode;
+  CU(timed(c, "skut_simt", s, [&] {
+    return launch_skut_simt(c->params, c->nn, &st, idx, nullptr, nullptr, st.n_items,
+                            c->skut_scratch, nullptr, logits, pooled, s);
+  }));
+  return TAV2_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tav2_nn_select(tav2_ctx* c, int mode, int32_t* idx_dev, float* scores_dev, void* stream) {
+  int rc = check_ready(c, mode);
+  if (rc) return rc;
+  if (!idx_dev) return fail(TAV2_EINVAL, "idx_dev is null");
+  CU(cudaSetDevice(c->device));
+  c->launches = 0;
+  return run_nn(c, mode, idx_dev, scores_dev, (cudaStream_t)stream);
+}
+
+int tav2_encode(tav2_ctx* c, const int32_t* idx_dev, float* features_dev, uint8_t* mask_dev,
+                void* stream) {
+  int rc = check_ready(c, TAV2_MODE_FP32);
+  if (rc) return rc;
+  if (!c->params_ok) return fail(TAV2_ESTATE, "parameters not loaded");
+  if (!idx_dev || !features_dev || !mask_dev) return fail(TAV2_EINVAL, "null device pointer");
+  CU(cudaSetDevice(c->device));
+  Staged st = staged_view(c);
+  CU(launch_prep(st, (cudaStream_t)stream));
+  CU(launch_encode(st, c->nn, c->params, idx_dev, features_dev, mask_dev, (cudaStream_t)stream));
+  return TAV2_OK;
+}
+
+int tav2_forward(tav2_ctx* c, int mode, const float* features_dev, const uint8_t* mask_dev,
+                 int32_t n, float* u_dev, void* stream) {
+  if (!c) return fail(TAV2_EINVAL, "null context");
+  if (!c->params_ok) return fail(TAV2_ESTATE, "parameters not loaded");
+  if (mode != TAV2_MODE_FP32 && mode != TAV2_MODE_BF16)
+    return fail(TAV2_EINVAL, "unknown precision mode %d", mode);
+  if (n < 0) return fail(TAV2_EINVAL, "negative batch");
+  if (n == 0) return TAV2_OK;
+  if (!features_dev || !mask_dev || !u_dev) return fail(TAV2_EINVAL, "null device pointer");
+  CU(cudaSetDevice(c->device));
+  CU(launch_skut_simt(c->params, c->nn, nullptr, nullptr, features_dev, mask_dev, n,
+                      c->skut_scratch, u_dev, nullptr, nullptr, (cudaStream_t)stream));
+  return TAV2_OK;
+}
+
+int tav2_score(tav2_ctx* c, int mode, const int32_t* idx_dev, float* logits_dev, float* pooled_dev,
+               void* stream) {
+  int rc = check_ready(c, mode);
+  if (rc) return rc;
+  if (!idx_dev || !logits_dev) return fail(TAV2_EINVAL, "null device pointer");
+  CU(cudaSetDevice(c->device));
+  c->launches = 0;
+  Staged st = staged_view(c);
+  CU(timed(c, "prep", (cudaStream_t)stream, [&] { return launch_prep(st, (cudaStream_t)stream); }));
+  return run_score(c, mode, idx_dev, logits_dev, pooled_dev, (cudaStream_t)stream);
+}
+
+int tav2_run_staged(tav2_ctx* c, int mode, float* logits_dev, void* stream) {
+  int rc = check_ready(c, mode);
+  if (rc) return rc;
+  CU(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  c->launches = 0;
+  if ((rc = run_nn(c, mode, c->idx, nullptr, s))) return rc;
+  return run_score(c, mode, c->idx, logits_dev ? logits_dev : c->logits, nullptr, s);
+}
+
+int tav2_rank(tav2_ctx* c, const tav2_request* reqs, int n_req, int mode, float* logits_host,
+              int32_t* idx_host, void* stream) {
+  if (!logits_host) return fail(TAV2_EINVAL, "logits_host is null");
+  int32_t n = 0;
+  int rc = tav2_stage(c, reqs, n_req, stream, &n);
+  if (rc) return rc;
+  if ((rc = tav2_run_staged(c, mode, c->logits, stream))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  CU(cudaMemcpyAsync(logits_host, c->logits, (size_t)n * kHeads * 4, cudaMemcpyDeviceToHost, s));
+  if (idx_host)
+    CU(cudaMemcpyAsync(idx_host, c->idx, (size_t)n * c->nn.seq_len * 4, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return TAV2_OK;
+}
+
+int tav2_last_launch_count(const tav2_ctx* c) { return c ? c->launches : 0; }
+
+int tav2_set_profiling(tav2_ctx* c, int on) {
+  if (!c) return fail(TAV2_EINVAL, "null context");
+  for (auto& sl : c->slots) {
+    settle(sl);
+    sl.ms = 0.0;
+    sl.n = 0;
+  }
+  c->profiling = on != 0;
+  return TAV2_OK;
+}
+
+int tav2_kernel_times(tav2_ctx* c, const char** names, double* ms, int32_t* launches, int max) {
+  if (!c) return fail(TAV2_EINVAL, "null context");
+  int k = 0;
+  for (auto& sl : c->slots) {
+    if (!sl.name) continue;
+    settle(sl);
+    if (k < max) {
+      if (names) names[k] = sl.name;
+      if (ms) ms[k] = sl.ms;
+      if (launches) launches[k] = sl.n;
+    }
+    ++k;
+  }
+  return k;
+}
+
+}  // extern "C"

@@ -1,0 +1,204 @@
+// Shared device/host definitions for the tav2 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tav2.h"
+
+namespace tav2 {
+
+constexpr int kEmbed = 32;      // EMBED_DIM (core.py:10)
+constexpr int kDModel = 64;     // 2 * embed (encoder.py:38)
+constexpr int kFfn = 32;        // EncoderConfig.ffn_dim
+constexpr int kCtx = 8;         // ModelConfig.ctx_dim
+constexpr int kHidden = 64;     // ModelConfig.hidden_dim
+constexpr int kHeads = 4;       // NUM_HEADS (dataset.py:36)
+constexpr int kMaxSeq = 384;    // S = recent + k_ll + k_rt + k_imp
+constexpr int kMaxLayers = 8;
+constexpr int kMaxK = 256;      // per-segment k (SURVEY C5 sweep)
+constexpr int kIdxBits = 14;    // LIFELONG_CAP = 16384 (core.py:31)
+constexpr uint64_t kIdxMask = (1ull << kIdxBits) - 1;
+
+// ---------------------------------------------------------------------------
+// Per-batch staging plan.  The pinned host arena and the device staged
+// region share this byte layout so staging is ONE contiguous H2D copy.
+// ---------------------------------------------------------------------------
+struct ReqInfo {          // one unique request (DedupBatch.users entry)
+  int32_t tok_off[3];     // first token of LL / RT / IMP in the token arena
+  int32_t len[3];         // source lengths
+  int32_t item_off;       // first item (candidate) of this request
+  int32_t n_items;
+};
+
+struct NNWork {           // one (candidate tile, source, token chunk) unit
+  int32_t tile;           // candidate tile id
+  int32_t source;         // 0 = LL, 1 = RT tail (RT[r:]), 2 = IMP
+  int32_t t0, t1;         // token range, source-relative (RT tail: RT index)
+};
+
+struct NNTile {           // up to kTile consecutive items of one request
+  int32_t req;
+  int32_t item0;
+  int32_t n;
+  int32_t work0[3];       // first work unit of each source for this tile
+  int32_t nwork[3];       // number of chunks per source
+};
+
+struct Plan {
+  int32_t n_req, n_items, n_tok;
+  int32_t n_tiles, n_work, tile_size;
+  // byte offsets inside the staged region
+  int64_t off_req, off_tiles, off_work, off_item_req, off_ctx, off_cand, off_action,
+      off_surface, off_emb, bytes;
+};
+
+// Device view of the model parameters (all f32, reference names in
+// comments; layouts exactly as the reference arrays, row-major [in, out]).
+struct Params {
+  int32_t num_layers, seq_len, action_rows, surface_rows;
+  const float* action_table;    // encoder.action_table   [A, 64]
+  const float* surface_table;   // encoder.surface_table  [256, 64] (rows 0..3 used)
+  const float* position_table;  // encoder.position_table [S, 64]
+  const float* out_linear;      // encoder.out_linear     [64, 64]
+  const float* wq[kMaxLayers];  // encoder.layerI.wq      [64, 64]
+  const float* wk[kMaxLayers];
+  const float* wv[kMaxLayers];
+  const float* wo[kMaxLayers];
+  const float* w1[kMaxLayers];  // [64, 32]
+  const float* w2[kMaxLayers];  // [32, 64]
+  const float* ln1_scale[kMaxLayers];
+  const float* ln1_shift[kMaxLayers];
+  const float* ln2_scale[kMaxLayers];
+  const float* ln2_shift[kMaxLayers];
+  const float* head_w1;  // head.w1 [104, 64]
+  const float* head_b1;  // head.b1 [64]
+  const float* head_w2;  // head.w2 [64, 4]
+  const float* head_b2;  // head.b2 [4]
+};
+
+struct NNCfg {
+  int32_t recent, k[3];       // k[0] = k_ll, k[1] = k_rt, k[2] = k_imp
+  int32_t seg_start[4];       // layout starts: NN_LL, RT_recent, NN_RT_tail, NN_IMP
+  int32_t seq_len;
+};
+
+// Staged batch, device side.
+struct Staged {
+  const ReqInfo* req;
+  const NNTile* tiles;
+  const NNWork* work;
+  const int32_t* item_req;
+  const float* ctx;        // [R, 8]
+  const float* cand;       // [N, 32]
+  const uint16_t* action;  // [T]
+  const uint8_t* surface;  // [T]
+  const int8_t* emb;       // [T, 32]
+  float* tok_unit;         // [T, 32] derived: unit(dequantize(q)) (core.py:77-79)
+  double* tok_rnorm;       // [T]     derived: 2^-27 / ||q||_2 of the int8 row (i8-limb path)
+  float* cand_unit;        // [N, 32] derived: l2_normalize_rows(cand)
+  int n_req, n_items, n_tok, n_tiles, n_work;
+};
+
+// ---------------------------------------------------------------------------
+// Top-k keys: larger key == better.  High bits: order-preserving image of
+// the f64 score truncated to 50 bits; low 14 bits: (2^14-1 - idx) so that on
+// equal scores the lower storage index wins (argsort stable, nnsearch.py:361).
+// ---------------------------------------------------------------------------
+__host__ __device__ inline uint64_t score_key(double s, int idx) {
+  s = s + 0.0;  // -0.0 -> +0.0 so zero scores tie exactly like the reference
+  uint64_t u;
+#ifdef __CUDA_ARCH__
+  u = (uint64_t)__double_as_longlong(s);
+#else
+  memcpy(&u, &s, 8);
+#endif
+  u = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+  return (u & ~kIdxMask) | (kIdxMask - (uint64_t)idx);
+}
+__host__ __device__ inline int key_index(uint64_t key) { return (int)(kIdxMask - (key & kIdxMask)); }
+__host__ __device__ inline double key_score(uint64_t key) {
+  uint64_t u = key & ~kIdxMask;
+  u = (u >> 63) ? (u & 0x7FFFFFFFFFFFFFFFull) : ~u;
+  double s;
+#ifdef __CUDA_ARCH__
+  s = __longlong_as_double((long long)u);
+#else
+  memcpy(&s, &u, 8);
+#endif
+  return s;
+}
+
+// Min-heap of `k` keys stored with stride `ld` (struct-of-arrays across the
+// threads of a block so concurrent per-thread heaps are bank-conflict free).
+__device__ __forceinline__ void heap_replace_root(uint64_t* h, int ld, int k, uint64_t key) {
+  int i = 0;
+  while (true) {
+    int l = 2 * i + 1;
+    if (l >= k) break;
+    int r = l + 1;
+    uint64_t lv = h[l * ld];
+    int c = l;
+    uint64_t cv = lv;
+    if (r < k) {
+      uint64_t rv = h[r * ld];
+      if (rv < lv) { c = r; cv = rv; }
+    }
+    if (cv >= key) break;
+    h[i * ld] = cv;
+    i = c;
+  }
+  h[i * ld] = key;
+}
+
+// Max-heap sift on u32 values (used to order the final picks by index).
+__device__ __forceinline__ void heap_sift_u32(int32_t* a, int ld, int n, int i) {
+  int32_t v = a[i * ld];
+  while (true) {
+    int l = 2 * i + 1;
+    if (l >= n) break;
+    int r = l + 1;
+    int c = l;
+    int32_t cv = a[l * ld];
+    if (r < n) {
+      int32_t rv = a[r * ld];
+      if (rv > cv) { c = r; cv = rv; }
+    }
+    if (cv <= v) break;
+    a[i * ld] = cv;
+    i = c;
+  }
+  a[i * ld] = v;
+}
+
+// ascending in-place heapsort of n values with stride ld
+__device__ __forceinline__ void heapsort_u32(int32_t* a, int ld, int n) {
+  for (int i = n / 2 - 1; i >= 0; --i) heap_sift_u32(a, ld, n, i);
+  for (int e = n - 1; e > 0; --e) {
+    int32_t t = a[0];
+    a[0] = a[e * ld];
+    a[e * ld] = t;
+    heap_sift_u32(a, ld, e, 0);
+  }
+}
+
+}  // namespace tav2
+
+// Host-side launchers (defined in the kernel translation units).
+namespace tav2 {
+cudaError_t launch_prep(const Staged& st, cudaStream_t s);
+cudaError_t launch_nn_simt(const Staged& st, const NNCfg& nn, uint64_t* part, int kmax,
+                           int tile_size, cudaStream_t s);
+cudaError_t launch_nn_tc(const Staged& st, const NNCfg& nn, uint64_t* part, int kmax,
+                         cudaStream_t s);
+cudaError_t launch_nn_merge(const Staged& st, const NNCfg& nn, const uint64_t* part, int kmax,
+                            int tile_size, int32_t* idx, float* scores, cudaStream_t s);
+cudaError_t launch_encode(const Staged& st, const NNCfg& nn, const Params& p, const int32_t* idx,
+                          float* F, uint8_t* mask, cudaStream_t s);
+cudaError_t launch_skut_simt(const Params& p, const NNCfg& nn, const Staged* st,
+                             const int32_t* idx, const float* F, const uint8_t* fmask, int n,
+                             float* scratch, float* U, float* logits, float* pooled,
+                             cudaStream_t s);
+int skut_simt_grid(int n);
+size_t skut_simt_scratch_floats(int seq_len);
+}  // namespace tav2

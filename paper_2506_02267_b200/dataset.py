@@ -1,0 +1,93 @@
+"""Head names, request context features and a vectorised synthetic request
+generator with the structure of ``seqrank.dataset.generate_synthetic``
+(dataset.py:297-427): per-user interest clusters, 15% HIDE tokens from
+foreign clusters, 10% multi-hot positives, impressions 75% foreign, unit
+f32 candidates half near / half far.  Values differ from the reference's
+per-token Python loop (this one is ~1000x faster); the distribution is the
+same, which is all the benchmark needs.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .core import CLICK, CLOSEUP, EMBED_DIM, HIDE, IMPRESSION, REPIN, TokenBlock, UserSequences, quantize
+
+HEAD_NAMES = ("repin", "click", "closeup", "hide")
+NUM_HEADS = len(HEAD_NAMES)
+
+_LL_BASE_TS = 1_700_000_000
+_RT_BASE_TS = 1_750_000_000
+
+
+def context_features(user_id: int, dim: int = 8) -> np.ndarray:
+    """Deterministic request context in [-1, 1] (dataset.py:282-289)."""
+    rng = np.random.default_rng([int(user_id), 96321])
+    return rng.uniform(-1.0, 1.0, dim).astype(np.float32)
+
+
+@dataclass
+class SyntheticRequest:
+    user_id: int
+    user: UserSequences
+    candidates: np.ndarray  # (n, 32) f32 unit rows
+    ctx: np.ndarray         # (8,) f32
+
+
+def _unit(x: np.ndarray) -> np.ndarray:
+    n = np.linalg.norm(x, axis=-1, keepdims=True).astype(np.float32)
+    return (x / np.where(n == 0, 1, n)).astype(np.float32)
+
+
+def _noisy(rng, centroids, which, sigma=0.08):
+    return _unit(centroids[which] + rng.normal(0.0, sigma, (len(which), EMBED_DIM)).astype(np.float32))
+
+
+def _engagement(rng, n, near, far, base_ts, step) -> TokenBlock:
+    ts = (base_ts - np.arange(n, dtype=np.int64) * step).astype(np.uint32)
+    surf = rng.integers(0, 4, n).astype(np.uint8)
+    hide = rng.random(n) < 0.15
+    pos = rng.choice(np.array([REPIN, CLICK, CLOSEUP], np.uint16), n)
+    extra = np.where(rng.random(n) < 0.1, rng.choice(np.array([REPIN, CLOSEUP], np.uint16), n), 0)
+    act = np.where(hide, HIDE, pos | extra).astype(np.uint16)
+    emb = np.where(hide[:, None], far(n), near(n))
+    return TokenBlock(ts, act, surf, quantize(emb))
+
+
+def _impressions(rng, n, near, far) -> TokenBlock:
+    ts = (_RT_BASE_TS + 30 - np.arange(n, dtype=np.int64) * 60).astype(np.uint32)
+    surf = rng.integers(0, 4, n).astype(np.uint8)
+    emb = np.where((rng.random(n) < 0.75)[:, None], far(n), near(n))
+    return TokenBlock(ts, np.full(n, IMPRESSION, np.uint16), surf, quantize(emb))
+
+
+def generate_requests(num_requests: int, n_candidates: int, ll_tokens: int = 16384,
+                      rt_tokens: int = 256, imp_tokens: int = 256, num_clusters: int = 8,
+                      seed: int = 0) -> list[SyntheticRequest]:
+    """Synthetic serving requests: one user + N candidates each."""
+    rng = np.random.default_rng(seed)
+    centroids = _unit(rng.normal(0.0, 1.0, (num_clusters, EMBED_DIM)).astype(np.float32))
+    out = []
+    for r in range(num_requests):
+        uid = r + 1
+        k = int(rng.integers(1, min(3, num_clusters) + 1))
+        interests = rng.choice(num_clusters, k, replace=False)
+        foreign = np.setdiff1d(np.arange(num_clusters), interests)
+
+        def near(n, _i=interests):
+            return _noisy(rng, centroids, rng.choice(_i, n))
+
+        def far(n, _f=foreign):
+            if len(_f) == 0:
+                return _unit(rng.normal(0, 1, (n, EMBED_DIM)).astype(np.float32))
+            return _noisy(rng, centroids, rng.choice(_f, n))
+
+        user = UserSequences(_engagement(rng, ll_tokens, near, far, _LL_BASE_TS, 3600),
+                             _engagement(rng, rt_tokens, near, far, _RT_BASE_TS, 60),
+                             _impressions(rng, imp_tokens, near, far))
+        is_near = rng.random(n_candidates) < 0.5
+        cands = np.where(is_near[:, None], near(n_candidates), far(n_candidates)).astype(np.float32)
+        out.append(SyntheticRequest(uid, user, np.ascontiguousarray(cands), context_features(uid)))
+    return out

@@ -1,0 +1,184 @@
+"""GPU parity: the native path against the reference golden vectors and the
+CPU oracle on identical seeded inputs (north_star tolerances):
+
+* NN index sets identical except ties within 1e-6 of the k-th score, order
+  descending storage index;
+* logits within 1e-5 abs in fp32 mode, within 2e-3 abs in bf16 mode.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2506_02267_b200 as P  # noqa: E402
+from paper_2506_02267_b200 import serving  # noqa: E402
+from paper_2506_02267_b200.runtime import Capacity, Engine  # noqa: E402
+from conftest import golden_cases, load_case  # noqa: E402
+from helpers import check_nn_contract, from_user, to_user  # noqa: E402
+from oracle import seqrank_oracle as orc  # noqa: E402
+
+TOL = {"fp32": 1e-5, "bf16": 2e-3}
+MODES = ["fp32", "bf16"]
+
+
+def _engine_for(nn, seed=0, cap=Capacity(8, 2048, 8 * 16896)):
+    model = P.RankingModel.init(P.ModelConfig.for_nn(nn), seed=seed)
+    return Engine(model, capacity=cap)
+
+
+def _golden(case):
+    z, reqs = load_case(case)
+    nn = P.NNConfig(*[int(v) for v in z["cfg"]])
+    return z, reqs, nn
+
+
+def _ref_scores_fn(reqs, offsets, cands, nn):
+    def fn(i, g, idx):
+        u = reqs[offsets[i]]["user"]
+        src = {0: "ll", 2: "rt", 3: "imp"}[g]
+        return orc.similarity_scores(u[f"{src}_emb"], cands[i])[idx]
+    return fn
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("case", golden_cases())
+def test_golden_nn_indices(case, mode):
+    z, reqs, nn = _golden(case)
+    eng = _engine_for(nn)
+    batch = P.build_dedup_batch([(to_user(r["user"]), r["cands"], None) for r in reqs])
+    idx = eng.nn_select(batch, mode=mode)
+    check_nn_contract(idx, z["idx"], _ref_scores_fn(reqs, z["offsets"], z["candidates"], nn),
+                      z["kth"], nn.segment_starts(), nn.segment_lengths())
+    # recent real-time segment is verbatim RT[:r] reversed
+    a, b = nn.segment_starts()[1], nn.segment_starts()[1] + nn.recent
+    assert np.array_equal(idx[:, a:b], z["idx"][:, a:b])
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("case", golden_cases())
+def test_golden_logits(case, mode):
+    z, reqs, nn = _golden(case)
+    eng = _engine_for(nn)
+    logits = eng.rank_requests([(to_user(r["user"]), r["cands"], r["ctx"]) for r in reqs], mode=mode)
+    err = np.abs(logits - z["logits"]).max()
+    assert err <= TOL[mode], f"{case}/{mode}: max |dlogit| = {err:.3g}"
+
+
+@pytest.mark.parametrize("case", golden_cases())
+def test_golden_encode(case):
+    z, reqs, nn = _golden(case)
+    eng = _engine_for(nn)
+    users = [to_user(r["user"]) for r in reqs]
+    seqs = [P.nnsearch.assembled_from_indices(users[o], z["idx"][i], nn)
+            for i, o in enumerate(z["offsets"][:4])]
+    F, mask = eng.encode(seqs, z["candidates"][:4])
+    assert np.array_equal(mask, z["mask"][:4])
+    np.testing.assert_allclose(F, z["features_head"], atol=1e-6, rtol=0)
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("case", golden_cases())
+def test_golden_forward(case, mode):
+    z, _, nn = _golden(case)
+    eng = _engine_for(nn)
+    U = eng.forward(z["features_head"], z["mask"][:4], mode=mode)
+    m = z["mask"][:4, :, None]
+    err = np.abs((U - z["U_head"]) * m).max()
+    assert err <= (2e-5 if mode == "fp32" else 5e-3), err
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_seeded_vs_oracle_medium(mode):
+    """Fresh seeded requests (not in the fixtures), compared with the oracle."""
+    nn = P.NNConfig()
+    reqs = P.generate_requests(3, 150, ll_tokens=4096, seed=11)
+    eng = _engine_for(nn, seed=2)
+    Pd = orc.model_init(2, seq_len=nn.seq_len)
+    logits, idx = eng.rank_requests([(r.user, r.candidates, r.ctx) for r in reqs], mode=mode,
+                                    return_indices=True)
+    row = 0
+    for r in reqs:
+        ud = from_user(r.user)
+        lg, det = orc.rank_request(ud, r.candidates, r.ctx, Pd, (32, 96, 32, 32), return_detail=True)
+        m = len(r.candidates)
+        ref_idx = np.full((m, nn.seq_len), -1, np.int32)
+        kth = np.zeros((m, 4))
+        for j in range(m):
+            for g, (st, sg) in enumerate(zip(nn.segment_starts(), det["segs"][j])):
+                ref_idx[j, st:st + len(sg)] = sg
+            for g, (name, src) in {0: ("nn_lifelong", "ll"), 2: ("nn_realtime_tail", "rt"),
+                                   3: ("nn_impression", "imp")}.items():
+                kth[j, g] = det["scores"][j][name][-1]
+
+        def fn(i, g, ii, _u=ud, _c=r.candidates):
+            src = {0: "ll", 2: "rt", 3: "imp"}[g]
+            return orc.similarity_scores(_u[f"{src}_emb"], _c[i])[ii]
+
+        check_nn_contract(idx[row:row + m], ref_idx, fn, kth, nn.segment_starts(), nn.segment_lengths())
+        err = np.abs(logits[row:row + m] - lg).max()
+        assert err <= TOL[mode], err
+        row += m
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_cobatched_equals_solo(mode):
+    """scores identical whether served alone or co-batched."""
+    nn = P.NNConfig()
+    reqs = P.generate_requests(4, 70, ll_tokens=3000, seed=3)
+    eng = _engine_for(nn)
+    together = eng.rank_requests([(r.user, r.candidates, r.ctx) for r in reqs], mode=mode)
+    solo = np.concatenate([eng.rank_requests([(r.user, r.candidates, r.ctx)], mode=mode) for r in reqs])
+    assert np.abs(together - solo).max() <= 1e-5
+
+
+def test_cold_start_and_rank_api():
+    nn = P.NNConfig()
+    eng = _engine_for(nn)
+    cands = P.generate_requests(1, 5, 100, seed=1)[0].candidates
+    resp = serving.rank(eng, 12345, None, cands, mode="fp32")
+    assert resp.cold_start and resp.probs.shape == (5, 4)
+    assert np.all((resp.probs > 0) & (resp.probs < 1))
+    Pd = orc.model_init(0, seq_len=nn.seq_len)
+    empty = {f"{s}_{c}": np.zeros((0, 32) if c == "emb" else 0, dt) for s in ("ll", "rt", "imp")
+             for c, dt in (("emb", np.int8), ("action", np.uint16), ("surface", np.uint8), ("ts", np.uint32))}
+    lg = orc.rank_request(empty, cands, orc.context_features(12345), Pd, (32, 96, 32, 32))
+    assert np.abs(resp.logits - lg).max() <= 1e-5
+
+
+def test_validation_errors_surface():
+    eng = _engine_for(P.NNConfig())
+    r = P.generate_requests(1, 3, 100)[0]
+    with pytest.raises(P.ValidationError):
+        eng.rank_requests([(r.user, np.zeros((0, 32), np.float32), None)])
+    with pytest.raises(P.ValidationError):
+        eng.rank_requests([(r.user, r.candidates, None)], mode="int4")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_full_size_c2_properties(mode):
+    """BASELINE configs[1] shape (1 x 1000 candidates, L=16384, S=192):
+    index contract on a candidate sample + logits vs the oracle on it."""
+    nn = P.NNConfig()
+    r = P.generate_requests(1, 1000, ll_tokens=16384, seed=7)[0]
+    eng = _engine_for(nn, cap=Capacity(1, 1000, 16896))
+    logits, idx = eng.rank_requests([(r.user, r.candidates, r.ctx)], mode=mode, return_indices=True)
+    assert np.all(np.isfinite(logits))
+    sample = np.arange(0, 1000, 37)
+    ud = from_user(r.user)
+    Pd = orc.model_init(0, seq_len=nn.seq_len)
+    lg, det = orc.rank_request(ud, r.candidates[sample], r.ctx, Pd, (32, 96, 32, 32), return_detail=True)
+    ref_idx = np.full((len(sample), nn.seq_len), -1, np.int32)
+    kth = np.zeros((len(sample), 4))
+    for j in range(len(sample)):
+        for st, sg in zip(nn.segment_starts(), det["segs"][j]):
+            ref_idx[j, st:st + len(sg)] = sg
+        for g, name in ((0, "nn_lifelong"), (2, "nn_realtime_tail"), (3, "nn_impression")):
+            kth[j, g] = det["scores"][j][name][-1]
+
+    def fn(i, g, ii):
+        src = {0: "ll", 2: "rt", 3: "imp"}[g]
+        return orc.similarity_scores(ud[f"{src}_emb"], r.candidates[sample[i]])[ii]
+
+    check_nn_contract(idx[sample], ref_idx, fn, kth, nn.segment_starts(), nn.segment_lengths())
+    assert np.abs(logits[sample] - lg).max() <= TOL[mode]
