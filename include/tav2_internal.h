@@ -1,0 +1,21 @@
+/*
+ * tav2_internal.h -- diagnostics exported by libtav2.so that are not part of
+ * the reference-facing interface (no reference equivalent).
+ */
+#ifndef TAV2_INTERNAL_H_
+#define TAV2_INTERNAL_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* One 128 x N x K tcgen05 MMA through the operand layouts the kernels use
+ * (which: 0 bf16 SS K-major, 1 bf16 A-in-TMEM, 2 bf16 B MN-major, 3 i8 with a
+ * TMA-loaded B, 4 i8 manual B).  A: [128, K], B: [N, K] ([K, N] for case 2),
+ * row-major device buffers; D: [128, N] f32 (s32 for i8).  Synchronous. */
+int tav2_tc_selftest(int which, const void* A, const void* B, void* D, int N, int K, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

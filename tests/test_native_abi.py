@@ -10,11 +10,11 @@ from conftest import REPO
 from paper_2506_02267_b200 import _native as N
 from paper_2506_02267_b200 import build
 
-HEADER = os.path.join(REPO, "include", "tav2.h")
+HEADERS = [os.path.join(REPO, "include", h) for h in ("tav2.h", "tav2_internal.h")]
 
 
 def declared():
-    src = open(HEADER).read()
+    src = "".join(open(h).read() for h in HEADERS)
     return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(tav2_\w+)\s*\(", src, re.M)))
 
 
