@@ -51,7 +51,9 @@ __global__ void __launch_bounds__(256) prep_kernel(Staged st) {
     for (int j = 0; j < kEmbed; j += 4)
       dst[j / 4] = make_float4(__fdiv_rn(d[j], nrm), __fdiv_rn(d[j + 1], nrm),
                                __fdiv_rn(d[j + 2], nrm), __fdiv_rn(d[j + 3], nrm));
-    st.tok_rnorm[i] = isq ? 7.450580596923828125e-9 / sqrt((double)isq) : 0.0;  // 2^-27/||q||
+    const double rn = isq ? 7.450580596923828125e-9 / sqrt((double)isq) : 0.0;  // 2^-27/||q||
+    st.tok_rnorm[i] = rn;
+    st.tok_rnorm_f[i] = (float)rn;
     return;
   }
   i -= st.n_tok;
@@ -143,8 +145,8 @@ __global__ void __launch_bounds__(kSimtTile) nn_simt_kernel(Staged st, NNCfg nn,
     }
   }
   if (!active) return;
-  uint64_t* out = part + (size_t)blockIdx.x * kmax * tile_size + lc;
-  for (int i = 0; i < k; ++i) out[(size_t)i * tile_size] = heap[i * kSimtTile + c];
+  uint64_t* out = part + part_offset(tile, src, lc, blockIdx.x - tile.work0[src], kmax, tile_size);
+  for (int i = 0; i < k; ++i) out[i] = heap[i * kSimtTile + c];
 }
 
 cudaError_t launch_nn_simt(const Staged& st, const NNCfg& nn, uint64_t* part, int kmax,
@@ -156,115 +158,6 @@ cudaError_t launch_nn_simt(const Staged& st, const NNCfg& nn, uint64_t* part, in
   if (e != cudaSuccess) return e;
   dim3 grid(st.n_work, tile_size / kSimtTile);
   nn_simt_kernel<<<grid, kSimtTile, smem, s>>>(st, nn, part, kmax, tile_size);
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// Merge: block (tile, source, half) x 64 threads; thread = candidate.  Folds
-// every chunk's partial top-k through one heap, then orders the picks by
-// descending storage index (ascending timestamp, nnsearch.py:364) and writes
-// them at the segment's slots with -1 padding (nnsearch.py:153-180).  The RT
-// block also writes the verbatim recent segment RT[:r] reversed (:144).
-// ---------------------------------------------------------------------------
-constexpr int kMergeThreads = 64;
-
-__device__ __forceinline__ void sift_max_u64(uint64_t* a, int ld, int n, int i) {
-  uint64_t v = a[i * ld];
-  while (true) {
-    int l = 2 * i + 1;
-    if (l >= n) break;
-    int c = l;
-    uint64_t cv = a[l * ld];
-    if (l + 1 < n) {
-      uint64_t rv = a[(l + 1) * ld];
-      if (rv > cv) { c = l + 1; cv = rv; }
-    }
-    if (cv <= v) break;
-    a[i * ld] = cv;
-    i = c;
-  }
-  a[i * ld] = v;
-}
-
-__global__ void __launch_bounds__(kMergeThreads) nn_merge_kernel(Staged st, NNCfg nn,
-                                                                 const uint64_t* part, int kmax,
-                                                                 int tile_size, int32_t* idx,
-                                                                 float* scores) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* heap = reinterpret_cast<uint64_t*>(smem);  // [k][64]
-  const NNTile tile = st.tiles[blockIdx.x];
-  const int s = blockIdx.y;
-  const int lc = blockIdx.z * kMergeThreads + threadIdx.x;  // candidate within tile
-  const int c = threadIdx.x;
-  if (lc >= tile.n) return;
-  const int item = tile.item0 + lc;
-  const int S = nn.seq_len;
-  const int k = nn.k[s];
-  const int seg = s == 0 ? 0 : (s == 1 ? 2 : 3);
-  int32_t* orow = idx + (size_t)item * S + nn.seg_start[seg];
-  float* srow = scores ? scores + (size_t)item * S + nn.seg_start[seg] : nullptr;
-
-  if (s == 1) {  // verbatim recent real-time segment
-    const ReqInfo rq = st.req[tile.req];
-    int n_recent = min(nn.recent, rq.len[1]);
-    int32_t* rrow = idx + (size_t)item * S + nn.seg_start[1];
-    for (int j = 0; j < nn.recent; ++j) {
-      rrow[j] = j < n_recent ? n_recent - 1 - j : -1;
-      if (scores) scores[(size_t)item * S + nn.seg_start[1] + j] = 0.0f;
-    }
-  }
-  if (k == 0) return;
-  for (int i = 0; i < k; ++i) heap[i * kMergeThreads + c] = 0ull;
-  uint64_t root = 0ull;
-  for (int w = tile.work0[s]; w < tile.work0[s] + tile.nwork[s]; ++w) {
-    const uint64_t* p = part + (size_t)w * kmax * tile_size + lc;
-    for (int i = 0; i < k; ++i) {
-      uint64_t key = p[(size_t)i * tile_size];
-      if (key > root) {
-        heap_replace_root(heap + c, kMergeThreads, k, key);
-        root = heap[c];
-      }
-    }
-  }
-  // re-key each pick as (index << 32 | f32 score bits) and sort ascending
-  int v = 0;
-  for (int i = 0; i < k; ++i) {
-    uint64_t key = heap[i * kMergeThreads + c];
-    if (key == 0ull) continue;
-    float sc = (float)key_score(key);
-    heap[v * kMergeThreads + c] =
-        ((uint64_t)key_index(key) << 32) | (uint64_t)__float_as_uint(sc);
-    ++v;
-  }
-  for (int i = v / 2 - 1; i >= 0; --i) sift_max_u64(heap + c, kMergeThreads, v, i);
-  for (int e = v - 1; e > 0; --e) {
-    uint64_t t = heap[c];
-    heap[c] = heap[e * kMergeThreads + c];
-    heap[e * kMergeThreads + c] = t;
-    sift_max_u64(heap + c, kMergeThreads, e, 0);
-  }
-  for (int j = 0; j < k; ++j) {
-    if (j < v) {
-      uint64_t e = heap[(v - 1 - j) * kMergeThreads + c];  // descending index
-      orow[j] = (int32_t)(e >> 32);
-      if (srow) srow[j] = __uint_as_float((uint32_t)e);
-    } else {
-      orow[j] = -1;
-      if (srow) srow[j] = 0.0f;
-    }
-  }
-}
-
-cudaError_t launch_nn_merge(const Staged& st, const NNCfg& nn, const uint64_t* part,
-                                  int kmax, int tile_size, int32_t* idx, float* scores,
-                                  cudaStream_t s) {
-  if (st.n_tiles == 0) return cudaSuccess;
-  size_t smem = (size_t)kmax * kMergeThreads * 8;
-  cudaError_t e = cudaFuncSetAttribute(nn_merge_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  dim3 grid(st.n_tiles, 3, tile_size / kMergeThreads);
-  nn_merge_kernel<<<grid, kMergeThreads, smem, s>>>(st, nn, part, kmax, tile_size, idx, scores);
   return cudaGetLastError();
 }
 

@@ -39,8 +39,8 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 constexpr int kTile = 128;        // candidates per NN tile (tcgen05 M)
-constexpr int kTargetWork = 296;  // ~2 NN work units per SM
 constexpr int kMinChunk = 256;    // minimum LL tokens per work unit
+constexpr int kMergeCap = 2048;   // nwork * k bound of the merge (nn_merge.cu)
 constexpr int kCaps[3] = {16384, 256, 256};  // LIFELONG/REALTIME/IMPRESSION_CAP (core.py:31-33)
 
 inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
@@ -55,6 +55,8 @@ struct tav2_ctx {
   NNCfg nn{};
   int kmax = 1;
   int max_tiles = 0, max_work = 0;
+  int sms = 148;
+  CUtensorMap emb_map{};
   // pinned host arena + device mirror of the staged region
   unsigned char* h_arena = nullptr;
   unsigned char* d_staged = nullptr;
@@ -65,6 +67,8 @@ struct tav2_ctx {
   double* tok_rnorm = nullptr;
   float* cand_unit = nullptr;
   uint64_t* part = nullptr;
+  float* part1 = nullptr;      // pass-1 per-chunk m-th best approx score (two-pass NN)
+  float* tok_rnorm_f = nullptr;
   int32_t* idx = nullptr;
   float* logits = nullptr;
   float* skut_scratch = nullptr;
@@ -106,12 +110,14 @@ Staged staged_view(tav2_ctx* c) {
   s.emb = reinterpret_cast<const int8_t*>(b + p.off_emb);
   s.tok_unit = c->tok_unit;
   s.tok_rnorm = c->tok_rnorm;
+  s.tok_rnorm_f = c->tok_rnorm_f;
   s.cand_unit = c->cand_unit;
   s.n_req = p.n_req;
   s.n_items = p.n_items;
   s.n_tok = p.n_tok;
   s.n_tiles = p.n_tiles;
   s.n_work = p.n_work;
+  s.p1_m = p.p1_m;
   return s;
 }
 
@@ -136,6 +142,8 @@ int free_all(tav2_ctx* c) {
   cudaFree(c->tok_rnorm);
   cudaFree(c->cand_unit);
   cudaFree(c->part);
+  cudaFree(c->part1);
+  cudaFree(c->tok_rnorm_f);
   cudaFree(c->idx);
   cudaFree(c->logits);
   cudaFree(c->skut_scratch);
@@ -231,8 +239,10 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
   c->kmax = std::max(1, std::max(m.k_lifelong, std::max(m.k_realtime, m.k_impression)));
   const int R = cap->max_requests, N = cap->max_items;
   const int64_t T = cap->max_tokens;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  if (c->sms <= 0) c->sms = 148;
   c->max_tiles = R + cdiv(N, kTile);
-  c->max_work = 3 * c->max_tiles + kTargetWork;
+  c->max_work = 3 * c->max_tiles + c->sms;
   c->staged_cap = staged_bytes(R, N, T, c->max_tiles, c->max_work);
 
   auto bad = [&](cudaError_t e, const char* what) {
@@ -251,6 +261,10 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
   if ((e = cudaMalloc(&c->cand_unit, (size_t)N * kEmbed * 4)) != cudaSuccess) return bad(e, "cand_unit");
   if ((e = cudaMalloc(&c->part, (size_t)c->max_work * c->kmax * kTile * 8)) != cudaSuccess)
     return bad(e, "partial top-k");
+  if ((e = cudaMalloc(&c->part1, (size_t)c->max_work * kTile * 4)) != cudaSuccess)
+    return bad(e, "pass-1 bounds");
+  if ((e = cudaMalloc(&c->tok_rnorm_f, std::max<int64_t>(T, 1) * 4)) != cudaSuccess)
+    return bad(e, "tok_rnorm_f");
   if ((e = cudaMalloc(&c->idx, (size_t)N * S * 4)) != cudaSuccess) return bad(e, "idx");
   if ((e = cudaMalloc(&c->logits, (size_t)N * kHeads * 4)) != cudaSuccess) return bad(e, "logits");
   {
@@ -372,10 +386,17 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
   if (T > c->cap.max_tokens)
     return fail(TAV2_ECAP, "%lld tokens exceed capacity %lld", (long long)T, (long long)c->cap.max_tokens);
 
-  // ---- NN work decomposition: LL chunks sized so the grid fills the GPU ----
-  const int ll_chunks_target = std::max(1, cdiv(kTargetWork, std::max(tiles, 1)));
+  // ---- NN work decomposition: one CTA per work unit; LL chunks sized so
+  // the units fill the SMs once, bounded by the merge capacity ----
+  int other = 0;
+  for (int r = 0; r < n_req; ++r) {
+    const int t = cdiv(reqs[r].n_cand, kTile);
+    other += t * ((nn.k[1] > 0 && reqs[r].len[1] > nn.recent) + (nn.k[2] > 0 && reqs[r].len[2] > 0));
+  }
+  const int ll_chunks_target = std::max(1, (c->sms - other) / std::max(tiles, 1));
   std::vector<NNTile> vt;
   std::vector<NNWork> vw;
+  int min_nw = 1 << 30;  // fewest chunks of any chunked LL source
   vt.reserve(tiles);
   {
     int item = 0;
@@ -393,7 +414,15 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
           t.work0[s] = (int)vw.size();
           t.nwork[s] = 0;
           if (nn.k[s] == 0 || hi <= lo) continue;
-          int nch = s == 0 ? std::min(ll_chunks_target, std::max(1, cdiv(hi - lo, kMinChunk))) : 1;
+          int nch = 1;
+          if (s == 0) {
+            // two-pass NN (nn_tc.cu) needs ceil(k/nch)+2 <= 16 register slots and the
+            // merge needs nch*k <= kMergeCap; otherwise one exact chunk
+            nch = std::max(1, std::min(ll_chunks_target, cdiv(hi - lo, kMinChunk)));
+            if (nch > 1) nch = std::max(nch, cdiv(nn.k[0], 16));
+            if (nch > 1 && (nch * nn.k[0] > kMergeCap || (hi - lo) / nch < 16)) nch = 1;
+            if (nch > 1) min_nw = std::min(min_nw, nch);
+          }
           int step = cdiv(hi - lo, nch);
           for (int a = lo; a < hi; a += step) {
             vw.push_back(NNWork{tid, s, a, std::min(hi, a + step)});
@@ -415,6 +444,7 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
   p.n_tiles = (int)vt.size();
   p.n_work = (int)vw.size();
   p.tile_size = kTile;
+  p.p1_m = (min_nw == (1 << 30) || min_nw * 8 >= nn.k[0]) ? 8 : 16;
   int64_t o = 0;
   p.off_req = o; o = align256(o + (int64_t)n_req * sizeof(ReqInfo));
   p.off_tiles = o; o = align256(o + (int64_t)p.n_tiles * sizeof(NNTile));
@@ -466,6 +496,8 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
   if (!vw.empty()) memcpy(h + p.off_work, vw.data(), vw.size() * sizeof(NNWork));
 
   CU(cudaSetDevice(c->device));
+  if (T > 0 && !make_rows32_map(&c->emb_map, c->d_staged + p.off_emb, T, 64))
+    return fail(TAV2_ECUDA, "cuTensorMapEncodeTiled failed for the token arena");
   CU(cudaMemcpyAsync(c->d_staged, h, p.bytes, cudaMemcpyHostToDevice, s));
   CU(cudaEventRecord(c->ev_staged, s));
   c->plan = p;
@@ -492,7 +524,12 @@ int run_nn(tav2_ctx* c, int mode, int32_t* idx, float* scores, cudaStream_t s) {
   if (mode == TAV2_MODE_FP32) {
     CU(timed(c, "nn_simt", s, [&] { return launch_nn_simt(st, c->nn, c->part, c->kmax, kTile, s); }));
   } else {
-    CU(timed(c, "nn_tc", s, [&] { return launch_nn_tc(st, c->nn, c->part, c->kmax, s); }));
+    CU(timed(c, "nn_tc_pass1", s, [&] {
+      return launch_nn_tc(st, c->nn, c->emb_map, c->part, c->part1, c->kmax, kTile, 1, s);
+    }));
+    CU(timed(c, "nn_tc_pass2", s, [&] {
+      return launch_nn_tc(st, c->nn, c->emb_map, c->part, c->part1, c->kmax, kTile, 2, s);
+    }));
   }
   CU(timed(c, "nn_merge", s,
            [&] { return launch_nn_merge(st, c->nn, c->part, c->kmax, kTile, idx, scores, s); }));

@@ -1,8 +1,10 @@
 // Shared device/host definitions for the tav2 kernels (sm_100a).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 #include "../../include/tav2.h"
 
@@ -47,7 +49,7 @@ struct NNTile {           // up to kTile consecutive items of one request
 
 struct Plan {
   int32_t n_req, n_items, n_tok;
-  int32_t n_tiles, n_work, tile_size;
+  int32_t n_tiles, n_work, tile_size, p1_m;
   // byte offsets inside the staged region
   int64_t off_req, off_tiles, off_work, off_item_req, off_ctx, off_cand, off_action,
       off_surface, off_emb, bytes;
@@ -96,8 +98,10 @@ struct Staged {
   const int8_t* emb;       // [T, 32]
   float* tok_unit;         // [T, 32] derived: unit(dequantize(q)) (core.py:77-79)
   double* tok_rnorm;       // [T]     derived: 2^-27 / ||q||_2 of the int8 row (i8-limb path)
+  float* tok_rnorm_f;      // [T]     the same in f32 (approximate pre-filter)
   float* cand_unit;        // [N, 32] derived: l2_normalize_rows(cand)
   int n_req, n_items, n_tok, n_tiles, n_work;
+  int p1_m;                // pass-1 list size of the two-pass NN (8 or 16)
 };
 
 // ---------------------------------------------------------------------------
@@ -129,6 +133,14 @@ __host__ __device__ inline double key_score(uint64_t key) {
   return s;
 }
 
+// Partial top-k buffer: for tile t, source s, candidate c (0..tile_size) and
+// chunk j (0..t.nwork[s]) the chunk's k keys are contiguous; all chunks of one
+// candidate are adjacent so the merge reads them coalesced.
+__host__ __device__ inline size_t part_offset(const NNTile& t, int s, int c, int j, int kmax,
+                                              int tile_size) {
+  return ((size_t)t.work0[s] * tile_size + (size_t)c * t.nwork[s] + j) * kmax;
+}
+
 // Min-heap of `k` keys stored with stride `ld` (struct-of-arrays across the
 // threads of a block so concurrent per-thread heaps are bank-conflict free).
 __device__ __forceinline__ void heap_replace_root(uint64_t* h, int ld, int k, uint64_t key) {
@@ -149,6 +161,25 @@ __device__ __forceinline__ void heap_replace_root(uint64_t* h, int ld, int k, ui
     i = c;
   }
   h[i * ld] = key;
+}
+
+// Restore the min-heap property below slot i (heapify building block).
+__device__ __forceinline__ void heap_sift_min(uint64_t* h, int ld, int n, int i) {
+  const uint64_t v = h[i * ld];
+  while (true) {
+    int l = 2 * i + 1;
+    if (l >= n) break;
+    int c = l;
+    uint64_t cv = h[l * ld];
+    if (l + 1 < n) {
+      const uint64_t rv = h[(l + 1) * ld];
+      if (rv < cv) { c = l + 1; cv = rv; }
+    }
+    if (cv >= v) break;
+    h[i * ld] = cv;
+    i = c;
+  }
+  h[i * ld] = v;
 }
 
 // Max-heap sift on u32 values (used to order the final picks by index).
@@ -189,8 +220,10 @@ namespace tav2 {
 cudaError_t launch_prep(const Staged& st, cudaStream_t s);
 cudaError_t launch_nn_simt(const Staged& st, const NNCfg& nn, uint64_t* part, int kmax,
                            int tile_size, cudaStream_t s);
-cudaError_t launch_nn_tc(const Staged& st, const NNCfg& nn, uint64_t* part, int kmax,
+cudaError_t launch_nn_tc(const Staged& st, const NNCfg& nn, const CUtensorMap& emb_map,
+                         uint64_t* part, float* part1, int kmax, int tile_size, int pass,
                          cudaStream_t s);
+bool make_rows32_map(CUtensorMap* map, const void* base, int64_t rows, int box_rows);
 cudaError_t launch_nn_merge(const Staged& st, const NNCfg& nn, const uint64_t* part, int kmax,
                             int tile_size, int32_t* idx, float* scores, cudaStream_t s);
 cudaError_t launch_encode(const Staged& st, const NNCfg& nn, const Params& p, const int32_t* idx,
