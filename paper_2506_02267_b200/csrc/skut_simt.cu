@@ -9,64 +9,13 @@
 #include <math.h>
 #include <stdint.h>
 
+#include "encode.cuh"
 #include "tav2_common.cuh"
 
 namespace tav2 {
 
 constexpr int kSkutThreads = 128;
 constexpr float kLnEps = 1e-5f;  // encoder.py:19
-
-// Which source and token does layout slot `r` of `item` hold?  Returns the
-// global token id or -1 for padding (nnsearch.py:153-180 segment order).
-__device__ __forceinline__ int slot_token(const Staged& st, const NNCfg& nn, const int32_t* idx,
-                                          int item, int r) {
-  int t = idx[(size_t)item * nn.seq_len + r];
-  if (t < 0) return -1;
-  const ReqInfo& rq = st.req[st.item_req[item]];
-  int src = r < nn.seg_start[1] ? 0 : (r < nn.seg_start[3] ? 1 : 2);
-  return rq.tok_off[src] + t;
-}
-
-// Eq. 4 (encoder.py:171-187): [unit(q) | unit(c)] + (bits @ action_table)
-// + surface_table[min(s,3)] + position_table[r]; masked rows are zero.
-__device__ __forceinline__ void encode_row(const Staged& st, const Params& p, int item, int tok,
-                                           int r, float* f) {
-  const float4* tu = reinterpret_cast<const float4*>(st.tok_unit + (size_t)tok * kEmbed);
-  const float4* cu = reinterpret_cast<const float4*>(st.cand_unit + (size_t)item * kEmbed);
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    float4 a = tu[j], b = cu[j];
-    f[4 * j] = a.x; f[4 * j + 1] = a.y; f[4 * j + 2] = a.z; f[4 * j + 3] = a.w;
-    f[32 + 4 * j] = b.x; f[33 + 4 * j] = b.y; f[34 + 4 * j] = b.z; f[35 + 4 * j] = b.w;
-  }
-  const unsigned act = st.action[tok];
-  int surf = st.surface[tok];
-  surf = surf > 3 ? 3 : surf;  // SURFACE_OTHER fold (encoder.py:178)
-  float asum[kDModel];
-#pragma unroll
-  for (int j = 0; j < kDModel; ++j) asum[j] = 0.0f;
-  for (int b = 0; b < p.action_rows; ++b) {
-    if ((act >> b) & 1u) {
-      const float4* row = reinterpret_cast<const float4*>(p.action_table + b * kDModel);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        float4 v = __ldg(row + j);
-        asum[4 * j] += v.x; asum[4 * j + 1] += v.y; asum[4 * j + 2] += v.z; asum[4 * j + 3] += v.w;
-      }
-    }
-  }
-  const float4* srow = reinterpret_cast<const float4*>(p.surface_table + surf * kDModel);
-  const float4* prow = reinterpret_cast<const float4*>(p.position_table + r * kDModel);
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    float4 s4 = __ldg(srow + j), p4 = __ldg(prow + j);
-    f[4 * j] = (f[4 * j] + asum[4 * j]) + s4.x;
-    f[4 * j + 1] = (f[4 * j + 1] + asum[4 * j + 1]) + s4.y;
-    f[4 * j + 2] = (f[4 * j + 2] + asum[4 * j + 2]) + s4.z;
-    f[4 * j + 3] = (f[4 * j + 3] + asum[4 * j + 3]) + s4.w;
-    f[4 * j] += p4.x; f[4 * j + 1] += p4.y; f[4 * j + 2] += p4.z; f[4 * j + 3] += p4.w;
-  }
-}
 
 // out[j] = sum_i a[i] * W[i, j]   (W row-major [IN, OUT] f32 in global)
 template <int IN, int OUT>

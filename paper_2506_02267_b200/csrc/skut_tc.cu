@@ -1,0 +1,552 @@
+// SKUT on the 5th-gen tensor cores: gather + Eq. 4 encode, 2 x pre-norm
+// causal transformer layers, linear + masked max-pool and the CTR head for
+// one candidate per CTA iteration (persistent over candidates).
+//
+// Reference: encoder.py:161-188 (encode_batch), :196-211 (layer_norm,
+// masked_softmax), :314-462 (forward_fused), trainer.py:354-366 (pool + head).
+//
+// Numerics ("bf16 mode"): every GEMM is a 3-term split-bf16 product
+// a.b ~= a_hi.b_hi + a_hi.b_lo + a_lo.b_hi (x_hi = bf16(x), x_lo = bf16(x -
+// x_hi)) accumulated in f32 in TMEM (~2^-16 relative per product, SURVEY
+// App. B: logits within 5e-5 vs the 2e-3 budget).  Residual stream, LN,
+// softmax statistics and the head stay f32 in registers.
+//
+// Layout: thread = sequence row.  Rows 0..127 are tile 0 (warps 0-3), rows
+// 128..255 tile 1 (warps 4-7); warp w owns TMEM lanes 32*(w%4)..+31.  The
+// residual row x[64] lives in registers.  A operands (LN outputs, Q, P,
+// O/l, ReLU(h)) are written by the row threads straight into TMEM as packed
+// bf16 hi/lo pairs (tcgen05.st); B operands (weights, K, V) live in shared
+// memory in the UMMA no-swizzle canonical layouts (tc_common.cuh).  Weight
+// images are streamed with cp.async.bulk into two buffers (WA: Wqkv or
+// out_linear, WB: Wo|W1|W2) one phase ahead.  Warp 8 lane 0 issues all MMAs
+// and bulk copies; row threads and the issuer hand off through mbarriers.
+//
+// TMEM columns (512): A/Q/O/LN2-A at 384+64t; D_qkv at 192t; S/P at 0 (tile
+// 0, 128 keys) and 128 (tile 1, S_pad keys); D_wo at 64t; D_w1 at 128+32t;
+// ReLU-A at 192+32t; D_w2 at 256+64t; pool D at 64t.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "encode.cuh"
+#include "tav2_common.cuh"
+#include "tc_common.cuh"
+
+namespace tav2 {
+
+using namespace tc;
+
+constexpr int kSkRowWarps = 8;
+constexpr int kSkThreads = 32 * (kSkRowWarps + 1);
+constexpr int kRowThreads = 32 * kSkRowWarps;
+constexpr float kLnEpsTc = 1e-5f;
+constexpr float kLog2e = 1.4426950408889634f;
+
+constexpr uint32_t kColA = 384, kColQKV = 0, kColS1 = 128, kColWo = 0, kColW1 = 128, kColA2 = 192,
+                   kColW2 = 256, kColOut = 0;
+
+// ---- row-thread helpers (warp-collective TMEM access) ----
+__device__ __forceinline__ void ld64(uint32_t ta, float* v) {
+  uint32_t r[32];
+  tmem_ld32(ta, r);
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  tmem_ld32(ta + 32, r);
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[32 + i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void ld32f(uint32_t ta, float* v) {
+  uint32_t r[32];
+  tmem_ld32(ta, r);
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+// split n (multiple of 16) floats into packed bf16 hi/lo pairs and store:
+// hi pairs at columns [0, n/2), lo pairs at [n/2, n) relative to `ta`
+template <int N>
+__device__ __forceinline__ void st_split(uint32_t ta, const float* v) {
+#pragma unroll
+  for (int c = 0; c < N / 16; ++c) {
+    uint32_t hi[8], lo[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) split_pair(v[16 * c + 2 * i], v[16 * c + 2 * i + 1], hi[i], lo[i]);
+    tmem_st8(ta + 8 * c, hi);
+    tmem_st8(ta + N / 2 + 8 * c, lo);
+  }
+}
+__device__ __forceinline__ void layer_norm_reg(const float* x, const float* __restrict__ g,
+                                               const float* __restrict__ b, float* y) {
+  float s = 0.0f;
+#pragma unroll
+  for (int j = 0; j < kDModel; ++j) s += x[j];
+  const float mu = s * (1.0f / 64.0f);
+  float v = 0.0f;
+#pragma unroll
+  for (int j = 0; j < kDModel; ++j) {
+    const float c = x[j] - mu;
+    v = fmaf(c, c, v);
+  }
+  const float rs = 1.0f / sqrtf(v * (1.0f / 64.0f) + kLnEpsTc);
+#pragma unroll
+  for (int j = 0; j < kDModel; ++j) y[j] = (x[j] - mu) * rs * __ldg(g + j) + __ldg(b + j);
+}
+// 16 bytes of 8 bf16 elements (from 8 floats)
+__device__ __forceinline__ void split8_store(uint8_t* hi_dst, uint8_t* lo_dst, const float* v) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) split_pair(v[2 * i], v[2 * i + 1], h[i], l[i]);
+  *reinterpret_cast<uint4*>(hi_dst) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(lo_dst) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+// ---- issuer helpers: D += A(TMEM hi/lo) x B(smem hi/lo), 3 terms per k-step ----
+// A: hi at a_col + 8j, lo at a_col + a_lo_off + 8j (k-step j covers 16 K)
+// B (K-major slabs): hi at b_hi + 2j*lbo, lo at b_lo + 2j*lbo
+__device__ __forceinline__ void mma3_kmajor(uint32_t d, uint32_t a_col, uint32_t a_lo_off,
+                                            uint32_t b_hi, uint32_t b_lo, uint32_t lbo, int ksteps,
+                                            uint32_t idesc) {
+  for (int j = 0; j < ksteps; ++j) {
+    const uint64_t bh = sdesc(b_hi + 2 * j * lbo, lbo, 128);
+    const uint64_t bl = sdesc(b_lo + 2 * j * lbo, lbo, 128);
+    mma_bf16_ts(d, a_col + 8 * j, bh, idesc, j > 0);
+    mma_bf16_ts(d, a_col + 8 * j, bl, idesc, 1);
+    mma_bf16_ts(d, a_col + a_lo_off + 8 * j, bh, idesc, 1);
+  }
+}
+
+struct SkSmem {
+  uint32_t wa, wb, khi, klo, vhi, vlo;  // shared-space byte addresses
+};
+
+__global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
+    Params p, SkutImages img, NNCfg nn, Staged st, int use_staged, const int32_t* idx,
+    const float* Fin, const uint8_t* fmask, int n, float* U, float* logits, float* pooled_out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ __align__(8) uint64_t bar_simt, bar_mma, bar_wa, bar_wb;
+  __shared__ uint32_t taddr_s;
+  __shared__ uint8_t valid_s[256];
+  __shared__ float red_s[kSkRowWarps][kDModel];
+  __shared__ float z_s[kDModel + kEmbed + kCtx];
+  __shared__ float hid_s[kHidden];
+  __shared__ int any_s;
+
+  const int S = nn.seq_len;
+  const int S_pad = (S + 15) & ~15;
+  const int NT = (S + 127) / 128;  // 1 or 2 row tiles
+  const int NL = p.num_layers;
+  uint8_t* WA = sm;
+  uint8_t* WB = sm + kImgWA;
+  uint8_t* Khi = WB + kImgWB;
+  uint8_t* Klo = Khi + S_pad * 128;
+  uint8_t* Vhi = Klo + S_pad * 128;
+  uint8_t* Vlo = Vhi + S_pad * 128;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    mbar_init(&bar_simt, kRowThreads);
+    mbar_init(&bar_mma, 1);
+    mbar_init(&bar_wa, 1);
+    mbar_init(&bar_wb, 1);
+    mbar_fence_init();
+  }
+  if (warp == kSkRowWarps) tmem_alloc<512>(&taddr_s);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t T = taddr_s;
+
+  if (warp == kSkRowWarps) {
+    // =================== MMA / bulk-copy issuer ===================
+    if (lane == 0) {
+      uint32_t ph_simt = 0, ph_wa = 0, ph_wb = 0, n_mma = 0;
+      auto wait_simt = [&]() { mbar_wait(&bar_simt, ph_simt); ph_simt ^= 1; fence_after(); };
+      auto mma_done = [&]() { commit(&bar_mma); ++n_mma; };
+      auto wait_mma = [&]() { mbar_wait(&bar_mma, (n_mma - 1) & 1); };
+      const uint32_t wa = smem_u32(WA), wb = smem_u32(WB);
+      const uint32_t khi = smem_u32(Khi), klo = smem_u32(Klo), vhi = smem_u32(Vhi), vlo = smem_u32(Vlo);
+      mbar_expect_tx(&bar_wa, kImgWA);
+      bulk_g2s(WA, img.wa[0], kImgWA, &bar_wa);
+      mbar_expect_tx(&bar_wb, kImgWB);
+      bulk_g2s(WB, img.wb[0], kImgWB, &bar_wb);
+      for (int item = blockIdx.x; item < n; item += gridDim.x) {
+        for (int L = 0; L < NL; ++L) {
+          // QKV = LN1(x) [Wq|Wk|Wv]   (N = 192, K = 64)
+          wait_simt();
+          mbar_wait(&bar_wa, ph_wa); ph_wa ^= 1;
+          fence_after();
+          for (int t = 0; t < NT; ++t)
+            mma3_kmajor(T + kColQKV + 192 * t, T + kColA + 64 * t, 32, wa, wa + kImgWA / 2, 192 * 16, 4,
+                        idesc_bf16(128, 192));
+          mma_done();
+          wait_mma();  // WA free: prefetch the next Wqkv (or out_linear)
+          if (L + 1 < NL) {
+            mbar_expect_tx(&bar_wa, kImgWA);
+            bulk_g2s(WA, img.wa[L + 1], kImgWA, &bar_wa);
+          } else {
+            mbar_expect_tx(&bar_wa, kImgWO);
+            bulk_g2s(WA, img.wout, kImgWO, &bar_wa);
+          }
+          // S_t = Q_t K^T  (N = keys of tile t, K = 64)
+          wait_simt();
+          for (int t = 0; t < NT; ++t) {
+            const int nk = t == 0 ? (S_pad < 128 ? S_pad : 128) : S_pad;
+            mma3_kmajor(T + (t == 0 ? 0u : kColS1), T + kColA + 64 * t, 32, khi, klo, S_pad * 16, 4,
+                        idesc_bf16(128, nk));
+          }
+          mma_done();
+          // O_t = P_t V  (N = 64, K = keys; V is MN-major)
+          wait_simt();
+          for (int t = 0; t < NT; ++t) {
+            const int nk = t == 0 ? (S_pad < 128 ? S_pad : 128) : S_pad;
+            const uint32_t pc = T + (t == 0 ? 0u : kColS1);
+            const uint32_t id = idesc_bf16(128, 64, 0, 1);
+            for (int j = 0; j < nk / 16; ++j) {
+              const uint64_t bh = sdesc(vhi + 2 * j * 1024, 1024, 128);
+              const uint64_t bl = sdesc(vlo + 2 * j * 1024, 1024, 128);
+              const uint32_t d = T + kColA + 64 * t;
+              mma_bf16_ts(d, pc + 16 * j, bh, id, j > 0);
+              mma_bf16_ts(d, pc + 16 * j, bl, id, 1);
+              mma_bf16_ts(d, pc + 16 * j + 8, bh, id, 1);
+            }
+          }
+          mma_done();
+          // Wo
+          wait_simt();
+          mbar_wait(&bar_wb, ph_wb); ph_wb ^= 1;
+          fence_after();
+          for (int t = 0; t < NT; ++t)
+            mma3_kmajor(T + kColWo + 64 * t, T + kColA + 64 * t, 32, wb, wb + 8192, 64 * 16, 4,
+                        idesc_bf16(128, 64));
+          mma_done();
+          // W1 (N = 32)
+          wait_simt();
+          for (int t = 0; t < NT; ++t)
+            mma3_kmajor(T + kColW1 + 32 * t, T + kColA + 64 * t, 32, wb + 16384, wb + 16384 + 4096,
+                        32 * 16, 4, idesc_bf16(128, 32));
+          mma_done();
+          // W2 (N = 64, K = 32)
+          wait_simt();
+          for (int t = 0; t < NT; ++t)
+            mma3_kmajor(T + kColW2 + 64 * t, T + kColA2 + 32 * t, 16, wb + 24576, wb + 24576 + 4096,
+                        64 * 16, 2, idesc_bf16(128, 64));
+          mma_done();
+          wait_mma();  // WB free: prefetch the next layer's (or candidate's) Wo|W1|W2
+          mbar_expect_tx(&bar_wb, kImgWB);
+          bulk_g2s(WB, img.wb[(L + 1) % NL], kImgWB, &bar_wb);
+        }
+        // pool: y = x out_linear
+        wait_simt();
+        mbar_wait(&bar_wa, ph_wa); ph_wa ^= 1;
+        fence_after();
+        for (int t = 0; t < NT; ++t)
+          mma3_kmajor(T + kColOut + 64 * t, T + kColA + 64 * t, 32, wa, wa + 8192, 64 * 16, 4,
+                      idesc_bf16(128, 64));
+        mma_done();
+        wait_mma();
+        mbar_expect_tx(&bar_wa, kImgWA);
+        bulk_g2s(WA, img.wa[0], kImgWA, &bar_wa);
+      }
+      // drain the last prefetches before the CTA retires
+      mbar_wait(&bar_wa, ph_wa);
+      mbar_wait(&bar_wb, ph_wb);
+    }
+  } else {
+    // =================== row threads ===================
+    const int t = warp >> 2, q = warp & 3;
+    const int r = 128 * t + 32 * q + lane;  // sequence row
+    const uint32_t lanebase = T + ((uint32_t)(32 * q) << 16);
+    const uint32_t cA = lanebase + kColA + 64 * t;
+    const bool in_seq = r < S;
+    uint32_t n_mma = 0;
+    auto wait_mma = [&]() { mbar_wait(&bar_mma, n_mma & 1); ++n_mma; fence_after(); };
+    auto done = [&]() { fence_before(); mbar_arrive(&bar_simt); };
+
+    for (int item = blockIdx.x; item < n; item += gridDim.x) {
+      // ---- K3: gather + encode this row (or load caller features) ----
+      float x[kDModel];
+      bool ok = false;
+      if (in_seq) {
+        if (use_staged) {
+          const int tok = slot_token(st, nn, idx, item, r);
+          ok = tok >= 0;
+          if (ok) encode_row(st, p, item, tok, r, x);
+        } else {
+          ok = fmask[(size_t)item * S + r] != 0;
+          if (ok) {
+            const float4* src = reinterpret_cast<const float4*>(Fin + ((size_t)item * S + r) * kDModel);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float4 v = src[j];
+              x[4 * j] = v.x; x[4 * j + 1] = v.y; x[4 * j + 2] = v.z; x[4 * j + 3] = v.w;
+            }
+          }
+        }
+      }
+      if (!ok) {
+#pragma unroll
+        for (int j = 0; j < kDModel; ++j) x[j] = 0.0f;
+      }
+      valid_s[r] = ok;
+      named_bar_sync(1, kRowThreads);
+      // warp-uniform bound of the keys any row of this warp may attend to
+      const int wmax_row = 128 * t + 32 * q + 31;
+
+      for (int L = 0; L < NL; ++L) {
+        // ---- LN1 -> A ----
+        {
+          float y[kDModel];
+          layer_norm_reg(x, p.ln1_scale[L], p.ln1_shift[L], y);
+          if (!ok) {
+#pragma unroll
+            for (int j = 0; j < kDModel; ++j) y[j] = 0.0f;
+          }
+          st_split<64>(cA, y);  // warp-collective: never under a divergent branch
+          tmem_st_wait();
+          done();
+        }
+        // ---- QKV epilogue: Q -> TMEM A, K/V -> smem ----
+        wait_mma();
+        {
+          const uint32_t cq = lanebase + kColQKV + 192 * t;
+          float v[32];
+          // Q (cols 0..63): A operand hi at cA+0..31, lo at cA+32..63
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            ld32f(cq + 32 * h, v);
+            if (!ok) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+            }
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              uint32_t hi[8], lo[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) split_pair(v[16 * c + 2 * i], v[16 * c + 2 * i + 1], hi[i], lo[i]);
+              tmem_st8(cA + 16 * h + 8 * c, hi);
+              tmem_st8(cA + 32 + 16 * h + 8 * c, lo);
+            }
+          }
+          // K (cols 64..127): K-major slabs, chunk c of row r at c*(S_pad*16) + r*16
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            ld32f(cq + 64 + 32 * h, v);
+            if (r < S_pad) {
+              if (!ok) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+              }
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const int off = (4 * h + c) * (S_pad * 16) + r * 16;
+                split8_store(Khi + off, Klo + off, v + 8 * c);
+              }
+            }
+          }
+          // V (cols 128..191): MN-major, (key r, d) at (r/8)*1024 + (d/8)*128 + (r%8)*16 + (d%8)*2
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            ld32f(cq + 128 + 32 * h, v);
+            if (r < S_pad) {
+              if (!ok) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+              }
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const int off = (r >> 3) * 1024 + (4 * h + c) * 128 + (r & 7) * 16;
+                split8_store(Vhi + off, Vlo + off, v + 8 * c);
+              }
+            }
+          }
+          tmem_st_wait();
+          fence_proxy_async();
+          done();
+        }
+        // ---- causal key-masked softmax -> P (bf16 hi/lo, in place over S) ----
+        wait_mma();
+        float inv_l = 0.0f;
+        {
+          const int nk = t == 0 ? (S_pad < 128 ? S_pad : 128) : S_pad;
+          const uint32_t cs = lanebase + (t == 0 ? 0u : kColS1);
+          const int jlast = min(nk / 16 - 1, wmax_row / 16);  // chunks any row of the warp needs
+          float m = -INFINITY;
+          for (int j = 0; j <= jlast; ++j) {
+            uint32_t s16[16];
+            tmem_ld16(cs + 16 * j, s16);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int key = 16 * j + e;
+              if (key <= r && valid_s[key]) m = fmaxf(m, __uint_as_float(s16[e]) * 0.125f);
+            }
+          }
+          const float mb = (m == -INFINITY ? 0.0f : m) * kLog2e;
+          float l = 0.0f;
+          for (int j = 0; j < nk / 16; ++j) {
+            uint32_t hi[8], lo[8];
+            if (j <= jlast) {
+              uint32_t s16[16];
+              tmem_ld16(cs + 16 * j, s16);
+              tmem_ld_wait();
+              float pv[16];
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                const int key = 16 * j + e;
+                const bool use = ok && key <= r && valid_s[key];
+                pv[e] = use ? exp2f(fmaf(__uint_as_float(s16[e]), 0.125f * kLog2e, -mb)) : 0.0f;
+                l += pv[e];
+              }
+#pragma unroll
+              for (int i = 0; i < 8; ++i) split_pair(pv[2 * i], pv[2 * i + 1], hi[i], lo[i]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) hi[i] = lo[i] = 0u;
+            }
+            tmem_st8(cs + 16 * j, hi);
+            tmem_st8(cs + 16 * j + 8, lo);
+          }
+          inv_l = l > 0.0f ? 1.0f / l : 0.0f;  // a valid row always sees itself
+          tmem_st_wait();
+          done();
+        }
+        // ---- O / l -> A ----
+        wait_mma();
+        {
+          float o[kDModel];
+          ld64(cA, o);
+#pragma unroll
+          for (int j = 0; j < kDModel; ++j) o[j] *= inv_l;
+          if (!ok) {
+#pragma unroll
+            for (int j = 0; j < kDModel; ++j) o[j] = 0.0f;
+          }
+          st_split<64>(cA, o);
+          tmem_st_wait();
+          done();
+        }
+        // ---- x += O Wo ; LN2 -> A ----
+        wait_mma();
+        {
+          float d[kDModel];
+          ld64(lanebase + kColWo + 64 * t, d);
+          if (ok) {
+#pragma unroll
+            for (int j = 0; j < kDModel; ++j) x[j] += d[j];
+          }
+          layer_norm_reg(x, p.ln2_scale[L], p.ln2_shift[L], d);
+          if (!ok) {
+#pragma unroll
+            for (int j = 0; j < kDModel; ++j) d[j] = 0.0f;
+          }
+          st_split<64>(cA, d);
+          tmem_st_wait();
+          done();
+        }
+        // ---- ReLU(h) -> A2 ----
+        wait_mma();
+        {
+          float h[kFfn];
+          ld32f(lanebase + kColW1 + 32 * t, h);
+#pragma unroll
+          for (int j = 0; j < kFfn; ++j) h[j] = ok ? fmaxf(h[j], 0.0f) : 0.0f;
+          st_split<32>(lanebase + kColA2 + 32 * t, h);
+          tmem_st_wait();
+          done();
+        }
+        // ---- x += ReLU(h) W2 ----
+        wait_mma();
+        {
+          float d[kDModel];
+          ld64(lanebase + kColW2 + 64 * t, d);
+          if (ok) {
+#pragma unroll
+            for (int j = 0; j < kDModel; ++j) x[j] += d[j];
+          }
+        }
+      }
+
+      if (U && in_seq) {  // forward_fused output rows (padded rows are zero)
+        float4* dst = reinterpret_cast<float4*>(U + ((size_t)item * S + r) * kDModel);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          dst[j] = ok ? make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3])
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      // ---- K5: y = x out_linear, masked max over rows, CTR head ----
+      st_split<64>(cA, x);  // invalid rows carry x = 0
+      tmem_st_wait();
+      done();
+      wait_mma();
+      {
+        float y[kDModel];
+        ld64(lanebase + kColOut + 64 * t, y);
+        if (tid == 0) any_s = 0;
+        named_bar_sync(1, kRowThreads);
+        if (ok) any_s = 1;
+#pragma unroll
+        for (int j = 0; j < kDModel; ++j) {
+          float v = ok ? y[j] : -INFINITY;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+          if (lane == 0) red_s[warp][j] = v;
+        }
+      }
+      named_bar_sync(1, kRowThreads);
+      if (logits) {
+        if (tid < kDModel) {
+          float v = -INFINITY;
+#pragma unroll
+          for (int w = 0; w < kSkRowWarps; ++w) v = fmaxf(v, red_s[w][tid]);
+          v = any_s ? v : 0.0f;  // empty user -> pooled = 0 (trainer.py:358-359)
+          z_s[tid] = v;
+          if (pooled_out) pooled_out[(size_t)item * kDModel + tid] = v;
+        } else if (tid < kDModel + kEmbed) {
+          z_s[tid] = use_staged ? st.cand_unit[(size_t)item * kEmbed + tid - kDModel] : 0.0f;
+        } else if (tid < kDModel + kEmbed + kCtx) {
+          z_s[tid] = use_staged ? st.ctx[st.item_req[item] * kCtx + tid - kDModel - kEmbed] : 0.0f;
+        }
+        named_bar_sync(1, kRowThreads);
+        if (tid < kHidden) {
+          float h = 0.0f;
+          for (int i = 0; i < kDModel + kEmbed + kCtx; ++i) h = fmaf(z_s[i], __ldg(p.head_w1 + i * kHidden + tid), h);
+          hid_s[tid] = fmaxf(h + __ldg(p.head_b1 + tid), 0.0f);
+        }
+        named_bar_sync(1, kRowThreads);
+        if (tid < kHeads) {
+          float o = 0.0f;
+          for (int j = 0; j < kHidden; ++j) o = fmaf(hid_s[j], __ldg(p.head_w2 + j * kHeads + tid), o);
+          logits[(size_t)item * kHeads + tid] = o + __ldg(p.head_b2 + tid);
+        }
+      }
+      named_bar_sync(1, kRowThreads);  // smem (valid_s, red_s, z_s) reuse by the next item
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == kSkRowWarps) tmem_free<512>(T);
+}
+
+cudaError_t launch_skut_tc(const Params& p, const SkutImages& img, const NNCfg& nn,
+                           const Staged* st, const int32_t* idx, const float* F,
+                           const uint8_t* fmask, int n, float* U, float* logits, float* pooled,
+                           cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int S_pad = (nn.seq_len + 15) & ~15;
+  const size_t smem = (size_t)kImgWA + kImgWB + 4 * (size_t)S_pad * 128;
+  cudaError_t e = cudaFuncSetAttribute(skut_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  Staged dummy{};
+  skut_tc_kernel<<<n < sms ? n : sms, kSkThreads, smem, s>>>(p, img, nn, st ? *st : dummy, st != nullptr, idx,
+                                                            F, fmask, n, U, logits, pooled);
+  return cudaGetLastError();
+}
+
+}  // namespace tav2

@@ -75,6 +75,8 @@ struct tav2_ctx {
   // params
   float* d_params = nullptr;
   Params params{};
+  uint8_t* d_images = nullptr;  // bf16x3 weight images (tensor-core SKUT)
+  SkutImages images{};
   bool params_ok = false;
   // current batch
   Plan plan{};
@@ -148,6 +150,7 @@ int free_all(tav2_ctx* c) {
   cudaFree(c->logits);
   cudaFree(c->skut_scratch);
   cudaFree(c->d_params);
+  cudaFree(c->d_images);
   if (c->ev_staged) cudaEventDestroy(c->ev_staged);
   for (auto& sl : c->slots) {
     if (sl.a) cudaEventDestroy(sl.a);
@@ -343,6 +346,7 @@ int tav2_load_params(tav2_ctx* c, int n, const char* const* names, const float* 
   if (c->d_params) {
     CU(cudaDeviceSynchronize());
     cudaFree(c->d_params);
+  cudaFree(c->d_images);
     c->d_params = nullptr;
   }
   CU(cudaMalloc(&c->d_params, total * 4));
@@ -353,6 +357,58 @@ int tav2_load_params(tav2_ctx* c, int n, const char* const* names, const float* 
   }
   CU(cudaMemcpy(c->d_params, host.data(), total * 4, cudaMemcpyHostToDevice));
   c->params = P;
+
+  // ---- bf16 hi/lo weight images, UMMA B-operand layout (tav2_common.cuh) ----
+  auto host_of = [&](const float* dev) { return host.data() + (dev - c->d_params); };
+  const int L = m.num_layers;
+  const size_t img_bytes = (size_t)L * (kImgWA + kImgWB) + kImgWO;
+  std::vector<uint8_t> img(img_bytes, 0);
+  auto bf16 = [](float x) -> uint16_t {  // round-to-nearest-even
+    uint32_t u;
+    memcpy(&u, &x, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+  };
+  auto bf16f = [](uint16_t h) {
+    uint32_t u = (uint32_t)h << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+  };
+  // write W^T of an [in, out] matrix into a (N = n_total, K) slab image at row offset n0
+  auto put = [&](uint8_t* base, int n_total, int K, int n0, const float* W, int in, int out) {
+    uint8_t* lo_base = base + (size_t)n_total * K * 2;
+    for (int k = 0; k < in; ++k)
+      for (int n = 0; n < out; ++n) {
+        const float w = W[k * out + n];
+        const uint16_t hi = bf16(w);
+        const uint16_t lo = bf16(w - bf16f(hi));
+        const size_t off = (size_t)(k / 8) * (n_total * 16) + (size_t)(n0 + n) * 16 + (k % 8) * 2;
+        memcpy(base + off, &hi, 2);
+        memcpy(lo_base + off, &lo, 2);
+      }
+  };
+  for (int l = 0; l < L; ++l) {
+    uint8_t* wa = img.data() + (size_t)l * (kImgWA + kImgWB);
+    uint8_t* wb = wa + kImgWA;
+    put(wa, 192, 64, 0, host_of(P.wq[l]), 64, 64);
+    put(wa, 192, 64, 64, host_of(P.wk[l]), 64, 64);
+    put(wa, 192, 64, 128, host_of(P.wv[l]), 64, 64);
+    put(wb, 64, 64, 0, host_of(P.wo[l]), 64, 64);                   // 16 KB
+    put(wb + 16384, 32, 64, 0, host_of(P.w1[l]), 64, 32);           //  8 KB
+    put(wb + 16384 + 8192, 64, 32, 0, host_of(P.w2[l]), 32, 64);    //  8 KB
+  }
+  put(img.data() + (size_t)L * (kImgWA + kImgWB), 64, 64, 0, host_of(P.out_linear), 64, 64);
+  if (c->d_images) cudaFree(c->d_images);
+  c->d_images = nullptr;
+  CU(cudaMalloc(&c->d_images, img_bytes));
+  CU(cudaMemcpy(c->d_images, img.data(), img_bytes, cudaMemcpyHostToDevice));
+  for (int l = 0; l < L; ++l) {
+    c->images.wa[l] = c->d_images + (size_t)l * (kImgWA + kImgWB);
+    c->images.wb[l] = c->images.wa[l] + kImgWA;
+  }
+  c->images.wout = c->d_images + (size_t)L * (kImgWA + kImgWB);
   c->params_ok = true;
   return TAV2_OK;
 }
@@ -540,7 +596,16 @@ int run_score(tav2_ctx* c, int mode, const int32_t* idx, float* logits, float* p
               cudaStream_t s) {
   if (!c->params_ok) return fail(TAV2_ESTATE, "parameters not loaded");
   Staged st = staged_view(c);
-  (void)mode;
+  // The 2-row-tile tensor-core SKUT holds K/V of <= 256 keys in shared
+  // memory; longer sequences (the k_ll = 256 sweep point, S = 352) run the
+  // SIMT kernel, which is f32 throughout and so also meets the bf16 budget.
+  if (mode == TAV2_MODE_BF16 && c->nn.seq_len <= 256) {
+    CU(timed(c, "skut_tc", s, [&] {
+      return launch_skut_tc(c->params, c->images, c->nn, &st, idx, nullptr, nullptr, st.n_items,
+                            nullptr, logits, pooled, s);
+    }));
+    return TAV2_OK;
+  }
   CU(timed(c, "skut_simt", s, [&] {
     return launch_skut_simt(c->params, c->nn, &st, idx, nullptr, nullptr, st.n_items,
                             c->skut_scratch, nullptr, logits, pooled, s);
@@ -584,6 +649,11 @@ int tav2_forward(tav2_ctx* c, int mode, const float* features_dev, const uint8_t
   if (n == 0) return TAV2_OK;
   if (!features_dev || !mask_dev || !u_dev) return fail(TAV2_EINVAL, "null device pointer");
   CU(cudaSetDevice(c->device));
+  if (mode == TAV2_MODE_BF16 && c->nn.seq_len <= 256) {
+    CU(launch_skut_tc(c->params, c->images, c->nn, nullptr, nullptr, features_dev, mask_dev, n,
+                      u_dev, nullptr, nullptr, (cudaStream_t)stream));
+    return TAV2_OK;
+  }
   CU(launch_skut_simt(c->params, c->nn, nullptr, nullptr, features_dev, mask_dev, n,
                       c->skut_scratch, u_dev, nullptr, nullptr, (cudaStream_t)stream));
   return TAV2_OK;

@@ -79,6 +79,19 @@ struct Params {
   const float* head_b2;  // head.b2 [4]
 };
 
+// bf16x3 weight images for the tensor-core SKUT (built once at load time).
+// Every matrix W [in, out] is stored as the UMMA B operand W^T [N=out][K=in],
+// K-major, 16-byte chunk slabs: element (n, k) at (k/8)*(N*16) + n*16 +
+// (k%8)*2, hi image followed by lo image (hi = bf16(w), lo = bf16(w - hi)).
+struct SkutImages {
+  const uint8_t* wa[kMaxLayers];  // layer L: [Wq|Wk|Wv]^T  N=192 K=64   48 KB
+  const uint8_t* wb[kMaxLayers];  // layer L: Wo^T (16 KB) | W1^T (8 KB) | W2^T (8 KB)
+  const uint8_t* wout;            // out_linear^T N=64 K=64 16 KB
+};
+constexpr int kImgWA = 2 * 192 * 64 * 2;  // 49152
+constexpr int kImgWB = 2 * (64 * 64 + 32 * 64 + 64 * 32) * 2;  // 32768
+constexpr int kImgWO = 2 * 64 * 64 * 2;   // 16384
+
 struct NNCfg {
   int32_t recent, k[3];       // k[0] = k_ll, k[1] = k_rt, k[2] = k_imp
   int32_t seg_start[4];       // layout starts: NN_LL, RT_recent, NN_RT_tail, NN_IMP
@@ -232,6 +245,10 @@ cudaError_t launch_skut_simt(const Params& p, const NNCfg& nn, const Staged* st,
                              const int32_t* idx, const float* F, const uint8_t* fmask, int n,
                              float* scratch, float* U, float* logits, float* pooled,
                              cudaStream_t s);
+cudaError_t launch_skut_tc(const Params& p, const SkutImages& img, const NNCfg& nn,
+                           const Staged* st, const int32_t* idx, const float* F,
+                           const uint8_t* fmask, int n, float* U, float* logits, float* pooled,
+                           cudaStream_t s);
 int skut_simt_grid(int n);
 size_t skut_simt_scratch_floats(int seq_len);
 }  // namespace tav2
