@@ -18,8 +18,9 @@
 // bf16 hi/lo pairs (tcgen05.st); B operands (weights, K, V) live in shared
 // memory in the UMMA no-swizzle canonical layouts (tc_common.cuh).  Weight
 // images are streamed with cp.async.bulk into two buffers (WA: Wqkv or
-// out_linear, WB: Wo|W1|W2) one phase ahead.  Warp 8 lane 0 issues all MMAs
-// and bulk copies; row threads and the issuer hand off through mbarriers.
+// out_linear, WB: Wo|W1|W2) one phase ahead.  Thread 0 also issues all
+// MMAs and bulk copies; row threads and the issuer hand off through
+// mbarriers (8 warps = 2 per SM sub-partition -> up to 255 registers).
 //
 // TMEM columns (512): A/Q/O/LN2-A at 384+64t; D_qkv at 192t; S/P at 0 (tile
 // 0, 128 keys) and 128 (tile 1, S_pad keys); D_wo at 64t; D_w1 at 128+32t;
@@ -29,6 +30,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "encode.cuh"
 #include "tav2_common.cuh"
@@ -39,7 +41,7 @@ namespace tav2 {
 using namespace tc;
 
 constexpr int kSkRowWarps = 8;
-constexpr int kSkThreads = 32 * (kSkRowWarps + 1);
+constexpr int kSkThreads = 32 * kSkRowWarps;
 constexpr int kRowThreads = 32 * kSkRowWarps;
 constexpr float kLnEpsTc = 1e-5f;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -49,22 +51,14 @@ constexpr uint32_t kColA = 384, kColQKV = 0, kColS1 = 128, kColWo = 0, kColW1 = 
 
 // ---- row-thread helpers (warp-collective TMEM access) ----
 __device__ __forceinline__ void ld64(uint32_t ta, float* v) {
-  uint32_t r[32];
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
   tmem_ld32(ta, r);
+  tmem_ld32(ta + 32, r + 32);
   tmem_ld_wait();
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-  tmem_ld32(ta + 32, r);
-  tmem_ld_wait();
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[32 + i] = __uint_as_float(r[i]);
 }
 __device__ __forceinline__ void ld32f(uint32_t ta, float* v) {
-  uint32_t r[32];
-  tmem_ld32(ta, r);
+  tmem_ld32(ta, reinterpret_cast<uint32_t*>(v));
   tmem_ld_wait();
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 // split n (multiple of 16) floats into packed bf16 hi/lo pairs and store:
 // hi pairs at columns [0, n/2), lo pairs at [n/2, n) relative to `ta`
@@ -79,8 +73,8 @@ __device__ __forceinline__ void st_split(uint32_t ta, const float* v) {
     tmem_st8(ta + N / 2 + 8 * c, lo);
   }
 }
-__device__ __forceinline__ void layer_norm_reg(const float* x, const float* __restrict__ g,
-                                               const float* __restrict__ b, float* y) {
+__device__ __forceinline__ void layer_norm_reg(const float* x, const float* g, const float* b,
+                                               float* y) {
   float s = 0.0f;
 #pragma unroll
   for (int j = 0; j < kDModel; ++j) s += x[j];
@@ -93,7 +87,7 @@ __device__ __forceinline__ void layer_norm_reg(const float* x, const float* __re
   }
   const float rs = 1.0f / sqrtf(v * (1.0f / 64.0f) + kLnEpsTc);
 #pragma unroll
-  for (int j = 0; j < kDModel; ++j) y[j] = (x[j] - mu) * rs * __ldg(g + j) + __ldg(b + j);
+  for (int j = 0; j < kDModel; ++j) y[j] = fmaf((x[j] - mu) * rs, g[j], b[j]);
 }
 // 16 bytes of 8 bf16 elements (from 8 floats)
 __device__ __forceinline__ void split8_store(uint8_t* hi_dst, uint8_t* lo_dst, const float* v) {
@@ -119,8 +113,98 @@ __device__ __forceinline__ void mma3_kmajor(uint32_t d, uint32_t a_col, uint32_t
   }
 }
 
-struct SkSmem {
-  uint32_t wa, wb, khi, klo, vhi, vlo;  // shared-space byte addresses
+// allowed keys k0..k0+15 for query row r: key-valid bits (low 16 of `bits`)
+// AND causal (key <= r)
+__device__ __forceinline__ uint32_t allowed16(uint32_t bits, int k0, int r) {
+  const int n = r - k0 + 1;  // keys k0..r are causal-visible
+  const uint32_t causal = n >= 16 ? 0xffffu : (n <= 0 ? 0u : ((1u << n) - 1u));
+  return bits & causal;
+}
+
+// MMA / bulk-copy issuer state, driven by thread 0 between its own
+// arrive on bar_simt and its wait on bar_mma (the CTA has no spare warp:
+// 8 warps keep 2 per SM sub-partition and so up to 255 registers each).
+struct Issuer {
+  uint32_t T, wa, wb, khi, klo, vhi, vlo;
+  uint32_t ph_simt = 0, ph_wa = 0, ph_wb = 0, n_mma = 0;
+  uint64_t *bar_simt, *bar_mma, *bar_wa, *bar_wb;
+  uint8_t *WA, *WB;
+  int NT, S_pad;
+
+  __device__ void wait_simt() {
+    mbar_wait(bar_simt, ph_simt);
+    ph_simt ^= 1;
+    fence_after();
+  }
+  __device__ void commit_mma() {
+    commit(bar_mma);
+    ++n_mma;
+  }
+  __device__ void wait_mma() { mbar_wait(bar_mma, (n_mma - 1) & 1); }
+  __device__ void load_wa(const void* src, uint32_t bytes) {
+    mbar_expect_tx(bar_wa, bytes);
+    bulk_g2s(WA, src, bytes, bar_wa);
+  }
+  __device__ void load_wb(const void* src) {
+    mbar_expect_tx(bar_wb, kImgWB);
+    bulk_g2s(WB, src, kImgWB, bar_wb);
+  }
+  __device__ void need_wa() {
+    mbar_wait(bar_wa, ph_wa);
+    ph_wa ^= 1;
+    fence_after();
+  }
+  __device__ void need_wb() {
+    mbar_wait(bar_wb, ph_wb);
+    ph_wb ^= 1;
+    fence_after();
+  }
+  __device__ int nkeys(int t) const { return t == 0 ? (S_pad < 128 ? S_pad : 128) : S_pad; }
+
+  // QKV = LN1(x) [Wq|Wk|Wv]   (N = 192, K = 64)
+  __device__ void qkv() {
+    for (int t = 0; t < NT; ++t)
+      mma3_kmajor(T + kColQKV + 192 * t, T + kColA + 64 * t, 32, wa, wa + kImgWA / 2, 192 * 16, 4,
+                  idesc_bf16(128, 192));
+  }
+  // S_t = Q_t K^T  (N = keys of tile t, K = 64)
+  __device__ void scores() {
+    for (int t = 0; t < NT; ++t)
+      mma3_kmajor(T + (t == 0 ? 0u : kColS1), T + kColA + 64 * t, 32, khi, klo, S_pad * 16, 4,
+                  idesc_bf16(128, nkeys(t)));
+  }
+  // O_t = P_t V  (N = 64, K = keys; V is MN-major)
+  __device__ void pv() {
+    const uint32_t id = idesc_bf16(128, 64, 0, 1);
+    for (int t = 0; t < NT; ++t) {
+      const uint32_t pc = T + (t == 0 ? 0u : kColS1), d = T + kColA + 64 * t;
+      for (int j = 0; j < nkeys(t) / 16; ++j) {
+        const uint64_t bh = sdesc(vhi + 2 * j * 1024, 1024, 128);
+        const uint64_t bl = sdesc(vlo + 2 * j * 1024, 1024, 128);
+        mma_bf16_ts(d, pc + 16 * j, bh, id, j > 0);
+        mma_bf16_ts(d, pc + 16 * j, bl, id, 1);
+        mma_bf16_ts(d, pc + 16 * j + 8, bh, id, 1);
+      }
+    }
+  }
+  __device__ void wo() {
+    for (int t = 0; t < NT; ++t)
+      mma3_kmajor(T + kColWo + 64 * t, T + kColA + 64 * t, 32, wb, wb + 8192, 64 * 16, 4, idesc_bf16(128, 64));
+  }
+  __device__ void w1() {
+    for (int t = 0; t < NT; ++t)
+      mma3_kmajor(T + kColW1 + 32 * t, T + kColA + 64 * t, 32, wb + 16384, wb + 16384 + 4096, 32 * 16, 4,
+                  idesc_bf16(128, 32));
+  }
+  __device__ void w2() {
+    for (int t = 0; t < NT; ++t)
+      mma3_kmajor(T + kColW2 + 64 * t, T + kColA2 + 32 * t, 16, wb + 24576, wb + 24576 + 4096, 64 * 16, 2,
+                  idesc_bf16(128, 64));
+  }
+  __device__ void pool() {
+    for (int t = 0; t < NT; ++t)
+      mma3_kmajor(T + kColOut + 64 * t, T + kColA + 64 * t, 32, wa, wa + 8192, 64 * 16, 4, idesc_bf16(128, 64));
+  }
 };
 
 __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
@@ -129,7 +213,8 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ __align__(8) uint64_t bar_simt, bar_mma, bar_wa, bar_wb;
   __shared__ uint32_t taddr_s;
-  __shared__ uint8_t valid_s[256];
+  __shared__ uint32_t valid_w[8];  // key-validity bitmask, bit r of word r/32
+  __shared__ __align__(16) float lnp_s[kMaxLayers][4][kDModel];  // ln1 g/b, ln2 g/b
   __shared__ float red_s[kSkRowWarps][kDModel];
   __shared__ float z_s[kDModel + kEmbed + kCtx];
   __shared__ float hid_s[kHidden];
@@ -154,381 +239,360 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
     mbar_init(&bar_wb, 1);
     mbar_fence_init();
   }
-  if (warp == kSkRowWarps) tmem_alloc<512>(&taddr_s);
+  if (warp == 0) tmem_alloc<512>(&taddr_s);
+  for (int i = tid; i < NL * 4 * kDModel; i += kSkThreads) {
+    const int L = i / (4 * kDModel), w = (i / kDModel) % 4, j = i % kDModel;
+    const float* src = w == 0 ? p.ln1_scale[L] : w == 1 ? p.ln1_shift[L] : w == 2 ? p.ln2_scale[L] : p.ln2_shift[L];
+    lnp_s[L][w][j] = src[j];
+  }
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t T = taddr_s;
 
-  if (warp == kSkRowWarps) {
-    // =================== MMA / bulk-copy issuer ===================
-    if (lane == 0) {
-      uint32_t ph_simt = 0, ph_wa = 0, ph_wb = 0, n_mma = 0;
-      auto wait_simt = [&]() { mbar_wait(&bar_simt, ph_simt); ph_simt ^= 1; fence_after(); };
-      auto mma_done = [&]() { commit(&bar_mma); ++n_mma; };
-      auto wait_mma = [&]() { mbar_wait(&bar_mma, (n_mma - 1) & 1); };
-      const uint32_t wa = smem_u32(WA), wb = smem_u32(WB);
-      const uint32_t khi = smem_u32(Khi), klo = smem_u32(Klo), vhi = smem_u32(Vhi), vlo = smem_u32(Vlo);
-      mbar_expect_tx(&bar_wa, kImgWA);
-      bulk_g2s(WA, img.wa[0], kImgWA, &bar_wa);
-      mbar_expect_tx(&bar_wb, kImgWB);
-      bulk_g2s(WB, img.wb[0], kImgWB, &bar_wb);
-      for (int item = blockIdx.x; item < n; item += gridDim.x) {
-        for (int L = 0; L < NL; ++L) {
-          // QKV = LN1(x) [Wq|Wk|Wv]   (N = 192, K = 64)
-          wait_simt();
-          mbar_wait(&bar_wa, ph_wa); ph_wa ^= 1;
-          fence_after();
-          for (int t = 0; t < NT; ++t)
-            mma3_kmajor(T + kColQKV + 192 * t, T + kColA + 64 * t, 32, wa, wa + kImgWA / 2, 192 * 16, 4,
-                        idesc_bf16(128, 192));
-          mma_done();
-          wait_mma();  // WA free: prefetch the next Wqkv (or out_linear)
-          if (L + 1 < NL) {
-            mbar_expect_tx(&bar_wa, kImgWA);
-            bulk_g2s(WA, img.wa[L + 1], kImgWA, &bar_wa);
-          } else {
-            mbar_expect_tx(&bar_wa, kImgWO);
-            bulk_g2s(WA, img.wout, kImgWO, &bar_wa);
+  Issuer is;
+  const bool issuer = tid == 0;
+  if (issuer) {
+    is.T = T;
+    is.WA = WA;
+    is.WB = WB;
+    is.wa = smem_u32(WA);
+    is.wb = smem_u32(WB);
+    is.khi = smem_u32(Khi);
+    is.klo = smem_u32(Klo);
+    is.vhi = smem_u32(Vhi);
+    is.vlo = smem_u32(Vlo);
+    is.bar_simt = &bar_simt;
+    is.bar_mma = &bar_mma;
+    is.bar_wa = &bar_wa;
+    is.bar_wb = &bar_wb;
+    is.NT = NT;
+    is.S_pad = S_pad;
+    is.load_wa(img.wa[0], kImgWA);
+    is.load_wb(img.wb[0]);
+  }
+
+  const int t = warp >> 2, q = warp & 3;
+  const int r = 128 * t + 32 * q + lane;  // sequence row
+  const uint32_t lanebase = T + ((uint32_t)(32 * q) << 16);
+  const uint32_t cA = lanebase + kColA + 64 * t;
+  const bool in_seq = r < S;
+  uint32_t n_mma = 0;
+  auto wait_mma = [&]() {
+    __syncwarp();
+    mbar_wait_sleep(&bar_mma, n_mma & 1);
+    ++n_mma;
+    fence_after();
+  };
+  auto done = [&]() {
+    fence_before();
+    mbar_arrive(&bar_simt);
+  };
+
+  for (int item = blockIdx.x; item < n; item += gridDim.x) {
+    // ---- K3: gather + encode this row (or load caller features) ----
+    float x[kDModel];
+    bool ok = false;
+    if (in_seq) {
+      if (use_staged) {
+        const int tok = slot_token(st, nn, idx, item, r);
+        ok = tok >= 0;
+        if (ok) encode_row(st, p, item, tok, r, x);
+      } else {
+        ok = fmask[(size_t)item * S + r] != 0;
+        if (ok) {
+          const float4* src = reinterpret_cast<const float4*>(Fin + ((size_t)item * S + r) * kDModel);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float4 v = src[j];
+            x[4 * j] = v.x; x[4 * j + 1] = v.y; x[4 * j + 2] = v.z; x[4 * j + 3] = v.w;
           }
-          // S_t = Q_t K^T  (N = keys of tile t, K = 64)
-          wait_simt();
-          for (int t = 0; t < NT; ++t) {
-            const int nk = t == 0 ? (S_pad < 128 ? S_pad : 128) : S_pad;
-            mma3_kmajor(T + (t == 0 ? 0u : kColS1), T + kColA + 64 * t, 32, khi, klo, S_pad * 16, 4,
-                        idesc_bf16(128, nk));
-          }
-          mma_done();
-          // O_t = P_t V  (N = 64, K = keys; V is MN-major)
-          wait_simt();
-          for (int t = 0; t < NT; ++t) {
-            const int nk = t == 0 ? (S_pad < 128 ? S_pad : 128) : S_pad;
-            const uint32_t pc = T + (t == 0 ? 0u : kColS1);
-            const uint32_t id = idesc_bf16(128, 64, 0, 1);
-            for (int j = 0; j < nk / 16; ++j) {
-              const uint64_t bh = sdesc(vhi + 2 * j * 1024, 1024, 128);
-              const uint64_t bl = sdesc(vlo + 2 * j * 1024, 1024, 128);
-              const uint32_t d = T + kColA + 64 * t;
-              mma_bf16_ts(d, pc + 16 * j, bh, id, j > 0);
-              mma_bf16_ts(d, pc + 16 * j, bl, id, 1);
-              mma_bf16_ts(d, pc + 16 * j + 8, bh, id, 1);
-            }
-          }
-          mma_done();
-          // Wo
-          wait_simt();
-          mbar_wait(&bar_wb, ph_wb); ph_wb ^= 1;
-          fence_after();
-          for (int t = 0; t < NT; ++t)
-            mma3_kmajor(T + kColWo + 64 * t, T + kColA + 64 * t, 32, wb, wb + 8192, 64 * 16, 4,
-                        idesc_bf16(128, 64));
-          mma_done();
-          // W1 (N = 32)
-          wait_simt();
-          for (int t = 0; t < NT; ++t)
-            mma3_kmajor(T + kColW1 + 32 * t, T + kColA + 64 * t, 32, wb + 16384, wb + 16384 + 4096,
-                        32 * 16, 4, idesc_bf16(128, 32));
-          mma_done();
-          // W2 (N = 64, K = 32)
-          wait_simt();
-          for (int t = 0; t < NT; ++t)
-            mma3_kmajor(T + kColW2 + 64 * t, T + kColA2 + 32 * t, 16, wb + 24576, wb + 24576 + 4096,
-                        64 * 16, 2, idesc_bf16(128, 64));
-          mma_done();
-          wait_mma();  // WB free: prefetch the next layer's (or candidate's) Wo|W1|W2
-          mbar_expect_tx(&bar_wb, kImgWB);
-          bulk_g2s(WB, img.wb[(L + 1) % NL], kImgWB, &bar_wb);
         }
-        // pool: y = x out_linear
-        wait_simt();
-        mbar_wait(&bar_wa, ph_wa); ph_wa ^= 1;
-        fence_after();
-        for (int t = 0; t < NT; ++t)
-          mma3_kmajor(T + kColOut + 64 * t, T + kColA + 64 * t, 32, wa, wa + 8192, 64 * 16, 4,
-                      idesc_bf16(128, 64));
-        mma_done();
-        wait_mma();
-        mbar_expect_tx(&bar_wa, kImgWA);
-        bulk_g2s(WA, img.wa[0], kImgWA, &bar_wa);
       }
-      // drain the last prefetches before the CTA retires
-      mbar_wait(&bar_wa, ph_wa);
-      mbar_wait(&bar_wb, ph_wb);
     }
-  } else {
-    // =================== row threads ===================
-    const int t = warp >> 2, q = warp & 3;
-    const int r = 128 * t + 32 * q + lane;  // sequence row
-    const uint32_t lanebase = T + ((uint32_t)(32 * q) << 16);
-    const uint32_t cA = lanebase + kColA + 64 * t;
-    const bool in_seq = r < S;
-    uint32_t n_mma = 0;
-    auto wait_mma = [&]() { mbar_wait(&bar_mma, n_mma & 1); ++n_mma; fence_after(); };
-    auto done = [&]() { fence_before(); mbar_arrive(&bar_simt); };
-
-    for (int item = blockIdx.x; item < n; item += gridDim.x) {
-      // ---- K3: gather + encode this row (or load caller features) ----
-      float x[kDModel];
-      bool ok = false;
-      if (in_seq) {
-        if (use_staged) {
-          const int tok = slot_token(st, nn, idx, item, r);
-          ok = tok >= 0;
-          if (ok) encode_row(st, p, item, tok, r, x);
-        } else {
-          ok = fmask[(size_t)item * S + r] != 0;
-          if (ok) {
-            const float4* src = reinterpret_cast<const float4*>(Fin + ((size_t)item * S + r) * kDModel);
+    if (!ok) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const float4 v = src[j];
-              x[4 * j] = v.x; x[4 * j + 1] = v.y; x[4 * j + 2] = v.z; x[4 * j + 3] = v.w;
-            }
-          }
+      for (int j = 0; j < kDModel; ++j) x[j] = 0.0f;
+    }
+    {
+      const unsigned b = __ballot_sync(0xffffffffu, ok);
+      if (lane == 0) valid_w[warp] = b;
+    }
+    named_bar_sync(1, kRowThreads);
+    const int wmax_row = 128 * t + 32 * q + 31;  // warp-uniform causal bound
+
+    for (int L = 0; L < NL; ++L) {
+      // ---- LN1 -> A ----
+      {
+        float y[kDModel];
+        layer_norm_reg(x, lnp_s[L][0], lnp_s[L][1], y);
+        if (!ok) {
+#pragma unroll
+          for (int j = 0; j < kDModel; ++j) y[j] = 0.0f;
         }
+        st_split<64>(cA, y);  // warp-collective: never under a divergent branch
+        tmem_st_wait();
+        done();
       }
-      if (!ok) {
+      if (issuer) {
+        is.wait_simt();
+        is.need_wa();
+        is.qkv();
+        is.commit_mma();
+        is.wait_mma();  // WA free: prefetch the next Wqkv (or out_linear)
+        if (L + 1 < NL) is.load_wa(img.wa[L + 1], kImgWA);
+        else is.load_wa(img.wout, kImgWO);
+      }
+      // ---- QKV epilogue: Q -> TMEM A, K/V -> smem ----
+      wait_mma();
+      {
+        const uint32_t cq = lanebase + kColQKV + 192 * t;
+        float v[32];
 #pragma unroll
-        for (int j = 0; j < kDModel; ++j) x[j] = 0.0f;
-      }
-      valid_s[r] = ok;
-      named_bar_sync(1, kRowThreads);
-      // warp-uniform bound of the keys any row of this warp may attend to
-      const int wmax_row = 128 * t + 32 * q + 31;
-
-      for (int L = 0; L < NL; ++L) {
-        // ---- LN1 -> A ----
-        {
-          float y[kDModel];
-          layer_norm_reg(x, p.ln1_scale[L], p.ln1_shift[L], y);
+        for (int h = 0; h < 2; ++h) {
+          ld32f(cq + 32 * h, v);
           if (!ok) {
 #pragma unroll
-            for (int j = 0; j < kDModel; ++j) y[j] = 0.0f;
+            for (int i = 0; i < 32; ++i) v[i] = 0.0f;
           }
-          st_split<64>(cA, y);  // warp-collective: never under a divergent branch
-          tmem_st_wait();
-          done();
-        }
-        // ---- QKV epilogue: Q -> TMEM A, K/V -> smem ----
-        wait_mma();
-        {
-          const uint32_t cq = lanebase + kColQKV + 192 * t;
-          float v[32];
-          // Q (cols 0..63): A operand hi at cA+0..31, lo at cA+32..63
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            ld32f(cq + 32 * h, v);
+          for (int c = 0; c < 2; ++c) {
+            uint32_t hi[8], lo[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) split_pair(v[16 * c + 2 * i], v[16 * c + 2 * i + 1], hi[i], lo[i]);
+            tmem_st8(cA + 16 * h + 8 * c, hi);
+            tmem_st8(cA + 32 + 16 * h + 8 * c, lo);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // K: K-major slabs, chunk c of row r at c*(S_pad*16) + r*16
+          ld32f(cq + 64 + 32 * h, v);
+          if (r < S_pad) {
             if (!ok) {
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] = 0.0f;
             }
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              uint32_t hi[8], lo[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) split_pair(v[16 * c + 2 * i], v[16 * c + 2 * i + 1], hi[i], lo[i]);
-              tmem_st8(cA + 16 * h + 8 * c, hi);
-              tmem_st8(cA + 32 + 16 * h + 8 * c, lo);
+            for (int c = 0; c < 4; ++c) {
+              const int off = (4 * h + c) * (S_pad * 16) + r * 16;
+              split8_store(Khi + off, Klo + off, v + 8 * c);
             }
           }
-          // K (cols 64..127): K-major slabs, chunk c of row r at c*(S_pad*16) + r*16
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            ld32f(cq + 64 + 32 * h, v);
-            if (r < S_pad) {
-              if (!ok) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = 0.0f;
-              }
-#pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                const int off = (4 * h + c) * (S_pad * 16) + r * 16;
-                split8_store(Khi + off, Klo + off, v + 8 * c);
-              }
-            }
-          }
-          // V (cols 128..191): MN-major, (key r, d) at (r/8)*1024 + (d/8)*128 + (r%8)*16 + (d%8)*2
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            ld32f(cq + 128 + 32 * h, v);
-            if (r < S_pad) {
-              if (!ok) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = 0.0f;
-              }
-#pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                const int off = (r >> 3) * 1024 + (4 * h + c) * 128 + (r & 7) * 16;
-                split8_store(Vhi + off, Vlo + off, v + 8 * c);
-              }
-            }
-          }
-          tmem_st_wait();
-          fence_proxy_async();
-          done();
         }
-        // ---- causal key-masked softmax -> P (bf16 hi/lo, in place over S) ----
-        wait_mma();
-        float inv_l = 0.0f;
-        {
-          const int nk = t == 0 ? (S_pad < 128 ? S_pad : 128) : S_pad;
-          const uint32_t cs = lanebase + (t == 0 ? 0u : kColS1);
-          const int jlast = min(nk / 16 - 1, wmax_row / 16);  // chunks any row of the warp needs
-          float m = -INFINITY;
-          for (int j = 0; j <= jlast; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // V: MN-major (key r, d) at (r/8)*1024 + (d/8)*128 + (r%8)*16 + (d%8)*2
+          ld32f(cq + 128 + 32 * h, v);
+          if (r < S_pad) {
+            if (!ok) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int off = (r >> 3) * 1024 + (4 * h + c) * 128 + (r & 7) * 16;
+              split8_store(Vhi + off, Vlo + off, v + 8 * c);
+            }
+          }
+        }
+        tmem_st_wait();
+        fence_proxy_async();
+        done();
+      }
+      if (issuer) {
+        is.wait_simt();
+        is.scores();
+        is.commit_mma();
+      }
+      // ---- causal key-masked softmax -> P (bf16 hi/lo, in place over S) ----
+      wait_mma();
+      float inv_l = 0.0f;
+      {
+        const int nk = t == 0 ? (S_pad < 128 ? S_pad : 128) : S_pad;
+        const uint32_t cs = lanebase + (t == 0 ? 0u : kColS1);
+        const int jlast = min(nk / 16 - 1, wmax_row / 16);  // chunks any row of the warp needs
+        float m = -INFINITY;
+        for (int j = 0; j <= jlast; ++j) {
+          uint32_t s16[16];
+          tmem_ld16(cs + 16 * j, s16);
+          const uint32_t vm = allowed16(valid_w[j >> 1] >> ((j & 1) * 16), 16 * j, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if ((vm >> e) & 1u) m = fmaxf(m, __uint_as_float(s16[e]));
+        }
+        const float mb = (m == -INFINITY ? 0.0f : m) * (0.125f * kLog2e);  // scale 1/sqrt(64)
+        float l = 0.0f;
+        for (int j = 0; j < nk / 16; ++j) {
+          uint32_t hi[8], lo[8];
+          if (j <= jlast) {
             uint32_t s16[16];
             tmem_ld16(cs + 16 * j, s16);
+            const uint32_t vm = ok ? allowed16(valid_w[j >> 1] >> ((j & 1) * 16), 16 * j, r) : 0u;
             tmem_ld_wait();
+            float pv[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
-              const int key = 16 * j + e;
-              if (key <= r && valid_s[key]) m = fmaxf(m, __uint_as_float(s16[e]) * 0.125f);
+              pv[e] = ((vm >> e) & 1u) ? exp2f(fmaf(__uint_as_float(s16[e]), 0.125f * kLog2e, -mb)) : 0.0f;
+              l += pv[e];
             }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) split_pair(pv[2 * i], pv[2 * i + 1], hi[i], lo[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) hi[i] = lo[i] = 0u;
           }
-          const float mb = (m == -INFINITY ? 0.0f : m) * kLog2e;
-          float l = 0.0f;
-          for (int j = 0; j < nk / 16; ++j) {
-            uint32_t hi[8], lo[8];
-            if (j <= jlast) {
-              uint32_t s16[16];
-              tmem_ld16(cs + 16 * j, s16);
-              tmem_ld_wait();
-              float pv[16];
-#pragma unroll
-              for (int e = 0; e < 16; ++e) {
-                const int key = 16 * j + e;
-                const bool use = ok && key <= r && valid_s[key];
-                pv[e] = use ? exp2f(fmaf(__uint_as_float(s16[e]), 0.125f * kLog2e, -mb)) : 0.0f;
-                l += pv[e];
-              }
-#pragma unroll
-              for (int i = 0; i < 8; ++i) split_pair(pv[2 * i], pv[2 * i + 1], hi[i], lo[i]);
-            } else {
-#pragma unroll
-              for (int i = 0; i < 8; ++i) hi[i] = lo[i] = 0u;
-            }
-            tmem_st8(cs + 16 * j, hi);
-            tmem_st8(cs + 16 * j + 8, lo);
-          }
-          inv_l = l > 0.0f ? 1.0f / l : 0.0f;  // a valid row always sees itself
-          tmem_st_wait();
-          done();
+          tmem_st8(cs + 16 * j, hi);
+          tmem_st8(cs + 16 * j + 8, lo);
         }
-        // ---- O / l -> A ----
-        wait_mma();
-        {
-          float o[kDModel];
-          ld64(cA, o);
-#pragma unroll
-          for (int j = 0; j < kDModel; ++j) o[j] *= inv_l;
-          if (!ok) {
-#pragma unroll
-            for (int j = 0; j < kDModel; ++j) o[j] = 0.0f;
-          }
-          st_split<64>(cA, o);
-          tmem_st_wait();
-          done();
-        }
-        // ---- x += O Wo ; LN2 -> A ----
-        wait_mma();
-        {
-          float d[kDModel];
-          ld64(lanebase + kColWo + 64 * t, d);
-          if (ok) {
-#pragma unroll
-            for (int j = 0; j < kDModel; ++j) x[j] += d[j];
-          }
-          layer_norm_reg(x, p.ln2_scale[L], p.ln2_shift[L], d);
-          if (!ok) {
-#pragma unroll
-            for (int j = 0; j < kDModel; ++j) d[j] = 0.0f;
-          }
-          st_split<64>(cA, d);
-          tmem_st_wait();
-          done();
-        }
-        // ---- ReLU(h) -> A2 ----
-        wait_mma();
-        {
-          float h[kFfn];
-          ld32f(lanebase + kColW1 + 32 * t, h);
-#pragma unroll
-          for (int j = 0; j < kFfn; ++j) h[j] = ok ? fmaxf(h[j], 0.0f) : 0.0f;
-          st_split<32>(lanebase + kColA2 + 32 * t, h);
-          tmem_st_wait();
-          done();
-        }
-        // ---- x += ReLU(h) W2 ----
-        wait_mma();
-        {
-          float d[kDModel];
-          ld64(lanebase + kColW2 + 64 * t, d);
-          if (ok) {
-#pragma unroll
-            for (int j = 0; j < kDModel; ++j) x[j] += d[j];
-          }
-        }
+        inv_l = l > 0.0f ? 1.0f / l : 0.0f;  // a valid row always sees itself
+        tmem_st_wait();
+        done();
       }
-
-      if (U && in_seq) {  // forward_fused output rows (padded rows are zero)
-        float4* dst = reinterpret_cast<float4*>(U + ((size_t)item * S + r) * kDModel);
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-          dst[j] = ok ? make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3])
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (issuer) {
+        is.wait_simt();
+        is.pv();
+        is.commit_mma();
       }
-      // ---- K5: y = x out_linear, masked max over rows, CTR head ----
-      st_split<64>(cA, x);  // invalid rows carry x = 0
-      tmem_st_wait();
-      done();
+      // ---- O / l -> A ----
       wait_mma();
       {
-        float y[kDModel];
-        ld64(lanebase + kColOut + 64 * t, y);
-        if (tid == 0) any_s = 0;
-        named_bar_sync(1, kRowThreads);
-        if (ok) any_s = 1;
+        float o[kDModel];
+        ld64(cA, o);
 #pragma unroll
-        for (int j = 0; j < kDModel; ++j) {
-          float v = ok ? y[j] : -INFINITY;
+        for (int j = 0; j < kDModel; ++j) o[j] = ok ? o[j] * inv_l : 0.0f;
+        st_split<64>(cA, o);
+        tmem_st_wait();
+        done();
+      }
+      if (issuer) {
+        is.wait_simt();
+        is.need_wb();
+        is.wo();
+        is.commit_mma();
+      }
+      // ---- x += O Wo ; LN2 -> A ----
+      wait_mma();
+      {
+        float d[kDModel];
+        ld64(lanebase + kColWo + 64 * t, d);
+        if (ok) {
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-          if (lane == 0) red_s[warp][j] = v;
+          for (int j = 0; j < kDModel; ++j) x[j] += d[j];
         }
+        layer_norm_reg(x, lnp_s[L][2], lnp_s[L][3], d);
+        if (!ok) {
+#pragma unroll
+          for (int j = 0; j < kDModel; ++j) d[j] = 0.0f;
+        }
+        st_split<64>(cA, d);
+        tmem_st_wait();
+        done();
+      }
+      if (issuer) {
+        is.wait_simt();
+        is.w1();
+        is.commit_mma();
+      }
+      // ---- ReLU(h) -> A2 ----
+      wait_mma();
+      {
+        float h[kFfn];
+        ld32f(lanebase + kColW1 + 32 * t, h);
+#pragma unroll
+        for (int j = 0; j < kFfn; ++j) h[j] = ok ? fmaxf(h[j], 0.0f) : 0.0f;
+        st_split<32>(lanebase + kColA2 + 32 * t, h);
+        tmem_st_wait();
+        done();
+      }
+      if (issuer) {
+        is.wait_simt();
+        is.w2();
+        is.commit_mma();
+        is.wait_mma();  // WB free: prefetch the next layer's (or candidate's) Wo|W1|W2
+        is.load_wb(img.wb[(L + 1) % NL]);
+      }
+      // ---- x += ReLU(h) W2 ----
+      wait_mma();
+      {
+        float d[kDModel];
+        ld64(lanebase + kColW2 + 64 * t, d);
+        if (ok) {
+#pragma unroll
+          for (int j = 0; j < kDModel; ++j) x[j] += d[j];
+        }
+      }
+    }
+
+    if (U && in_seq) {  // forward_fused output rows (padded rows are zero)
+      float4* dst = reinterpret_cast<float4*>(U + ((size_t)item * S + r) * kDModel);
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        dst[j] = ok ? make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3])
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    // ---- K5: y = x out_linear, masked max over rows, CTR head ----
+    st_split<64>(cA, x);  // invalid rows carry x = 0
+    tmem_st_wait();
+    done();
+    if (issuer) {
+      is.wait_simt();
+      is.need_wa();
+      is.pool();
+      is.commit_mma();
+      is.wait_mma();  // WA free: next candidate's layer-0 Wqkv
+      is.load_wa(img.wa[0], kImgWA);
+    }
+    wait_mma();
+    {
+      float y[kDModel];
+      ld64(lanebase + kColOut + 64 * t, y);
+      if (tid == 0) any_s = 0;
+      named_bar_sync(1, kRowThreads);
+      if (ok) any_s = 1;
+#pragma unroll
+      for (int j = 0; j < kDModel; ++j) {
+        float v = ok ? y[j] : -INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (lane == 0) red_s[warp][j] = v;
+      }
+    }
+    named_bar_sync(1, kRowThreads);
+    if (logits) {
+      if (tid < kDModel) {
+        float v = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kSkRowWarps; ++w) v = fmaxf(v, red_s[w][tid]);
+        v = any_s ? v : 0.0f;  // empty user -> pooled = 0 (trainer.py:358-359)
+        z_s[tid] = v;
+        if (pooled_out) pooled_out[(size_t)item * kDModel + tid] = v;
+      } else if (tid < kDModel + kEmbed) {
+        z_s[tid] = use_staged ? st.cand_unit[(size_t)item * kEmbed + tid - kDModel] : 0.0f;
+      } else if (tid < kDModel + kEmbed + kCtx) {
+        z_s[tid] = use_staged ? st.ctx[st.item_req[item] * kCtx + tid - kDModel - kEmbed] : 0.0f;
       }
       named_bar_sync(1, kRowThreads);
-      if (logits) {
-        if (tid < kDModel) {
-          float v = -INFINITY;
-#pragma unroll
-          for (int w = 0; w < kSkRowWarps; ++w) v = fmaxf(v, red_s[w][tid]);
-          v = any_s ? v : 0.0f;  // empty user -> pooled = 0 (trainer.py:358-359)
-          z_s[tid] = v;
-          if (pooled_out) pooled_out[(size_t)item * kDModel + tid] = v;
-        } else if (tid < kDModel + kEmbed) {
-          z_s[tid] = use_staged ? st.cand_unit[(size_t)item * kEmbed + tid - kDModel] : 0.0f;
-        } else if (tid < kDModel + kEmbed + kCtx) {
-          z_s[tid] = use_staged ? st.ctx[st.item_req[item] * kCtx + tid - kDModel - kEmbed] : 0.0f;
-        }
-        named_bar_sync(1, kRowThreads);
-        if (tid < kHidden) {
-          float h = 0.0f;
-          for (int i = 0; i < kDModel + kEmbed + kCtx; ++i) h = fmaf(z_s[i], __ldg(p.head_w1 + i * kHidden + tid), h);
-          hid_s[tid] = fmaxf(h + __ldg(p.head_b1 + tid), 0.0f);
-        }
-        named_bar_sync(1, kRowThreads);
-        if (tid < kHeads) {
-          float o = 0.0f;
-          for (int j = 0; j < kHidden; ++j) o = fmaf(hid_s[j], __ldg(p.head_w2 + j * kHeads + tid), o);
-          logits[(size_t)item * kHeads + tid] = o + __ldg(p.head_b2 + tid);
-        }
+      if (tid < kHidden) {
+        float h = 0.0f;
+        for (int i = 0; i < kDModel + kEmbed + kCtx; ++i) h = fmaf(z_s[i], __ldg(p.head_w1 + i * kHidden + tid), h);
+        hid_s[tid] = fmaxf(h + __ldg(p.head_b1 + tid), 0.0f);
       }
-      named_bar_sync(1, kRowThreads);  // smem (valid_s, red_s, z_s) reuse by the next item
+      named_bar_sync(1, kRowThreads);
+      if (tid < kHeads) {
+        float o = 0.0f;
+        for (int j = 0; j < kHidden; ++j) o = fmaf(hid_s[j], __ldg(p.head_w2 + j * kHeads + tid), o);
+        logits[(size_t)item * kHeads + tid] = o + __ldg(p.head_b2 + tid);
+      }
     }
+    named_bar_sync(1, kRowThreads);  // smem (valid_w, red_s, z_s) reuse by the next item
+  }
+  if (issuer) {  // drain the last prefetches before the CTA retires
+    is.need_wa();
+    is.need_wb();
   }
   fence_before();
   __syncthreads();
-  if (warp == kSkRowWarps) tmem_free<512>(T);
+  if (warp == 0) tmem_free<512>(T);
 }
 
 cudaError_t launch_skut_tc(const Params& p, const SkutImages& img, const NNCfg& nn,
@@ -546,7 +610,14 @@ cudaError_t launch_skut_tc(const Params& p, const SkutImages& img, const NNCfg& 
   Staged dummy{};
   skut_tc_kernel<<<n < sms ? n : sms, kSkThreads, smem, s>>>(p, img, nn, st ? *st : dummy, st != nullptr, idx,
                                                             F, fmask, n, U, logits, pooled);
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, skut_tc_kernel);
+    fprintf(stderr, "skut_tc launch failed: regs=%d maxThreads=%d static_smem=%zu dyn_smem=%zu local=%zu\n",
+            fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, smem, fa.localSizeBytes);
+  }
+  return e;
 }
 
 }  // namespace tav2
