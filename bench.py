@@ -120,56 +120,65 @@ class Clocks:
 # CPU reference arm (oracle port of the reference path), one process per core
 # ---------------------------------------------------------------------------
 
-def _cpu_worker(args):
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    seed, n_cand, L, nn, reps = args
+_CPU_STATE = {}
+
+
+def _cpu_init(seed, n_cand, L, nn):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
     import paper_2506_02267_b200 as P
     from oracle import seqrank_oracle as orc
     r = P.generate_requests(1, n_cand, ll_tokens=L, seed=seed)[0]
     user = {f"{s}_{c}": getattr(b, a) for s, b in zip(("ll", "rt", "imp"), r.user.blocks())
             for c, a in (("emb", "embeddings"), ("action", "actions"), ("surface", "surfaces"),
                          ("ts", "timestamps"))}
-    Pd = orc.model_init(0, seq_len=sum(nn))
-    lat = []
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        t = time.perf_counter()
-        orc.rank_request(user, r.candidates, r.ctx, Pd, nn)
-        lat.append(time.perf_counter() - t)
-    return n_cand * reps, time.perf_counter() - t0, lat
+    _CPU_STATE.update(orc=orc, user=user, cands=r.candidates, ctx=r.ctx, nn=nn,
+                      P=orc.model_init(0, seq_len=sum(nn)))
 
 
-def cpu_baseline(cfg_name, seconds_budget=12.0, procs=None):
-    """Bounded sample: each process scores `n` candidates of a full-length
-    request (L as configured) `reps` times; aggregate cand/s over all cores."""
-    reqs, n_cand, L, nn = CONFIGS[cfg_name]
+def _cpu_step(_):
+    """One bounded sample: the oracle port of the reference path over this
+    process's candidate slice of a full-length request."""
+    st = _CPU_STATE
+    t = time.perf_counter()
+    st["orc"].rank_request(st["user"], st["cands"], st["ctx"], st["P"], st["nn"])
+    return len(st["cands"]), time.perf_counter() - t
+
+
+def cpu_baseline(cfg_name, steps=3, warmup=1, budget_s=60.0, procs=None, n_per_proc=250):
+    """Reference CPU path (oracle port; the Python reference cannot travel to
+    the GPU box) in one process per host core, OPENBLAS_NUM_THREADS=1.  A step
+    = every process scores `n_per_proc` candidates of a full-length request
+    once; timed steps stop early when `budget_s` is spent (reported)."""
+    _, n_cand, L, nn = CONFIGS[cfg_name]
     procs = procs or os.cpu_count() or 1
-    n = min(n_cand, 250)  # ~1 s per process per rep at ~250 cand/s/core (SURVEY §6)
-    env_old = os.environ.get("OPENBLAS_NUM_THREADS")
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    n = min(n_cand, n_per_proc)
     ctx = mp.get_context("spawn")
-    with ctx.Pool(procs) as pool:
-        # calibrate one rep on one process first (bounded), then size reps
-        done, secs, _ = pool.apply(_cpu_worker, ((0, n, L, nn, 1),))
-        per = secs / 1
-        reps = max(1, int(seconds_budget / max(per, 1e-3)))
-        reps = min(reps, 8)
-        t0 = time.perf_counter()
-        res = pool.map(_cpu_worker, [(i, n, L, nn, reps) for i in range(procs)])
-        wall = time.perf_counter() - t0
-    if env_old is None:
-        os.environ.pop("OPENBLAS_NUM_THREADS", None)
-    else:
-        os.environ["OPENBLAS_NUM_THREADS"] = env_old
-    total = sum(r[0] for r in res)
-    lats = [x for r in res for x in r[2]]
+    old = os.environ.get("OPENBLAS_NUM_THREADS")
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    try:
+        with ctx.Pool(procs, initializer=_cpu_init, initargs=(0, n, L, nn)) as pool:
+            for _ in range(max(1, min(warmup, 2))):
+                pool.map(_cpu_step, range(procs))
+            done, lats, wall, k = 0, [], 0.0, 0
+            while k < max(1, steps) and (k == 0 or wall < budget_s):
+                t0 = time.perf_counter()
+                res = pool.map(_cpu_step, range(procs))
+                wall += time.perf_counter() - t0
+                done += sum(r[0] for r in res)
+                lats += [r[1] for r in res]
+                k += 1
+    finally:
+        if old is None:
+            os.environ.pop("OPENBLAS_NUM_THREADS", None)
+        else:
+            os.environ["OPENBLAS_NUM_THREADS"] = old
     return {
-        "value": total / wall, "unit": UNIT, "cores": procs, "kind": "port",
-        "sample": (f"{procs} processes x {reps} reps x {n} candidates of one L={L} request "
+        "value": done / wall, "unit": UNIT, "cores": procs, "kind": "port", "steps_timed": k,
+        "sample": (f"{procs} processes x {k} steps x {n} candidates of one L={L} request "
                    f"(oracle port of build_dedup_batch->fused_assemble->encode_batch->forward_fused"
-                   f"->pool->head, OPENBLAS_NUM_THREADS=1); {wall:.1f}s wall"),
+                   f"->pool->head, OPENBLAS_NUM_THREADS=1); {wall:.1f}s timed wall"),
         "per_process_cand_s": n / statistics.median(lats),
-        "request_ms_p50_for_sample": 1e3 * sorted(lats)[len(lats) // 2],
+        "p50_sample_ms": 1e3 * statistics.median(lats),
     }
 
 
@@ -325,23 +334,21 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        steps_rates = []
-        cb = None
-        for i in range(args.warmup + args.steps):
-            if i < args.warmup:
-                continue
-            cb = cpu_baseline(args.config, seconds_budget=4.0)
-            steps_rates.append(cb["value"])
-        value = statistics.median(steps_rates)
         n_req, n_cand, L, nn_t = CONFIGS[args.config]
+        cb = cpu_baseline(args.config, steps=args.steps, warmup=args.warmup, budget_s=90.0)
+        value = cb["value"]
         print(json.dumps({
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "impl": "reference",
-            "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "fp32/f64 (numpy)", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {n_req} request(s) x {n_cand} candidates, L={L}, NNConfig{nn_t}"},
-            "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cb["cores"], "kind": "port",
-                             "sample": cb["sample"]},
-            "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "n_gpus": 0, "steps": cb["steps_timed"], "warmup": min(args.warmup, 2),
+            "ms_per_step": round(1e3 * n_cand / value, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64 (numpy)",
+            "data": "synthetic (generate_requests), random-init weights seed 0",
+            "config": {"workload": f"{args.config}: {n_req} request(s) x {n_cand} candidates, L={L}, "
+                                   f"NNConfig{nn_t} (CPU: bounded candidate sample per process)"},
+            "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cb["cores"],
+                             "kind": "port", "sample": cb["sample"]},
+            "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
         }))
         return
 
@@ -351,7 +358,7 @@ def main():
     out = run_gpu(args, rank, world, local_rank)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
-            cb = cpu_baseline(args.config)
+            cb = cpu_baseline(args.config, steps=3, warmup=1, budget_s=20.0)
             out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         print(json.dumps(out))
     if world > 1:
