@@ -25,7 +25,7 @@ EXPORTS = (
     "tav2_create", "tav2_destroy", "tav2_load_params", "tav2_stage", "tav2_nn_select",
     "tav2_encode", "tav2_forward", "tav2_score", "tav2_rank", "tav2_run_staged",
     "tav2_last_launch_count", "tav2_last_error", "tav2_build_info", "tav2_set_profiling",
-    "tav2_kernel_times", "tav2_tc_selftest",
+    "tav2_kernel_times", "tav2_tc_selftest", "tav2_debug_timeline",
 )
 
 
@@ -90,6 +90,7 @@ def lib() -> ctypes.CDLL:
             L.tav2_kernel_times.argtypes = [vp, ctypes.POINTER(ctypes.c_char_p),
                                             ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32),
                                             ctypes.c_int]
+            L.tav2_debug_timeline.argtypes = [vp, ctypes.c_int]
             L.tav2_tc_selftest.argtypes = [ctypes.c_int, vp, vp, vp, ctypes.c_int, ctypes.c_int, vp]
             L.tav2_last_error.restype = ctypes.c_char_p
             L.tav2_build_info.restype = ctypes.c_char_p

@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include "tav2_common.cuh"
+#include "tc_common.cuh"
 
 namespace tav2 {
 
@@ -46,14 +47,25 @@ __global__ void __launch_bounds__(256) prep_kernel(Staged st) {
     }
     float nrm = __fsqrt_rn(sumsq8(d));
     if (nrm == 0.0f) nrm = 1.0f;
+    float u[kEmbed];
+#pragma unroll
+    for (int j = 0; j < kEmbed; ++j) u[j] = __fdiv_rn(d[j], nrm);
     float4* dst = reinterpret_cast<float4*>(st.tok_unit + (size_t)i * kEmbed);
 #pragma unroll
-    for (int j = 0; j < kEmbed; j += 4)
-      dst[j / 4] = make_float4(__fdiv_rn(d[j], nrm), __fdiv_rn(d[j + 1], nrm),
-                               __fdiv_rn(d[j + 2], nrm), __fdiv_rn(d[j + 3], nrm));
-    const double rn = isq ? 7.450580596923828125e-9 / sqrt((double)isq) : 0.0;  // 2^-27/||q||
-    st.tok_rnorm[i] = rn;
-    st.tok_rnorm_f[i] = (float)rn;
+    for (int j = 0; j < kEmbed; j += 4) dst[j / 4] = make_float4(u[j], u[j + 1], u[j + 2], u[j + 3]);
+    // bf16 hi/lo image of the unit row, pre-tiled for the tensor-core NN
+    // scores: 64-token tiles of 8 KB = [8 chunks (hi 0-3, lo 4-7)][64 rows][16 B]
+    // (the UMMA K-major no-swizzle B-operand layout), one bulk copy per tile
+    uint8_t* tile = reinterpret_cast<uint8_t*>(st.tok_bf16) + (size_t)(i >> 6) * 8192 + (i & 63) * 16;
+#pragma unroll
+    for (int j = 0; j < kEmbed; j += 8) {
+      uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) tc::split_pair(u[j + 2 * e], u[j + 2 * e + 1], hi[e], lo[e]);
+      *reinterpret_cast<uint4*>(tile + (j / 8) * 1024) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4*>(tile + (4 + j / 8) * 1024) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+    (void)isq;
     return;
   }
   i -= st.n_tok;

@@ -56,7 +56,7 @@ struct tav2_ctx {
   int kmax = 1;
   int max_tiles = 0, max_work = 0;
   int sms = 148;
-  CUtensorMap emb_map{};
+
   // pinned host arena + device mirror of the staged region
   unsigned char* h_arena = nullptr;
   unsigned char* d_staged = nullptr;
@@ -64,11 +64,12 @@ struct tav2_ctx {
   cudaEvent_t ev_staged = nullptr;
   // derived device buffers
   float* tok_unit = nullptr;
-  double* tok_rnorm = nullptr;
+  uint32_t* tok_bf16 = nullptr;
   float* cand_unit = nullptr;
   uint64_t* part = nullptr;
-  float* part1 = nullptr;      // pass-1 per-chunk m-th best approx score (two-pass NN)
-  float* tok_rnorm_f = nullptr;
+  float* part1 = nullptr;      // pass-1 per-chunk top-8 lists (two column halves)
+  float* bound = nullptr;      // [max_items][3] pass-2 gate bound per (candidate, source)
+
   int32_t* idx = nullptr;
   float* logits = nullptr;
   float* skut_scratch = nullptr;
@@ -111,8 +112,7 @@ Staged staged_view(tav2_ctx* c) {
   s.surface = reinterpret_cast<const uint8_t*>(b + p.off_surface);
   s.emb = reinterpret_cast<const int8_t*>(b + p.off_emb);
   s.tok_unit = c->tok_unit;
-  s.tok_rnorm = c->tok_rnorm;
-  s.tok_rnorm_f = c->tok_rnorm_f;
+  s.tok_bf16 = c->tok_bf16;
   s.cand_unit = c->cand_unit;
   s.n_req = p.n_req;
   s.n_items = p.n_items;
@@ -141,11 +141,11 @@ int free_all(tav2_ctx* c) {
   cudaFreeHost(c->h_arena);
   cudaFree(c->d_staged);
   cudaFree(c->tok_unit);
-  cudaFree(c->tok_rnorm);
+  cudaFree(c->tok_bf16);
   cudaFree(c->cand_unit);
   cudaFree(c->part);
   cudaFree(c->part1);
-  cudaFree(c->tok_rnorm_f);
+  cudaFree(c->bound);
   cudaFree(c->idx);
   cudaFree(c->logits);
   cudaFree(c->skut_scratch);
@@ -258,16 +258,18 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
   if ((e = cudaSetDevice(device)) != cudaSuccess) return bad(e, "cudaSetDevice");
   if ((e = cudaMallocHost(&c->h_arena, c->staged_cap)) != cudaSuccess) return bad(e, "pinned arena");
   if ((e = cudaMalloc(&c->d_staged, c->staged_cap)) != cudaSuccess) return bad(e, "staged region");
-  if ((e = cudaMalloc(&c->tok_unit, std::max<int64_t>(T, 1) * kEmbed * 4)) != cudaSuccess)
+  // padded to whole 64-token tiles (+1): the NN kernel bulk-copies full tiles
+  if ((e = cudaMalloc(&c->tok_unit, (size_t)(cdiv((int)std::max<int64_t>(T, 1), 64) + 1) * 64 * kEmbed * 4)) !=
+      cudaSuccess)
     return bad(e, "tok_unit");
-  if ((e = cudaMalloc(&c->tok_rnorm, std::max<int64_t>(T, 1) * 8)) != cudaSuccess) return bad(e, "tok_rnorm");
+  if ((e = cudaMalloc(&c->tok_bf16, (size_t)(cdiv((int)std::max<int64_t>(T, 1), 64) + 1) * 8192)) != cudaSuccess)
+    return bad(e, "tok_bf16");
   if ((e = cudaMalloc(&c->cand_unit, (size_t)N * kEmbed * 4)) != cudaSuccess) return bad(e, "cand_unit");
   if ((e = cudaMalloc(&c->part, (size_t)c->max_work * c->kmax * kTile * 8)) != cudaSuccess)
     return bad(e, "partial top-k");
-  if ((e = cudaMalloc(&c->part1, (size_t)c->max_work * kTile * 4)) != cudaSuccess)
-    return bad(e, "pass-1 bounds");
-  if ((e = cudaMalloc(&c->tok_rnorm_f, std::max<int64_t>(T, 1) * 4)) != cudaSuccess)
-    return bad(e, "tok_rnorm_f");
+  if ((e = cudaMalloc(&c->part1, (size_t)c->max_work * kTile * 16 * 4)) != cudaSuccess)
+    return bad(e, "pass-1 lists");
+  if ((e = cudaMalloc(&c->bound, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "pass-2 bounds");
   if ((e = cudaMalloc(&c->idx, (size_t)N * S * 4)) != cudaSuccess) return bad(e, "idx");
   if ((e = cudaMalloc(&c->logits, (size_t)N * kHeads * 4)) != cudaSuccess) return bad(e, "logits");
   {
@@ -442,17 +444,31 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
   if (T > c->cap.max_tokens)
     return fail(TAV2_ECAP, "%lld tokens exceed capacity %lld", (long long)T, (long long)c->cap.max_tokens);
 
-  // ---- NN work decomposition: one CTA per work unit; LL chunks sized so
-  // the units fill the SMs once, bounded by the merge capacity ----
+  // ---- NN work decomposition: one CTA per (candidate tile, source, chunk).
+  // The two-pass tensor-core NN (nn_tc.cu) keeps two register top-8 lists per
+  // chunk, so a chunked source needs max(2, ceil(k/16)) <= nch <= 32 (bound
+  // kernel holds <= 512 values), nch*k <= kMergeCap (merge) and >= 64 tokens
+  // per chunk; otherwise one exact chunk.  RT tail and IMP take the smallest
+  // legal count; LL chunks are sized so that all units fill the SMs. ----
+  auto chunk_range = [&](int s, int len, int& lo_n, int& hi_n) {
+    const int k = nn.k[s];
+    lo_n = std::max(2, cdiv(k, 16));
+    hi_n = std::min(std::min(32, kMergeCap / std::max(k, 1)), len / 64);
+  };
+  auto rt_imp_chunks = [&](int s, int len) {
+    int a, b;
+    chunk_range(s, len, a, b);
+    return a <= b ? a : 1;
+  };
   int other = 0;
   for (int r = 0; r < n_req; ++r) {
     const int t = cdiv(reqs[r].n_cand, kTile);
-    other += t * ((nn.k[1] > 0 && reqs[r].len[1] > nn.recent) + (nn.k[2] > 0 && reqs[r].len[2] > 0));
+    if (nn.k[1] > 0 && reqs[r].len[1] > nn.recent) other += t * rt_imp_chunks(1, reqs[r].len[1] - nn.recent);
+    if (nn.k[2] > 0 && reqs[r].len[2] > 0) other += t * rt_imp_chunks(2, reqs[r].len[2]);
   }
   const int ll_chunks_target = std::max(1, (c->sms - other) / std::max(tiles, 1));
   std::vector<NNTile> vt;
   std::vector<NNWork> vw;
-  int min_nw = 1 << 30;  // fewest chunks of any chunked LL source
   vt.reserve(tiles);
   {
     int item = 0;
@@ -472,12 +488,12 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
           if (nn.k[s] == 0 || hi <= lo) continue;
           int nch = 1;
           if (s == 0) {
-            // two-pass NN (nn_tc.cu) needs ceil(k/nch)+2 <= 16 register slots and the
-            // merge needs nch*k <= kMergeCap; otherwise one exact chunk
-            nch = std::max(1, std::min(ll_chunks_target, cdiv(hi - lo, kMinChunk)));
-            if (nch > 1) nch = std::max(nch, cdiv(nn.k[0], 16));
-            if (nch > 1 && (nch * nn.k[0] > kMergeCap || (hi - lo) / nch < 16)) nch = 1;
-            if (nch > 1) min_nw = std::min(min_nw, nch);
+            int a, b;
+            chunk_range(0, hi - lo, a, b);
+            nch = std::min(std::max(ll_chunks_target, a), b);
+            if (a > b || nch < 2) nch = 1;
+          } else {
+            nch = rt_imp_chunks(s, hi - lo);
           }
           int step = cdiv(hi - lo, nch);
           for (int a = lo; a < hi; a += step) {
@@ -500,7 +516,7 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
   p.n_tiles = (int)vt.size();
   p.n_work = (int)vw.size();
   p.tile_size = kTile;
-  p.p1_m = (min_nw == (1 << 30) || min_nw * 8 >= nn.k[0]) ? 8 : 16;
+  p.p1_m = 16;
   int64_t o = 0;
   p.off_req = o; o = align256(o + (int64_t)n_req * sizeof(ReqInfo));
   p.off_tiles = o; o = align256(o + (int64_t)p.n_tiles * sizeof(NNTile));
@@ -552,8 +568,6 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
   if (!vw.empty()) memcpy(h + p.off_work, vw.data(), vw.size() * sizeof(NNWork));
 
   CU(cudaSetDevice(c->device));
-  if (T > 0 && !make_rows32_map(&c->emb_map, c->d_staged + p.off_emb, T, 64))
-    return fail(TAV2_ECUDA, "cuTensorMapEncodeTiled failed for the token arena");
   CU(cudaMemcpyAsync(c->d_staged, h, p.bytes, cudaMemcpyHostToDevice, s));
   CU(cudaEventRecord(c->ev_staged, s));
   c->plan = p;
@@ -581,10 +595,11 @@ int run_nn(tav2_ctx* c, int mode, int32_t* idx, float* scores, cudaStream_t s) {
     CU(timed(c, "nn_simt", s, [&] { return launch_nn_simt(st, c->nn, c->part, c->kmax, kTile, s); }));
   } else {
     CU(timed(c, "nn_tc_pass1", s, [&] {
-      return launch_nn_tc(st, c->nn, c->emb_map, c->part, c->part1, c->kmax, kTile, 1, s);
+      return launch_nn_tc(st, c->nn, c->part, c->part1, c->bound, c->kmax, kTile, 1, s);
     }));
+    CU(timed(c, "nn_bound", s, [&] { return launch_nn_bound(st, c->nn, c->part1, c->bound, kTile, s); }));
     CU(timed(c, "nn_tc_pass2", s, [&] {
-      return launch_nn_tc(st, c->nn, c->emb_map, c->part, c->part1, c->kmax, kTile, 2, s);
+      return launch_nn_tc(st, c->nn, c->part, c->part1, c->bound, c->kmax, kTile, 2, s);
     }));
   }
   CU(timed(c, "nn_merge", s,
@@ -697,6 +712,10 @@ int tav2_rank(tav2_ctx* c, const tav2_request* reqs, int n_req, int mode, float*
 }
 
 int tav2_last_launch_count(const tav2_ctx* c) { return c ? c->launches : 0; }
+
+int tav2_debug_timeline(long long* dev, int block) {
+  return set_debug_timeline(dev, block) == cudaSuccess ? TAV2_OK : fail(TAV2_ECUDA, "debug timeline");
+}
 
 int tav2_set_profiling(tav2_ctx* c, int on) {
   if (!c) return fail(TAV2_EINVAL, "null context");

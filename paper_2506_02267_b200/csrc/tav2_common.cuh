@@ -110,8 +110,7 @@ struct Staged {
   const uint8_t* surface;  // [T]
   const int8_t* emb;       // [T, 32]
   float* tok_unit;         // [T, 32] derived: unit(dequantize(q)) (core.py:77-79)
-  double* tok_rnorm;       // [T]     derived: 2^-27 / ||q||_2 of the int8 row (i8-limb path)
-  float* tok_rnorm_f;      // [T]     the same in f32 (approximate pre-filter)
+  uint32_t* tok_bf16;      // derived: unit rows as bf16 hi/lo, 64-token tiles of 8 KB (prep_kernel)
   float* cand_unit;        // [N, 32] derived: l2_normalize_rows(cand)
   int n_req, n_items, n_tok, n_tiles, n_work;
   int p1_m;                // pass-1 list size of the two-pass NN (8 or 16)
@@ -233,10 +232,13 @@ namespace tav2 {
 cudaError_t launch_prep(const Staged& st, cudaStream_t s);
 cudaError_t launch_nn_simt(const Staged& st, const NNCfg& nn, uint64_t* part, int kmax,
                            int tile_size, cudaStream_t s);
-cudaError_t launch_nn_tc(const Staged& st, const NNCfg& nn, const CUtensorMap& emb_map,
-                         uint64_t* part, float* part1, int kmax, int tile_size, int pass,
-                         cudaStream_t s);
+cudaError_t launch_nn_tc(const Staged& st, const NNCfg& nn, uint64_t* part, float* part1,
+                         const float* bound, int kmax, int tile_size, int pass, cudaStream_t s);
+cudaError_t launch_nn_bound(const Staged& st, const NNCfg& nn, const float* part1, float* bound,
+                            int tile_size, cudaStream_t s);
+cudaError_t set_debug_timeline(long long* dev, int block);
 bool make_rows32_map(CUtensorMap* map, const void* base, int64_t rows, int box_rows);
+
 cudaError_t launch_nn_merge(const Staged& st, const NNCfg& nn, const uint64_t* part, int kmax,
                             int tile_size, int32_t* idx, float* scores, cudaStream_t s);
 cudaError_t launch_encode(const Staged& st, const NNCfg& nn, const Params& p, const int32_t* idx,
