@@ -15,8 +15,9 @@ extern "C" {
  * row-major device buffers; D: [128, N] f32 (s32 for i8).  Synchronous. */
 int tav2_tc_selftest(int which, const void* A, const void* B, void* D, int N, int K, void* stream);
 
-/* Debug: device buffer (>= 256 int64) receiving %globaltimer stamps of the
- * first NN work unit's CTA (NULL disables).  Not thread-safe. */
+/* Debug: device buffer (>= 512 int64) receiving %globaltimer stamps of NN
+ * work unit `block`'s CTA (slots 0..319) and of SKUT CTA 0's first
+ * candidate (slots 320..447).  NULL disables.  Not thread-safe. */
 int tav2_debug_timeline(long long* dev, int block);
 
 #ifdef __cplusplus

@@ -49,6 +49,16 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr uint32_t kColA = 384, kColQKV = 0, kColS1 = 128, kColWo = 0, kColW1 = 128, kColA2 = 192,
                    kColW2 = 256, kColOut = 0;
 
+// Debug timeline (tav2_debug_timeline): %globaltimer stamps of CTA 0's
+// first candidate: slot 2p = SIMT phase p done (thread 0), 2p+1 = MMA phase p
+// issued; 64 + p = MMA phase p observed complete by thread 0.
+__device__ long long* g_dbg_skut = nullptr;
+__device__ __forceinline__ long long sk_time() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ---- row-thread helpers (warp-collective TMEM access) ----
 __device__ __forceinline__ void ld64(uint32_t ta, float* v) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
@@ -136,8 +146,10 @@ struct Issuer {
     ph_simt ^= 1;
     fence_after();
   }
+  long long* dbg = nullptr;
   __device__ void commit_mma() {
     commit(bar_mma);
+    if (dbg && n_mma < 32) dbg[2 * n_mma + 1] = sk_time();
     ++n_mma;
   }
   __device__ void wait_mma() { mbar_wait(bar_mma, (n_mma - 1) & 1); }
@@ -219,6 +231,9 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
   __shared__ float z_s[kDModel + kEmbed + kCtx];
   __shared__ float hid_s[kHidden];
   __shared__ int any_s;
+  __shared__ unsigned kmax_s[kMaxLayers];  // per layer: max over rows of ||k_r||^2 (f32 bits)
+  __shared__ float qn2_s[256];             // ||q_r||^2 per row (softmax shift)
+  __shared__ float lsum_s[2][256];         // softmax row sums: [owner warp | helper warp]
 
   const int S = nn.seq_len;
   const int S_pad = (S + 15) & ~15;
@@ -268,6 +283,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
     is.bar_wb = &bar_wb;
     is.NT = NT;
     is.S_pad = S_pad;
+    is.dbg = blockIdx.x == 0 ? g_dbg_skut : nullptr;
     is.load_wa(img.wa[0], kImgWA);
     is.load_wb(img.wb[0]);
   }
@@ -277,16 +293,20 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
   const uint32_t lanebase = T + ((uint32_t)(32 * q) << 16);
   const uint32_t cA = lanebase + kColA + 64 * t;
   const bool in_seq = r < S;
-  uint32_t n_mma = 0;
+  uint32_t n_mma = 0, n_done = 0;
+  long long* dbg = (blockIdx.x == 0 && tid == 0) ? g_dbg_skut : nullptr;
   auto wait_mma = [&]() {
     __syncwarp();
     mbar_wait_sleep(&bar_mma, n_mma & 1);
+    if (dbg && n_mma < 64) dbg[64 + n_mma] = sk_time();
     ++n_mma;
     fence_after();
   };
   auto done = [&]() {
     fence_before();
     mbar_arrive(&bar_simt);
+    if (dbg && n_done < 32) dbg[2 * n_done] = sk_time();
+    ++n_done;
   };
 
   for (int item = blockIdx.x; item < n; item += gridDim.x) {
@@ -317,11 +337,13 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
     {
       const unsigned b = __ballot_sync(0xffffffffu, ok);
       if (lane == 0) valid_w[warp] = b;
+      if (tid < kMaxLayers) kmax_s[tid] = 0u;
     }
     named_bar_sync(1, kRowThreads);
     const int wmax_row = 128 * t + 32 * q + 31;  // warp-uniform causal bound
 
     for (int L = 0; L < NL; ++L) {
+      float qn2 = 0.0f;  // ||q_r||^2 of this row (QKV epilogue -> softmax)
       // ---- LN1 -> A ----
       {
         float y[kDModel];
@@ -348,6 +370,8 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
       {
         const uint32_t cq = lanebase + kColQKV + 192 * t;
         float v[32];
+        qn2 = 0.0f;
+        float kn2 = 0.0f;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           ld32f(cq + 32 * h, v);
@@ -355,6 +379,8 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = 0.0f;
           }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) qn2 = fmaf(v[i], v[i], qn2);
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
             uint32_t hi[8], lo[8];
@@ -373,12 +399,19 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
               for (int i = 0; i < 32; ++i) v[i] = 0.0f;
             }
 #pragma unroll
+            for (int i = 0; i < 32; ++i) kn2 = fmaf(v[i], v[i], kn2);
+#pragma unroll
             for (int c = 0; c < 4; ++c) {
               const int off = (4 * h + c) * (S_pad * 16) + r * 16;
               split8_store(Khi + off, Klo + off, v + 8 * c);
             }
           }
         }
+        // max_j ||k_j||^2 over the valid keys: shift bound of the softmax below
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) kn2 = fmaxf(kn2, __shfl_xor_sync(0xffffffffu, kn2, o));
+        if (lane == 0) atomicMax(&kmax_s[L], __float_as_uint(kn2));
+        qn2_s[r] = qn2;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {  // V: MN-major (key r, d) at (r/8)*1024 + (d/8)*128 + (r%8)*16 + (d%8)*2
           ld32f(cq + 128 + 32 * h, v);
@@ -404,47 +437,70 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
         is.commit_mma();
       }
       // ---- causal key-masked softmax -> P (bf16 hi/lo, in place over S) ----
+      // Single pass: softmax is shift invariant, so instead of the row max we
+      // subtract its Cauchy-Schwarz bound m' = ||q_r|| max_j ||k_j|| / 8 >=
+      // q_r.k_j / 8 (m' - max stays far inside the f32 exp range for
+      // LN-scaled activations; 1/l normalises exactly as encoder.py:203-211).
+      // No row max also means a row's key chunks can be split across the two
+      // warps that share its TMEM lanes (q and q+4): the chunks of tile-0 rows
+      // 32q.. and tile-1 rows 128+32q.. are dealt out evenly between them and
+      // the two partial row sums are combined through shared memory.
       wait_mma();
-      float inv_l = 0.0f;
       {
-        const int nk = t == 0 ? (S_pad < 128 ? S_pad : 128) : S_pad;
-        const uint32_t cs = lanebase + (t == 0 ? 0u : kColS1);
-        const int jlast = min(nk / 16 - 1, wmax_row / 16);  // chunks any row of the warp needs
-        float m = -INFINITY;
-        for (int j = 0; j <= jlast; ++j) {
-          uint32_t s16[16];
-          tmem_ld16(cs + 16 * j, s16);
-          const uint32_t vm = allowed16(valid_w[j >> 1] >> ((j & 1) * 16), 16 * j, r);
-          tmem_ld_wait();
+        named_bar_sync(1, kRowThreads);  // kmax_s[L], qn2_s complete
+        const float kmax2 = __uint_as_float(kmax_s[L]);
+        const int nkt[2] = {S_pad < 128 ? S_pad : 128, S_pad};
+        const int nA = 32 * q < S ? min(nkt[0] / 16, (32 * q + 31) / 16 + 1) : 0;        // tile-0 chunks
+        const int nB = 128 + 32 * q < S ? min(nkt[1] / 16, (128 + 32 * q + 31) / 16 + 1) : 0;  // tile-1
+        const int half = (nA + nB + 1) / 2;
+        const int s0 = t == 0 ? 0 : half, s1 = t == 0 ? half : nA + nB;  // this warp's chunk slots
+        float lpart[2] = {0.0f, 0.0f};
 #pragma unroll
-          for (int e = 0; e < 16; ++e)
-            if ((vm >> e) & 1u) m = fmaxf(m, __uint_as_float(s16[e]));
-        }
-        const float mb = (m == -INFINITY ? 0.0f : m) * (0.125f * kLog2e);  // scale 1/sqrt(64)
-        float l = 0.0f;
-        for (int j = 0; j < nk / 16; ++j) {
-          uint32_t hi[8], lo[8];
-          if (j <= jlast) {
-            uint32_t s16[16];
-            tmem_ld16(cs + 16 * j, s16);
-            const uint32_t vm = ok ? allowed16(valid_w[j >> 1] >> ((j & 1) * 16), 16 * j, r) : 0u;
+        for (int tt = 0; tt < 2; ++tt) {
+          const int base = tt == 0 ? 0 : nA;
+          const int j_lo = max(s0 - base, 0), j_hi = min(s1 - base, tt == 0 ? nA : nB);
+          const int rr = 128 * tt + 32 * q + lane;
+          const bool okr = (valid_w[rr >> 5] >> lane) & 1u;
+          const float mb = sqrtf(qn2_s[rr] * kmax2) * (0.125f * kLog2e);
+          const uint32_t cs = lanebase + (tt == 0 ? 0u : kColS1);
+          for (int j0 = j_lo; j0 < j_hi; j0 += 2) {
+            uint32_t s32[32];
+            const bool two = j0 + 1 < j_hi;  // warp-uniform
+            tmem_ld16(cs + 16 * j0, s32);
+            if (two) tmem_ld16(cs + 16 * (j0 + 1), s32 + 16);
             tmem_ld_wait();
-            float pv[16];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              pv[e] = ((vm >> e) & 1u) ? exp2f(fmaf(__uint_as_float(s16[e]), 0.125f * kLog2e, -mb)) : 0.0f;
-              l += pv[e];
+            for (int u = 0; u < 2; ++u) {
+              const int j = j0 + u;
+              if (u == 1 && !two) break;
+              const uint32_t vm = okr ? allowed16(valid_w[j >> 1] >> ((j & 1) * 16), 16 * j, rr) : 0u;
+              float pv[16];
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                float p;
+                asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p) : "f"(fmaf(__uint_as_float(s32[16 * u + e]), 0.125f * kLog2e, -mb)));
+                pv[e] = ((vm >> e) & 1u) ? p : 0.0f;
+                lpart[tt] += pv[e];
+              }
+              uint32_t hi[8], lo[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) split_pair(pv[2 * i], pv[2 * i + 1], hi[i], lo[i]);
+              tmem_st8(cs + 16 * j, hi);
+              tmem_st8(cs + 16 * j + 8, lo);
             }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) split_pair(pv[2 * i], pv[2 * i + 1], hi[i], lo[i]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) hi[i] = lo[i] = 0u;
           }
-          tmem_st8(cs + 16 * j, hi);
-          tmem_st8(cs + 16 * j + 8, lo);
         }
-        inv_l = l > 0.0f ? 1.0f / l : 0.0f;  // a valid row always sees itself
+        // the row owner zero-fills its tile's chunks past the causal range
+        {
+          const uint32_t cs = lanebase + (t == 0 ? 0u : kColS1);
+          const uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          for (int j = t == 0 ? nA : nB; j < nkt[t] / 16; ++j) {
+            tmem_st8(cs + 16 * j, z);
+            tmem_st8(cs + 16 * j + 8, z);
+          }
+        }
+        lsum_s[0][r] = lpart[t];                          // owner's part of row r
+        lsum_s[1][128 * (1 - t) + 32 * q + lane] = lpart[1 - t];  // helper's part of the other tile's row
         tmem_st_wait();
         done();
       }
@@ -456,6 +512,9 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
       // ---- O / l -> A ----
       wait_mma();
       {
+        named_bar_sync(1, kRowThreads);  // lsum_s complete
+        const float l = lsum_s[0][r] + lsum_s[1][r];
+        const float inv_l = l > 0.0f ? 1.0f / l : 0.0f;  // a valid row always sees itself
         float o[kDModel];
         ld64(cA, o);
 #pragma unroll
@@ -594,6 +653,8 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
   __syncthreads();
   if (warp == 0) tmem_free<512>(T);
 }
+
+cudaError_t set_debug_skut(long long* dev) { return cudaMemcpyToSymbol(g_dbg_skut, &dev, sizeof(dev)); }
 
 cudaError_t launch_skut_tc(const Params& p, const SkutImages& img, const NNCfg& nn,
                            const Staged* st, const int32_t* idx, const float* F,

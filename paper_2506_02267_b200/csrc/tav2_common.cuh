@@ -237,6 +237,7 @@ cudaError_t launch_nn_tc(const Staged& st, const NNCfg& nn, uint64_t* part, floa
 cudaError_t launch_nn_bound(const Staged& st, const NNCfg& nn, const float* part1, float* bound,
                             int tile_size, cudaStream_t s);
 cudaError_t set_debug_timeline(long long* dev, int block);
+cudaError_t set_debug_skut(long long* dev);
 bool make_rows32_map(CUtensorMap* map, const void* base, int64_t rows, int box_rows);
 
 cudaError_t launch_nn_merge(const Staged& st, const NNCfg& nn, const uint64_t* part, int kmax,
