@@ -141,8 +141,11 @@ struct Issuer {
   uint8_t *WA, *WB;
   int NT, S_pad;
 
+  int n_ws = 0;
   __device__ void wait_simt() {
     mbar_wait(bar_simt, ph_simt);
+    if (dbg && n_ws < 32) dbg[160 + n_ws] = sk_time();
+    ++n_ws;
     ph_simt ^= 1;
     fence_after();
   }

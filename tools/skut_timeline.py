@@ -15,7 +15,7 @@ logits = torch.empty((1000, 4), device="cuda")
 for _ in range(3):
     eng.run_staged("bf16", logits)
 torch.cuda.synchronize()
-buf = torch.zeros(512, dtype=torch.int64, device="cuda")
+buf = torch.zeros(640, dtype=torch.int64, device="cuda")
 N.lib().tav2_debug_timeline(buf.data_ptr(), 0)
 eng.run_staged("bf16", logits)
 torch.cuda.synchronize()
@@ -25,7 +25,6 @@ names = ["LN1->QKV", "QKVepi->S", "softmax->PV", "O/l->Wo", "LN2->W1", "relu->W2
 t0 = t[0]
 prev = t0
 for p in range(13):
-    simt, mma, done = t[2 * p], t[2 * p + 1], t[64 + p]
-    print(f"{names[p]:12s} simt_done {(simt - t0)/1e3:7.2f}  mma_issued {(mma - t0)/1e3:7.2f}  mma_done {(done - t0)/1e3:7.2f}"
-          f"   [simt {(simt - prev)/1e3:5.2f} us, issue {(mma - simt)/1e3:5.2f}, mma {(done - mma)/1e3:5.2f}]")
+    simt, mma, done, allin = t[2 * p], t[2 * p + 1], t[64 + p], t[160 + p]
+    print(f"{names[p]:12s} w0 simt {(simt - prev)/1e3:5.2f} us | all warps in +{(allin - simt)/1e3:5.2f} | issue {(mma - allin)/1e3:5.2f} | mma {(done - mma)/1e3:5.2f}")
     prev = done
