@@ -657,6 +657,512 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
   if (warp == 0) tmem_free<512>(T);
 }
 
+// ===========================================================================
+// Tile-decoupled SKUT (S <= 192): two independent row tiles.
+//
+// Sequence rows are interleaved between the tiles (row r -> tile r & 1, TMEM
+// lane r >> 1) so both carry the same causal work.  Each tile t (warps
+// 4t..4t+3) owns a 256-column TMEM region, its own simt/mma mbarriers and its
+// own issuer lane (thread 128t), so one tile's SIMT epilogue runs while the
+// tensor core executes the other tile's MMAs.  Coupling points: K/V of a
+// layer are complete when all 256 rows arrived on bar_kvready (both tiles'
+// score MMAs need every key), the next layer's K/V may be written once both
+// tiles' P.V MMAs retired (bar_kvfree), and the shared weight buffers are
+// refilled (by tile 1's issuer) once both tiles' MMAs released them.
+//
+// TMEM per tile (base 256t): A/Q/O/LN2-A at +192 (64 cols); D_qkv at +0
+// (192); S/P at +0 (S_pad <= 192); D_wo / pool D at +0; D_w1 at +64;
+// ReLU-A at +96; D_w2 at +128.
+// ===========================================================================
+constexpr uint32_t kTA = 192, kTD = 0, kTW1 = 64, kTA2 = 96, kTW2 = 128;
+
+// 8 valid bits (lanes i0..i0+7 of a tile-quadrant ballot) -> even bit slots
+__device__ __forceinline__ uint32_t spread8(uint32_t x) {
+  x &= 0xffu;
+  x = (x | (x << 4)) & 0x0f0fu;
+  x = (x | (x << 2)) & 0x3333u;
+  x = (x | (x << 1)) & 0x5555u;
+  return x;
+}
+
+struct Tc2Bars {
+  uint64_t simt[2], mma[2], kvready, kvfree, wa_full, wb_full, wa_free, wb_free;
+};
+__shared__ __align__(8) Tc2Bars tc2;  // one set per CTA (static shared, only skut_tc2 uses it)
+
+// MMA issue for tile t (thread 128t).  Only phase bits live in registers: the
+// barrier and operand addresses are static shared / derivable from S_pad.
+struct TileIssuer {
+  uint32_t R;       // TMEM column base of the tile
+  uint32_t S_pad;
+  uint32_t ph = 0;  // bit0 simt, bit1 wa_full, bit2 wb_full, bit3 wa_free, bit4 wb_free
+  int n_commit = 0;
+  bool dbg = false;
+
+  __device__ static uint32_t base() {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    return smem_u32(sm);
+  }
+  __device__ uint32_t wa() const { return base(); }
+  __device__ uint32_t wb() const { return base() + kImgWA; }
+  __device__ uint32_t khi() const { return base() + kImgWA + kImgWB; }
+  __device__ uint32_t klo() const { return khi() + S_pad * 128; }
+  __device__ uint32_t vhi() const { return khi() + 2 * S_pad * 128; }
+  __device__ uint32_t vlo() const { return khi() + 3 * S_pad * 128; }
+  __device__ void wait_ph(uint64_t* bar, int bit) {
+    mbar_wait(bar, (ph >> bit) & 1u);
+    ph ^= 1u << bit;
+  }
+  __device__ void wait_simt() {
+    wait_ph(&tc2.simt[R >> 8], 0);
+    fence_after();
+  }
+  __device__ void commit_mma() {
+    commit(&tc2.mma[R >> 8]);
+    if (dbg && n_commit < 32) g_dbg_skut[2 * n_commit + 1] = sk_time();
+    ++n_commit;
+  }
+  __device__ void need_wa() { wait_ph(&tc2.wa_full, 1); fence_after(); }
+  __device__ void need_wb() { wait_ph(&tc2.wb_full, 2); fence_after(); }
+  // loader role (tile 1): refill once both tiles released the buffer
+  __device__ void refill_wa(const void* src, uint32_t bytes) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    wait_ph(&tc2.wa_free, 3);
+    mbar_expect_tx(&tc2.wa_full, bytes);
+    bulk_g2s(sm, src, bytes, &tc2.wa_full);
+  }
+  __device__ void refill_wb(const void* src) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    wait_ph(&tc2.wb_free, 4);
+    mbar_expect_tx(&tc2.wb_full, kImgWB);
+    bulk_g2s(sm + kImgWA, src, kImgWB, &tc2.wb_full);
+  }
+  __device__ void qkv() { mma3_kmajor(R + kTD, R + kTA, 32, wa(), wa() + kImgWA / 2, 192 * 16, 4, idesc_bf16(128, 192)); }
+  __device__ void scores() { mma3_kmajor(R + kTD, R + kTA, 32, khi(), klo(), S_pad * 16, 4, idesc_bf16(128, S_pad)); }
+  __device__ void pv() {
+    const uint32_t id = idesc_bf16(128, 64, 0, 1);
+    for (int j = 0; j < (int)S_pad / 16; ++j) {
+      const uint64_t bh = sdesc(vhi() + 2 * j * 1024, 1024, 128);
+      const uint64_t bl = sdesc(vlo() + 2 * j * 1024, 1024, 128);
+      mma_bf16_ts(R + kTA, R + kTD + 16 * j, bh, id, j > 0);
+      mma_bf16_ts(R + kTA, R + kTD + 16 * j, bl, id, 1);
+      mma_bf16_ts(R + kTA, R + kTD + 16 * j + 8, bh, id, 1);
+    }
+  }
+  __device__ void wo() { mma3_kmajor(R + kTD, R + kTA, 32, wb(), wb() + 8192, 64 * 16, 4, idesc_bf16(128, 64)); }
+  __device__ void w1() { mma3_kmajor(R + kTW1, R + kTA, 32, wb() + 16384, wb() + 16384 + 4096, 32 * 16, 4, idesc_bf16(128, 32)); }
+  __device__ void w2() { mma3_kmajor(R + kTW2, R + kTA2, 16, wb() + 24576, wb() + 24576 + 4096, 64 * 16, 2, idesc_bf16(128, 64)); }
+  __device__ void pool() { mma3_kmajor(R + kTD, R + kTA, 32, wa(), wa() + 8192, 64 * 16, 4, idesc_bf16(128, 64)); }
+};
+
+__global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
+    Params p, SkutImages img, NNCfg nn, Staged st, int use_staged, const int32_t* idx,
+    const float* Fin, const uint8_t* fmask, int n, float* U, float* logits, float* pooled_out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t taddr_s;
+  __shared__ uint32_t ballot_s[2][4];  // row validity: ballot of tile t, quadrant q
+  __shared__ __align__(16) float lnp_s[kMaxLayers][4][kDModel];
+  __shared__ float red_s[kSkRowWarps][kDModel];
+  __shared__ float z_s[kDModel + kEmbed + kCtx];
+  __shared__ float hid_s[kHidden];
+  __shared__ int any_s;
+  __shared__ unsigned kmax_s[kMaxLayers];
+
+  const int S = nn.seq_len;
+  const int S_pad = (S + 15) & ~15;
+  const int NL = p.num_layers;
+  uint8_t* WA = sm;
+  uint8_t* WB = sm + kImgWA;
+  uint8_t* Khi = WB + kImgWB;
+  uint8_t* Klo = Khi + S_pad * 128;
+  uint8_t* Vhi = Klo + S_pad * 128;
+  uint8_t* Vlo = Vhi + S_pad * 128;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int t = warp >> 2, q = warp & 3;
+  const int li = 32 * q + lane;  // TMEM lane within the tile
+  const int r = 2 * li + t;      // sequence row
+  if (tid == 0) {
+    mbar_init(&tc2.simt[0], 128);
+    mbar_init(&tc2.simt[1], 128);
+    mbar_init(&tc2.mma[0], 1);
+    mbar_init(&tc2.mma[1], 1);
+    mbar_init(&tc2.kvready, kRowThreads);
+    mbar_init(&tc2.kvfree, 2);
+    mbar_init(&tc2.wa_full, 1);
+    mbar_init(&tc2.wb_full, 1);
+    mbar_init(&tc2.wa_free, 2);
+    mbar_init(&tc2.wb_free, 2);
+    mbar_fence_init();
+  }
+  if (warp == 0) tmem_alloc<512>(&taddr_s);
+  for (int i = tid; i < NL * 4 * kDModel; i += kSkThreads) {
+    const int L = i / (4 * kDModel), w = (i / kDModel) % 4, j = i % kDModel;
+    const float* src = w == 0 ? p.ln1_scale[L] : w == 1 ? p.ln1_shift[L] : w == 2 ? p.ln2_scale[L] : p.ln2_shift[L];
+    lnp_s[L][w][j] = src[j];
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (taddr_s != 0u) __trap();  // a 512-column allocation always starts at column 0
+
+  const bool issuer = li == 0;  // thread 128t issues tile t's MMAs
+  TileIssuer is;
+  is.R = 256u * t;
+  is.S_pad = S_pad;
+  is.dbg = issuer && blockIdx.x == 0 && t == 0 && g_dbg_skut != nullptr;
+  if (issuer && t == 1) {  // loader: initial fills
+    mbar_expect_tx(&tc2.wa_full, kImgWA);
+    bulk_g2s(WA, img.wa[0], kImgWA, &tc2.wa_full);
+    mbar_expect_tx(&tc2.wb_full, kImgWB);
+    bulk_g2s(WB, img.wb[0], kImgWB, &tc2.wb_full);
+  }
+
+  const uint32_t lanebase = ((uint32_t)(32 * q) << 16) + 256u * t;
+  const uint32_t cA = lanebase + kTA;
+  const bool in_seq = r < S;
+  uint32_t n_mma = 0, n_kv = 0, n_done = 0;
+  long long* dbg = (blockIdx.x == 0 && tid == 0) ? g_dbg_skut : nullptr;
+  auto wait_mma = [&]() {
+    __syncwarp();
+    mbar_wait_sleep(&tc2.mma[t], n_mma & 1);
+    if (dbg && n_mma < 64) dbg[64 + n_mma] = sk_time();
+    ++n_mma;
+    fence_after();
+  };
+  auto done = [&]() {
+    fence_before();
+    mbar_arrive(&tc2.simt[t]);
+    if (dbg && n_done < 32) dbg[2 * n_done] = sk_time();
+    ++n_done;
+  };
+  // warp-uniform causal bound: the largest row of this warp
+  const int wmax_row = 2 * (32 * q + 31) + t;
+
+  for (int item = blockIdx.x; item < n; item += gridDim.x) {
+    // ---- K3: gather + encode this row (or load caller features) ----
+    float x[kDModel];
+    bool ok = false;
+    if (in_seq) {
+      if (use_staged) {
+        const int tok = slot_token(st, nn, idx, item, r);
+        ok = tok >= 0;
+        if (ok) encode_row(st, p, item, tok, r, x);
+      } else {
+        ok = fmask[(size_t)item * S + r] != 0;
+        if (ok) {
+          const float4* src = reinterpret_cast<const float4*>(Fin + ((size_t)item * S + r) * kDModel);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float4 v = src[j];
+            x[4 * j] = v.x; x[4 * j + 1] = v.y; x[4 * j + 2] = v.z; x[4 * j + 3] = v.w;
+          }
+        }
+      }
+    }
+    if (!ok) {
+#pragma unroll
+      for (int j = 0; j < kDModel; ++j) x[j] = 0.0f;
+    }
+    {
+      const unsigned b = __ballot_sync(0xffffffffu, ok);
+      if (lane == 0) ballot_s[t][q] = b;
+      if (tid < kMaxLayers) kmax_s[tid] = 0u;
+    }
+    named_bar_sync(1, kRowThreads);
+
+    for (int L = 0; L < NL; ++L) {
+      float qn2 = 0.0f;
+      // ---- LN1 -> A ----
+      {
+        float y[kDModel];
+        layer_norm_reg(x, lnp_s[L][0], lnp_s[L][1], y);
+        if (!ok) {
+#pragma unroll
+          for (int j = 0; j < kDModel; ++j) y[j] = 0.0f;
+        }
+        st_split<64>(cA, y);  // warp-collective: never under a divergent branch
+        tmem_st_wait();
+        done();
+      }
+      if (issuer) {
+        is.wait_simt();
+        is.need_wa();
+        is.qkv();
+        is.commit_mma();
+        commit(&tc2.wa_free);
+        if (t == 1) {  // WA free once both tiles' QKV retired: next Wqkv (or out_linear)
+          if (L + 1 < NL) is.refill_wa(img.wa[L + 1], kImgWA);
+          else is.refill_wa(img.wout, kImgWO);
+        }
+      }
+      // ---- QKV epilogue: Q -> TMEM A, K/V -> smem (once both tiles' previous P.V retired) ----
+      wait_mma();
+      {
+        if (n_kv > 0) mbar_wait_sleep(&tc2.kvfree, (n_kv - 1) & 1);
+        const uint32_t cq = lanebase + kTD;
+        float v[32];
+        float kn2 = 0.0f;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          ld32f(cq + 32 * h, v);
+          if (!ok) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) qn2 = fmaf(v[i], v[i], qn2);
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint32_t hi[8], lo[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) split_pair(v[16 * c + 2 * i], v[16 * c + 2 * i + 1], hi[i], lo[i]);
+            tmem_st8(cA + 16 * h + 8 * c, hi);
+            tmem_st8(cA + 32 + 16 * h + 8 * c, lo);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // K: K-major slabs, chunk c of row r at c*(S_pad*16) + r*16
+          ld32f(cq + 64 + 32 * h, v);
+          if (r < S_pad) {
+            if (!ok) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) kn2 = fmaf(v[i], v[i], kn2);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int off = (4 * h + c) * (S_pad * 16) + r * 16;
+              split8_store(Khi + off, Klo + off, v + 8 * c);
+            }
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // V: MN-major (key r, d) at (r/8)*1024 + (d/8)*128 + (r%8)*16 + (d%8)*2
+          ld32f(cq + 128 + 32 * h, v);
+          if (r < S_pad) {
+            if (!ok) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int off = (r >> 3) * 1024 + (4 * h + c) * 128 + (r & 7) * 16;
+              split8_store(Vhi + off, Vlo + off, v + 8 * c);
+            }
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) kn2 = fmaxf(kn2, __shfl_xor_sync(0xffffffffu, kn2, o));
+        if (lane == 0) atomicMax(&kmax_s[L], __float_as_uint(kn2));
+        tmem_st_wait();
+        fence_proxy_async();
+        fence_before();
+        mbar_arrive(&tc2.kvready);  // this row's K/V (and Q) are in place
+      }
+      if (issuer) {
+        mbar_wait(&tc2.kvready, n_kv & 1);  // every key of the layer present
+        fence_after();
+        is.scores();
+        is.commit_mma();
+      }
+      // ---- causal key-masked softmax -> P (bf16 hi/lo, in place over S) ----
+      // single pass with the Cauchy-Schwarz shift m' = ||q_r|| max_j ||k_j|| / 8
+      wait_mma();
+      float inv_l = 0.0f;
+      {
+        mbar_wait_sleep(&tc2.kvready, n_kv & 1);  // kmax_s[L] complete (already passed)
+        const float mb = sqrtf(qn2 * __uint_as_float(kmax_s[L])) * (0.125f * kLog2e);
+        const uint32_t cs = lanebase + kTD;
+        const int nch = S_pad / 16;
+        const int jlast = min(nch - 1, wmax_row / 16);
+        float l = 0.0f;
+        for (int j0 = 0; j0 < nch; j0 += 2) {
+          uint32_t s32[32];
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            if (j0 + u <= jlast) tmem_ld16(cs + 16 * (j0 + u), s32 + 16 * u);  // warp-uniform
+          tmem_ld_wait();
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int j = j0 + u;
+            if (j >= nch) break;
+            uint32_t hi[8], lo[8];
+            uint32_t vm = 0u;
+            if (ok && j <= jlast) {
+              // keys 16j..16j+15: even ones from tile 0, odd from tile 1, lanes 8(j&3)..+7 of quadrant j/4
+              const int sh = 8 * (j & 3);
+              vm = spread8(ballot_s[0][j >> 2] >> sh) | (spread8(ballot_s[1][j >> 2] >> sh) << 1);
+              vm = allowed16(vm, 16 * j, r);
+            }
+            float pv[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              float pe;
+              asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(pe) : "f"(fmaf(__uint_as_float(s32[16 * u + e]), 0.125f * kLog2e, -mb)));
+              pv[e] = ((vm >> e) & 1u) ? pe : 0.0f;
+              l += pv[e];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) split_pair(pv[2 * i], pv[2 * i + 1], hi[i], lo[i]);
+            tmem_st8(cs + 16 * j, hi);
+            tmem_st8(cs + 16 * j + 8, lo);
+          }
+        }
+        inv_l = l > 0.0f ? 1.0f / l : 0.0f;  // a valid row always sees itself
+        tmem_st_wait();
+        done();
+      }
+      if (issuer) {
+        is.wait_simt();
+        is.pv();
+        is.commit_mma();
+        commit(&tc2.kvfree);  // this tile no longer reads K/V of this layer
+      }
+      ++n_kv;
+      // ---- O / l -> A ----
+      wait_mma();
+      {
+        float o[kDModel];
+        ld64(cA, o);
+#pragma unroll
+        for (int j = 0; j < kDModel; ++j) o[j] = ok ? o[j] * inv_l : 0.0f;
+        st_split<64>(cA, o);
+        tmem_st_wait();
+        done();
+      }
+      if (issuer) {
+        is.wait_simt();
+        is.need_wb();
+        is.wo();
+        is.commit_mma();
+      }
+      // ---- x += O Wo ; LN2 -> A ----
+      wait_mma();
+      {
+        float d[kDModel];
+        ld64(lanebase + kTD, d);
+        if (ok) {
+#pragma unroll
+          for (int j = 0; j < kDModel; ++j) x[j] += d[j];
+        }
+        layer_norm_reg(x, lnp_s[L][2], lnp_s[L][3], d);
+        if (!ok) {
+#pragma unroll
+          for (int j = 0; j < kDModel; ++j) d[j] = 0.0f;
+        }
+        st_split<64>(cA, d);
+        tmem_st_wait();
+        done();
+      }
+      if (issuer) {
+        is.wait_simt();
+        is.w1();
+        is.commit_mma();
+      }
+      // ---- ReLU(h) -> A2 ----
+      wait_mma();
+      {
+        float h[kFfn];
+        ld32f(lanebase + kTW1, h);
+#pragma unroll
+        for (int j = 0; j < kFfn; ++j) h[j] = ok ? fmaxf(h[j], 0.0f) : 0.0f;
+        st_split<32>(lanebase + kTA2, h);
+        tmem_st_wait();
+        done();
+      }
+      if (issuer) {
+        is.wait_simt();
+        is.w2();
+        is.commit_mma();
+        commit(&tc2.wb_free);
+        if (t == 1) is.refill_wb(img.wb[(L + 1) % NL]);  // next layer's (or candidate's) Wo|W1|W2
+      }
+      // ---- x += ReLU(h) W2 ----
+      wait_mma();
+      {
+        float d[kDModel];
+        ld64(lanebase + kTW2, d);
+        if (ok) {
+#pragma unroll
+          for (int j = 0; j < kDModel; ++j) x[j] += d[j];
+        }
+      }
+    }
+
+    if (U && in_seq) {  // forward_fused output rows (padded rows are zero)
+      float4* dst = reinterpret_cast<float4*>(U + ((size_t)item * S + r) * kDModel);
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        dst[j] = ok ? make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3])
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    // ---- K5: y = x out_linear, masked max over rows, CTR head ----
+    st_split<64>(cA, x);  // invalid rows carry x = 0
+    tmem_st_wait();
+    done();
+    if (issuer) {
+      is.wait_simt();
+      is.need_wa();
+      is.pool();
+      is.commit_mma();
+      commit(&tc2.wa_free);
+      if (t == 1) is.refill_wa(img.wa[0], kImgWA);  // next candidate's layer-0 Wqkv
+    }
+    wait_mma();
+    {
+      float y[kDModel];
+      ld64(lanebase + kTD, y);
+      if (tid == 0) any_s = 0;
+      named_bar_sync(1, kRowThreads);
+      if (ok) any_s = 1;
+#pragma unroll
+      for (int j = 0; j < kDModel; ++j) {
+        float v = ok ? y[j] : -INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (lane == 0) red_s[warp][j] = v;
+      }
+    }
+    named_bar_sync(1, kRowThreads);
+    if (logits) {
+      if (tid < kDModel) {
+        float v = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kSkRowWarps; ++w) v = fmaxf(v, red_s[w][tid]);
+        v = any_s ? v : 0.0f;  // empty user -> pooled = 0 (trainer.py:358-359)
+        z_s[tid] = v;
+        if (pooled_out) pooled_out[(size_t)item * kDModel + tid] = v;
+      } else if (tid < kDModel + kEmbed) {
+        z_s[tid] = use_staged ? st.cand_unit[(size_t)item * kEmbed + tid - kDModel] : 0.0f;
+      } else if (tid < kDModel + kEmbed + kCtx) {
+        z_s[tid] = use_staged ? st.ctx[st.item_req[item] * kCtx + tid - kDModel - kEmbed] : 0.0f;
+      }
+      named_bar_sync(1, kRowThreads);
+      if (tid < kHidden) {
+        float h = 0.0f;
+        for (int i = 0; i < kDModel + kEmbed + kCtx; ++i) h = fmaf(z_s[i], __ldg(p.head_w1 + i * kHidden + tid), h);
+        hid_s[tid] = fmaxf(h + __ldg(p.head_b1 + tid), 0.0f);
+      }
+      named_bar_sync(1, kRowThreads);
+      if (tid < kHeads) {
+        float o = 0.0f;
+        for (int j = 0; j < kHidden; ++j) o = fmaf(hid_s[j], __ldg(p.head_w2 + j * kHeads + tid), o);
+        logits[(size_t)item * kHeads + tid] = o + __ldg(p.head_b2 + tid);
+      }
+    }
+    named_bar_sync(1, kRowThreads);  // smem (ballot_s, red_s, z_s, kmax_s) reuse by the next item
+  }
+  if (issuer && t == 1) {  // drain the loader's last prefetches before the CTA retires
+    mbar_wait(&tc2.wa_full, (is.ph >> 1) & 1u);
+    mbar_wait(&tc2.wb_full, (is.ph >> 2) & 1u);
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_free<512>(0u);
+}
+
 cudaError_t set_debug_skut(long long* dev) { return cudaMemcpyToSymbol(g_dbg_skut, &dev, sizeof(dev)); }
 
 cudaError_t launch_skut_tc(const Params& p, const SkutImages& img, const NNCfg& nn,
@@ -666,18 +1172,20 @@ cudaError_t launch_skut_tc(const Params& p, const SkutImages& img, const NNCfg& 
   if (n == 0) return cudaSuccess;
   const int S_pad = (nn.seq_len + 15) & ~15;
   const size_t smem = (size_t)kImgWA + kImgWB + 4 * (size_t)S_pad * 128;
-  cudaError_t e = cudaFuncSetAttribute(skut_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // S <= 192: tile-decoupled kernel; 192 < S <= 256: the coupled 2-tile kernel
+  auto kern = S_pad <= 192 ? skut_tc2_kernel : skut_tc_kernel;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   Staged dummy{};
-  skut_tc_kernel<<<n < sms ? n : sms, kSkThreads, smem, s>>>(p, img, nn, st ? *st : dummy, st != nullptr, idx,
-                                                            F, fmask, n, U, logits, pooled);
+  kern<<<n < sms ? n : sms, kSkThreads, smem, s>>>(p, img, nn, st ? *st : dummy, st != nullptr, idx, F, fmask, n,
+                                                  U, logits, pooled);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, skut_tc_kernel);
+    cudaFuncGetAttributes(&fa, kern);
     fprintf(stderr, "skut_tc launch failed: regs=%d maxThreads=%d static_smem=%zu dyn_smem=%zu local=%zu\n",
             fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, smem, fa.localSizeBytes);
   }
