@@ -613,9 +613,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
       if (ok) any_s = 1;
 #pragma unroll
       for (int j = 0; j < kDModel; ++j) {
-        float v = ok ? y[j] : -INFINITY;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        const float v = warp_max_f32(ok ? y[j] : -INFINITY);
         if (lane == 0) red_s[warp][j] = v;
       }
     }
@@ -660,8 +658,8 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
 // ===========================================================================
 // Tile-decoupled SKUT (S <= 192): two independent row tiles.
 //
-// Sequence rows are interleaved between the tiles (row r -> tile r & 1, TMEM
-// lane r >> 1) so both carry the same causal work.  Each tile t (warps
+// Rows are laid out in 8 blocks of S_pad/8 (see the kernel prologue) so
+// every SM sub-partition carries equal causal work.  Each tile t (warps
 // 4t..4t+3) owns a 256-column TMEM region, its own simt/mma mbarriers and its
 // own issuer lane (thread 128t), so one tile's SIMT epilogue runs while the
 // tensor core executes the other tile's MMAs.  Coupling points: K/V of a
@@ -676,15 +674,6 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
 // ===========================================================================
 constexpr uint32_t kTA = 192, kTD = 0, kTW1 = 64, kTA2 = 96, kTW2 = 128;
 
-// 8 valid bits (lanes i0..i0+7 of a tile-quadrant ballot) -> even bit slots
-__device__ __forceinline__ uint32_t spread8(uint32_t x) {
-  x &= 0xffu;
-  x = (x | (x << 4)) & 0x0f0fu;
-  x = (x | (x << 2)) & 0x3333u;
-  x = (x | (x << 1)) & 0x5555u;
-  return x;
-}
-
 struct Tc2Bars {
   uint64_t simt[2], mma[2], kvready, kvfree, wa_full, wb_full, wa_free, wb_free;
 };
@@ -695,6 +684,7 @@ __shared__ __align__(8) Tc2Bars tc2;  // one set per CTA (static shared, only sk
 struct TileIssuer {
   uint32_t R;       // TMEM column base of the tile
   uint32_t S_pad;
+  uint32_t NK;      // keys this tile's rows can see (multiple of 16)
   uint32_t ph = 0;  // bit0 simt, bit1 wa_full, bit2 wb_full, bit3 wa_free, bit4 wb_free
   int n_commit = 0;
   bool dbg = false;
@@ -738,10 +728,10 @@ struct TileIssuer {
     bulk_g2s(sm + kImgWA, src, kImgWB, &tc2.wb_full);
   }
   __device__ void qkv() { mma3_kmajor(R + kTD, R + kTA, 32, wa(), wa() + kImgWA / 2, 192 * 16, 4, idesc_bf16(128, 192)); }
-  __device__ void scores() { mma3_kmajor(R + kTD, R + kTA, 32, khi(), klo(), S_pad * 16, 4, idesc_bf16(128, S_pad)); }
+  __device__ void scores() { mma3_kmajor(R + kTD, R + kTA, 32, khi(), klo(), S_pad * 16, 4, idesc_bf16(128, NK)); }
   __device__ void pv() {
     const uint32_t id = idesc_bf16(128, 64, 0, 1);
-    for (int j = 0; j < (int)S_pad / 16; ++j) {
+    for (int j = 0; j < (int)NK / 16; ++j) {
       const uint64_t bh = sdesc(vhi() + 2 * j * 1024, 1024, 128);
       const uint64_t bl = sdesc(vlo() + 2 * j * 1024, 1024, 128);
       mma_bf16_ts(R + kTA, R + kTD + 16 * j, bh, id, j > 0);
@@ -760,7 +750,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
     const float* Fin, const uint8_t* fmask, int n, float* U, float* logits, float* pooled_out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t taddr_s;
-  __shared__ uint32_t ballot_s[2][4];  // row validity: ballot of tile t, quadrant q
+  __shared__ uint32_t valid_w[8];  // key-validity bitmask, bit r of word r/32
   __shared__ __align__(16) float lnp_s[kMaxLayers][4][kDModel];
   __shared__ float red_s[kSkRowWarps][kDModel];
   __shared__ float z_s[kDModel + kEmbed + kCtx];
@@ -781,7 +771,16 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = warp >> 2, q = warp & 3;
   const int li = 32 * q + lane;  // TMEM lane within the tile
-  const int r = 2 * li + t;      // sequence row
+  // Row blocks: S_pad rows in 8 blocks of rpw = S_pad/8 (<= 24); warp (t, q)
+  // takes block kb = q (tile 0) or 7 - q (tile 1), lanes >= rpw are padding.
+  // Each SM sub-partition q thus holds one early and one late block, so the
+  // causal softmax work is balanced across sub-partitions, no warp is pure
+  // padding, and tile 0 (rows < S_pad/2) only needs keys < NK0.
+  const int rpw = S_pad >> 3;
+  const int kb = t == 0 ? q : 7 - q;
+  const bool mapped = lane < rpw;   // lane carries a row < S_pad
+  const int r = rpw * kb + lane;    // sequence row (when mapped)
+  const int NK0 = ((S_pad >> 1) + 15) & ~15;
   if (tid == 0) {
     mbar_init(&tc2.simt[0], 128);
     mbar_init(&tc2.simt[1], 128);
@@ -796,6 +795,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
     mbar_fence_init();
   }
   if (warp == 0) tmem_alloc<512>(&taddr_s);
+  if (tid < 8) valid_w[tid] = 0u;
   for (int i = tid; i < NL * 4 * kDModel; i += kSkThreads) {
     const int L = i / (4 * kDModel), w = (i / kDModel) % 4, j = i % kDModel;
     const float* src = w == 0 ? p.ln1_scale[L] : w == 1 ? p.ln1_shift[L] : w == 2 ? p.ln2_scale[L] : p.ln2_shift[L];
@@ -810,6 +810,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
   TileIssuer is;
   is.R = 256u * t;
   is.S_pad = S_pad;
+  is.NK = t == 0 ? NK0 : S_pad;
   is.dbg = issuer && blockIdx.x == 0 && t == 0 && g_dbg_skut != nullptr;
   if (issuer && t == 1) {  // loader: initial fills
     mbar_expect_tx(&tc2.wa_full, kImgWA);
@@ -820,7 +821,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
 
   const uint32_t lanebase = ((uint32_t)(32 * q) << 16) + 256u * t;
   const uint32_t cA = lanebase + kTA;
-  const bool in_seq = r < S;
+  const bool in_seq = mapped && r < S;
   uint32_t n_mma = 0, n_kv = 0, n_done = 0;
   long long* dbg = (blockIdx.x == 0 && tid == 0) ? g_dbg_skut : nullptr;
   auto wait_mma = [&]() {
@@ -837,7 +838,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
     ++n_done;
   };
   // warp-uniform causal bound: the largest row of this warp
-  const int wmax_row = 2 * (32 * q + 31) + t;
+  const int wmax_row = rpw * kb + rpw - 1;
 
   for (int item = blockIdx.x; item < n; item += gridDim.x) {
     // ---- K3: gather + encode this row (or load caller features) ----
@@ -865,8 +866,13 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
       for (int j = 0; j < kDModel; ++j) x[j] = 0.0f;
     }
     {
-      const unsigned b = __ballot_sync(0xffffffffu, ok);
-      if (lane == 0) ballot_s[t][q] = b;
+      const unsigned b = __ballot_sync(0xffffffffu, ok);  // lanes >= rpw are never ok
+      if (lane == 0 && b) {
+        const int r0 = rpw * kb;
+        const unsigned long long w = (unsigned long long)b << (r0 & 31);
+        atomicOr(&valid_w[r0 >> 5], (uint32_t)w);
+        if ((uint32_t)(w >> 32)) atomicOr(&valid_w[(r0 >> 5) + 1], (uint32_t)(w >> 32));
+      }
       if (tid < kMaxLayers) kmax_s[tid] = 0u;
     }
     named_bar_sync(1, kRowThreads);
@@ -924,7 +930,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
 #pragma unroll
         for (int h = 0; h < 2; ++h) {  // K: K-major slabs, chunk c of row r at c*(S_pad*16) + r*16
           ld32f(cq + 64 + 32 * h, v);
-          if (r < S_pad) {
+          if (mapped) {
             if (!ok) {
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] = 0.0f;
@@ -941,7 +947,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
 #pragma unroll
         for (int h = 0; h < 2; ++h) {  // V: MN-major (key r, d) at (r/8)*1024 + (d/8)*128 + (r%8)*16 + (d%8)*2
           ld32f(cq + 128 + 32 * h, v);
-          if (r < S_pad) {
+          if (mapped) {
             if (!ok) {
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] = 0.0f;
@@ -975,7 +981,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
         mbar_wait_sleep(&tc2.kvready, n_kv & 1);  // kmax_s[L] complete (already passed)
         const float mb = sqrtf(qn2 * __uint_as_float(kmax_s[L])) * (0.125f * kLog2e);
         const uint32_t cs = lanebase + kTD;
-        const int nch = S_pad / 16;
+        const int nch = (t == 0 ? NK0 : S_pad) / 16;
         const int jlast = min(nch - 1, wmax_row / 16);
         float l = 0.0f;
         for (int j0 = 0; j0 < nch; j0 += 2) {
@@ -990,12 +996,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
             if (j >= nch) break;
             uint32_t hi[8], lo[8];
             uint32_t vm = 0u;
-            if (ok && j <= jlast) {
-              // keys 16j..16j+15: even ones from tile 0, odd from tile 1, lanes 8(j&3)..+7 of quadrant j/4
-              const int sh = 8 * (j & 3);
-              vm = spread8(ballot_s[0][j >> 2] >> sh) | (spread8(ballot_s[1][j >> 2] >> sh) << 1);
-              vm = allowed16(vm, 16 * j, r);
-            }
+            if (ok && j <= jlast) vm = allowed16(valid_w[j >> 1] >> ((j & 1) * 16), 16 * j, r);
             float pv[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
@@ -1115,13 +1116,12 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
       float y[kDModel];
       ld64(lanebase + kTD, y);
       if (tid == 0) any_s = 0;
-      named_bar_sync(1, kRowThreads);
+      named_bar_sync(1, kRowThreads);  // every row is past its last softmax
       if (ok) any_s = 1;
+      if (tid < 8) valid_w[tid] = 0u;
 #pragma unroll
       for (int j = 0; j < kDModel; ++j) {
-        float v = ok ? y[j] : -INFINITY;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        const float v = warp_max_f32(ok ? y[j] : -INFINITY);
         if (lane == 0) red_s[warp][j] = v;
       }
     }
@@ -1152,7 +1152,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
         logits[(size_t)item * kHeads + tid] = o + __ldg(p.head_b2 + tid);
       }
     }
-    named_bar_sync(1, kRowThreads);  // smem (ballot_s, red_s, z_s, kmax_s) reuse by the next item
+    named_bar_sync(1, kRowThreads);  // smem (valid_w, red_s, z_s, kmax_s) reuse by the next item
   }
   if (issuer && t == 1) {  // drain the loader's last prefetches before the CTA retires
     mbar_wait(&tc2.wa_full, (is.ph >> 1) & 1u);
