@@ -88,11 +88,18 @@ def test_golden_forward(case, mode):
     assert err <= (2e-5 if mode == "fp32" else 5e-3), err
 
 
+# S=192: decoupled-tile tensor kernel; 200/256: coupled 2-tile kernel
+# (192 < S <= 256); 96: small decoupled case with an odd row-block size.
+SEEDED = [((32, 96, 32, 32), 3, 150), ((24, 112, 32, 32), 2, 40), ((32, 128, 48, 48), 2, 40),
+          ((16, 48, 16, 16), 2, 60)]
+
+
 @pytest.mark.parametrize("mode", MODES)
-def test_seeded_vs_oracle_medium(mode):
+@pytest.mark.parametrize("cfg,nreq,ncand", SEEDED, ids=lambda v: str(v))
+def test_seeded_vs_oracle_medium(mode, cfg, nreq, ncand):
     """Fresh seeded requests (not in the fixtures), compared with the oracle."""
-    nn = P.NNConfig()
-    reqs = P.generate_requests(3, 150, ll_tokens=4096, seed=11)
+    nn = P.NNConfig(*cfg)
+    reqs = P.generate_requests(nreq, ncand, ll_tokens=4096, seed=11)
     eng = _engine_for(nn, seed=2)
     Pd = orc.model_init(2, seq_len=nn.seq_len)
     logits, idx = eng.rank_requests([(r.user, r.candidates, r.ctx) for r in reqs], mode=mode,
@@ -100,7 +107,7 @@ def test_seeded_vs_oracle_medium(mode):
     row = 0
     for r in reqs:
         ud = from_user(r.user)
-        lg, det = orc.rank_request(ud, r.candidates, r.ctx, Pd, (32, 96, 32, 32), return_detail=True)
+        lg, det = orc.rank_request(ud, r.candidates, r.ctx, Pd, cfg, return_detail=True)
         m = len(r.candidates)
         ref_idx = np.full((m, nn.seq_len), -1, np.int32)
         kth = np.zeros((m, 4))
