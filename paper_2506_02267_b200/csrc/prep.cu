@@ -1,0 +1,92 @@
+// K1: token and candidate prep for the NN scan and the encoder.
+//
+// Reference: nnsearch.py:274-286 (_unit_rows_into), :313-320 (candidate
+// normalisation); core.py:54-79 (dequantize / l2_normalize_rows /
+// unit_embeddings).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tav2_common.cuh"
+#include "tc_common.cuh"
+
+namespace tav2 {
+
+// ---------------------------------------------------------------------------
+// K1: per token  unit(dequantize(q)) in f32 with the reference's rounding
+// steps (core.py:54-57 then :69-74) plus its bf16 hi/lo tile image for the
+// tensor-core scan; per candidate  l2_normalize_rows (nnsearch.py:313-320).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float sumsq8(const float* v) {
+  // 8 interleaved accumulators, adjacent-pair combine (a fixed order; the
+  // reference's einsum order is BLAS-internal, differences are <= 1 ulp).
+  float a[8];
+#pragma unroll
+  for (int l = 0; l < 8; ++l) a[l] = __fmul_rn(v[l], v[l]);
+#pragma unroll
+  for (int j = 8; j < kEmbed; ++j) a[j & 7] = __fadd_rn(a[j & 7], __fmul_rn(v[j], v[j]));
+  float b0 = __fadd_rn(a[0], a[1]), b1 = __fadd_rn(a[2], a[3]);
+  float b2 = __fadd_rn(a[4], a[5]), b3 = __fadd_rn(a[6], a[7]);
+  return __fadd_rn(__fadd_rn(b0, b1), __fadd_rn(b2, b3));
+}
+
+__global__ void __launch_bounds__(256) prep_kernel(Staged st) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < st.n_tok) {
+    const int4* src = reinterpret_cast<const int4*>(st.emb + (size_t)i * kEmbed);
+    int4 raw[2] = {src[0], src[1]};
+    const int8_t* q = reinterpret_cast<const int8_t*>(raw);
+    float d[kEmbed];
+#pragma unroll
+    for (int j = 0; j < kEmbed; ++j) {
+      int qi = q[j];
+      d[j] = __fmul_rn(__fdiv_rn((float)qi, 127.0f), 0.65f);
+    }
+    float nrm = __fsqrt_rn(sumsq8(d));
+    if (nrm == 0.0f) nrm = 1.0f;
+    float u[kEmbed];
+#pragma unroll
+    for (int j = 0; j < kEmbed; ++j) u[j] = __fdiv_rn(d[j], nrm);
+    float4* dst = reinterpret_cast<float4*>(st.tok_unit + (size_t)i * kEmbed);
+#pragma unroll
+    for (int j = 0; j < kEmbed; j += 4) dst[j / 4] = make_float4(u[j], u[j + 1], u[j + 2], u[j + 3]);
+    // bf16 hi/lo image of the unit row, pre-tiled for the tensor-core NN
+    // scores: 64-token tiles of 8 KB = [8 chunks (hi 0-3, lo 4-7)][64 rows][16 B]
+    // (the UMMA K-major no-swizzle B-operand layout), one bulk copy per tile
+    uint8_t* tile = reinterpret_cast<uint8_t*>(st.tok_bf16) + (size_t)(i >> 6) * 8192 + (i & 63) * 16;
+#pragma unroll
+    for (int j = 0; j < kEmbed; j += 8) {
+      uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) tc::split_pair(u[j + 2 * e], u[j + 2 * e + 1], hi[e], lo[e]);
+      *reinterpret_cast<uint4*>(tile + (j / 8) * 1024) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4*>(tile + (4 + j / 8) * 1024) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+    return;
+  }
+  i -= st.n_tok;
+  if (i < st.n_items) {
+    const float4* src = reinterpret_cast<const float4*>(st.cand + (size_t)i * kEmbed);
+    float c[kEmbed];
+#pragma unroll
+    for (int j = 0; j < kEmbed; j += 4) {
+      float4 v = src[j / 4];
+      c[j] = v.x; c[j + 1] = v.y; c[j + 2] = v.z; c[j + 3] = v.w;
+    }
+    float nrm = __fsqrt_rn(sumsq8(c));
+    if (nrm == 0.0f) nrm = 1.0f;
+    float4* dst = reinterpret_cast<float4*>(st.cand_unit + (size_t)i * kEmbed);
+#pragma unroll
+    for (int j = 0; j < kEmbed; j += 4)
+      dst[j / 4] = make_float4(__fdiv_rn(c[j], nrm), __fdiv_rn(c[j + 1], nrm),
+                               __fdiv_rn(c[j + 2], nrm), __fdiv_rn(c[j + 3], nrm));
+  }
+}
+
+cudaError_t launch_prep(const Staged& st, cudaStream_t s) {
+  int n = st.n_tok + st.n_items;
+  if (n == 0) return cudaSuccess;
+  prep_kernel<<<(n + 255) / 256, 256, 0, s>>>(st);
+  return cudaGetLastError();
+}
+
+}  // namespace tav2

@@ -40,7 +40,6 @@ int fail(int code, const char* fmt, ...) {
 
 constexpr int kTile = 128;        // candidates per NN tile (tcgen05 M)
 constexpr int kMinChunk = 256;    // minimum LL tokens per work unit
-constexpr int kMergeCap = 2048;   // nwork * k bound of the merge (nn_merge.cu)
 constexpr int kCaps[3] = {16384, 256, 256};  // LIFELONG/REALTIME/IMPRESSION_CAP (core.py:31-33)
 
 inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
@@ -66,9 +65,7 @@ struct tav2_ctx {
   float* tok_unit = nullptr;
   uint32_t* tok_bf16 = nullptr;
   float* cand_unit = nullptr;
-  uint64_t* part = nullptr;
-  float* part1 = nullptr;      // pass-1 per-chunk top-8 lists (two column halves)
-  float* bound = nullptr;      // [max_items][3] pass-2 gate bound per (candidate, source)
+  NNScan scan{};               // threshold-scan NN buffers (nn_scan.cu)
 
   int32_t* idx = nullptr;
   float* logits = nullptr;
@@ -119,7 +116,6 @@ Staged staged_view(tav2_ctx* c) {
   s.n_tok = p.n_tok;
   s.n_tiles = p.n_tiles;
   s.n_work = p.n_work;
-  s.p1_m = p.p1_m;
   return s;
 }
 
@@ -143,9 +139,10 @@ int free_all(tav2_ctx* c) {
   cudaFree(c->tok_unit);
   cudaFree(c->tok_bf16);
   cudaFree(c->cand_unit);
-  cudaFree(c->part);
-  cudaFree(c->part1);
-  cudaFree(c->bound);
+  cudaFree(c->scan.gmax);
+  cudaFree(c->scan.bound);
+  cudaFree(c->scan.count);
+  cudaFree(c->scan.surv);
   cudaFree(c->idx);
   cudaFree(c->logits);
   cudaFree(c->skut_scratch);
@@ -265,11 +262,17 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
   if ((e = cudaMalloc(&c->tok_bf16, (size_t)(cdiv((int)std::max<int64_t>(T, 1), 64) + 1) * 8192)) != cudaSuccess)
     return bad(e, "tok_bf16");
   if ((e = cudaMalloc(&c->cand_unit, (size_t)N * kEmbed * 4)) != cudaSuccess) return bad(e, "cand_unit");
-  if ((e = cudaMalloc(&c->part, (size_t)c->max_work * c->kmax * kTile * 8)) != cudaSuccess)
-    return bad(e, "partial top-k");
-  if ((e = cudaMalloc(&c->part1, (size_t)c->max_work * kTile * 16 * 4)) != cudaSuccess)
-    return bad(e, "pass-1 lists");
-  if ((e = cudaMalloc(&c->bound, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "pass-2 bounds");
+  // scan buffers: a source has at most max(8k + 2, 16384/32 + 2) groups
+  // (planner), a (candidate, source) at most its source length of survivors
+  c->scan.gcap = (std::max(8 * c->kmax + 2, kCaps[0] / 32 + 2) + 7) & ~7;
+  c->scan.surv_stride =
+      (int)((std::min<int64_t>(std::max<int64_t>(T, 8), kCaps[0] + kCaps[1] + kCaps[2]) + 7) & ~int64_t(7));
+  if ((e = cudaMalloc(&c->scan.gmax, (size_t)N * 3 * c->scan.gcap * 4)) != cudaSuccess)
+    return bad(e, "scan group maxima");
+  if ((e = cudaMalloc(&c->scan.bound, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "scan bounds");
+  if ((e = cudaMalloc(&c->scan.count, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "scan counts");
+  if ((e = cudaMalloc(&c->scan.surv, (size_t)N * c->scan.surv_stride * 2)) != cudaSuccess)
+    return bad(e, "scan survivors");
   if ((e = cudaMalloc(&c->idx, (size_t)N * S * 4)) != cudaSuccess) return bad(e, "idx");
   if ((e = cudaMalloc(&c->logits, (size_t)N * kHeads * 4)) != cudaSuccess) return bad(e, "logits");
   {
@@ -445,35 +448,41 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
     return fail(TAV2_ECAP, "%lld tokens exceed capacity %lld", (long long)T, (long long)c->cap.max_tokens);
 
   // ---- NN work decomposition: one CTA per (candidate tile, source, chunk).
-  // The two-pass tensor-core NN (nn_tc.cu) keeps two register top-8 lists per
-  // chunk, so a chunked source needs max(2, ceil(k/16)) <= nch <= 32 (bound
-  // kernel holds <= 512 values), nch*k <= kMergeCap (merge) and >= 64 tokens
-  // per chunk; otherwise one exact chunk.  RT tail and IMP take the smallest
-  // legal count; LL chunks are sized so that all units fill the SMs. ----
-  auto chunk_range = [&](int s, int len, int& lo_n, int& hi_n) {
-    const int k = nn.k[s];
-    lo_n = std::max(2, cdiv(k, 16));
-    hi_n = std::min(std::min(32, kMergeCap / std::max(k, 1)), len / 64);
+  // A source with n <= k tokens needs no scan (all selected).  Otherwise the
+  // threshold scan (nn_scan.cu) groups its tokens in G = 2^glog (about 4k to
+  // 8k groups, G <= 32); chunk boundaries are 64-token aligned in the global
+  // token index so every group lies in one chunk.  RT tail and IMP take one
+  // chunk per tile; LL chunks (>= kMinChunk tokens) fill the SMs. ----
+  auto scanned = [&](const tav2_request& q, int s) {
+    const int lo = s == 1 ? nn.recent : 0;
+    return nn.k[s] > 0 && q.len[s] - lo > nn.k[s];
   };
-  auto rt_imp_chunks = [&](int s, int len) {
-    int a, b;
-    chunk_range(s, len, a, b);
-    return a <= b ? a : 1;
+  auto group_log = [&](int n, int k) {
+    int g = 0;
+    while (g < 5 && (n >> (g + 1)) >= 4 * k) ++g;
+    return g;
   };
   int other = 0;
   for (int r = 0; r < n_req; ++r) {
     const int t = cdiv(reqs[r].n_cand, kTile);
-    if (nn.k[1] > 0 && reqs[r].len[1] > nn.recent) other += t * rt_imp_chunks(1, reqs[r].len[1] - nn.recent);
-    if (nn.k[2] > 0 && reqs[r].len[2] > 0) other += t * rt_imp_chunks(2, reqs[r].len[2]);
+    other += t * ((int)scanned(reqs[r], 1) + (int)scanned(reqs[r], 2));
   }
   const int ll_chunks_target = std::max(1, (c->sms - other) / std::max(tiles, 1));
   std::vector<NNTile> vt;
   std::vector<NNWork> vw;
+  std::vector<int> glogs((size_t)n_req * 3, 0);
   vt.reserve(tiles);
   {
     int item = 0;
+    int64_t tok_req = 0;
     for (int r = 0; r < n_req; ++r) {
       const tav2_request& q = reqs[r];
+      int64_t tok_off[3];
+      for (int s = 0, o = 0; s < 3; ++s) {
+        tok_off[s] = tok_req + o;
+        o += q.len[s];
+        if (scanned(q, s)) glogs[r * 3 + s] = group_log(q.len[s] - (s == 1 ? nn.recent : 0), nn.k[s]);
+      }
       for (int i0 = 0; i0 < q.n_cand; i0 += kTile) {
         NNTile t{};
         t.req = r;
@@ -481,29 +490,24 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
         t.n = std::min(kTile, q.n_cand - i0);
         const int tid = (int)vt.size();
         for (int s = 0; s < 3; ++s) {
-          int lo = s == 1 ? nn.recent : 0;
-          int hi = q.len[s];
+          const int lo = s == 1 ? nn.recent : 0, hi = q.len[s];
           t.work0[s] = (int)vw.size();
           t.nwork[s] = 0;
-          if (nn.k[s] == 0 || hi <= lo) continue;
+          if (!scanned(q, s)) continue;
           int nch = 1;
-          if (s == 0) {
-            int a, b;
-            chunk_range(0, hi - lo, a, b);
-            nch = std::min(std::max(ll_chunks_target, a), b);
-            if (a > b || nch < 2) nch = 1;
-          } else {
-            nch = rt_imp_chunks(s, hi - lo);
-          }
-          int step = cdiv(hi - lo, nch);
-          for (int a = lo; a < hi; a += step) {
-            vw.push_back(NNWork{tid, s, a, std::min(hi, a + step)});
+          if (s == 0) nch = std::max(1, std::min(ll_chunks_target, (hi - lo) / kMinChunk));
+          const int64_t step = std::max<int64_t>(64, ((int64_t)cdiv(hi - lo, nch) + 63) & ~int64_t(63));
+          for (int64_t a = tok_off[s] + lo, end = tok_off[s] + hi; a < end;) {
+            const int64_t b = std::min(end, (a & ~int64_t(63)) + step);
+            vw.push_back(NNWork{tid, s, (int32_t)(a - tok_off[s]), (int32_t)(b - tok_off[s])});
             t.nwork[s]++;
+            a = b;
           }
         }
         vt.push_back(t);
       }
       item += q.n_cand;
+      tok_req += (int64_t)q.len[0] + q.len[1] + q.len[2];
     }
   }
   if ((int)vt.size() > c->max_tiles || (int)vw.size() > c->max_work)
@@ -516,7 +520,6 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
   p.n_tiles = (int)vt.size();
   p.n_work = (int)vw.size();
   p.tile_size = kTile;
-  p.p1_m = 16;
   int64_t o = 0;
   p.off_req = o; o = align256(o + (int64_t)n_req * sizeof(ReqInfo));
   p.off_tiles = o; o = align256(o + (int64_t)p.n_tiles * sizeof(NNTile));
@@ -546,9 +549,11 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
     const tav2_request& q = reqs[r];
     ri[r].item_off = item;
     ri[r].n_items = q.n_cand;
+    ri[r].pad_ = 0;
     for (int s = 0; s < 3; ++s) {
       ri[r].tok_off[s] = (int32_t)tok;
       ri[r].len[s] = q.len[s];
+      ri[r].glog[s] = glogs[r * 3 + s];
       if (q.len[s]) {
         memcpy(emb + tok * kEmbed, q.emb[s], (size_t)q.len[s] * kEmbed);
         memcpy(act + tok, q.action[s], (size_t)q.len[s] * 2);
@@ -588,22 +593,15 @@ int check_ready(tav2_ctx* c, int mode) {
   return TAV2_OK;
 }
 
-int run_nn(tav2_ctx* c, int mode, int32_t* idx, float* scores, cudaStream_t s) {
+// NN selection (both precision modes: the scan's survivors are re-scored with
+// the reference's f64 formula, so the index sets are the reference's).
+int run_nn(tav2_ctx* c, int32_t* idx, float* scores, cudaStream_t s) {
   Staged st = staged_view(c);
   CU(timed(c, "prep", s, [&] { return launch_prep(st, s); }));
-  if (mode == TAV2_MODE_FP32) {
-    CU(timed(c, "nn_simt", s, [&] { return launch_nn_simt(st, c->nn, c->part, c->kmax, kTile, s); }));
-  } else {
-    CU(timed(c, "nn_tc_pass1", s, [&] {
-      return launch_nn_tc(st, c->nn, c->part, c->part1, c->bound, c->kmax, kTile, 1, s);
-    }));
-    CU(timed(c, "nn_bound", s, [&] { return launch_nn_bound(st, c->nn, c->part1, c->bound, kTile, s); }));
-    CU(timed(c, "nn_tc_pass2", s, [&] {
-      return launch_nn_tc(st, c->nn, c->part, c->part1, c->bound, c->kmax, kTile, 2, s);
-    }));
-  }
-  CU(timed(c, "nn_merge", s,
-           [&] { return launch_nn_merge(st, c->nn, c->part, c->kmax, kTile, idx, scores, s); }));
+  CU(timed(c, "nn_scan1", s, [&] { return launch_nn_scan(st, c->nn, c->scan, 1, s); }));
+  CU(timed(c, "nn_bound", s, [&] { return launch_nn_bound(st, c->nn, c->scan, s); }));
+  CU(timed(c, "nn_scan2", s, [&] { return launch_nn_scan(st, c->nn, c->scan, 2, s); }));
+  CU(timed(c, "nn_select", s, [&] { return launch_nn_select(st, c->nn, c->scan, idx, scores, s); }));
   return TAV2_OK;
 }
 
@@ -638,7 +636,7 @@ int tav2_nn_select(tav2_ctx* c, int mode, int32_t* idx_dev, float* scores_dev, v
   if (!idx_dev) return fail(TAV2_EINVAL, "idx_dev is null");
   CU(cudaSetDevice(c->device));
   c->launches = 0;
-  return run_nn(c, mode, idx_dev, scores_dev, (cudaStream_t)stream);
+  return run_nn(c, idx_dev, scores_dev, (cudaStream_t)stream);
 }
 
 int tav2_encode(tav2_ctx* c, const int32_t* idx_dev, float* features_dev, uint8_t* mask_dev,
@@ -692,7 +690,7 @@ int tav2_run_staged(tav2_ctx* c, int mode, float* logits_dev, void* stream) {
   CU(cudaSetDevice(c->device));
   cudaStream_t s = (cudaStream_t)stream;
   c->launches = 0;
-  if ((rc = run_nn(c, mode, c->idx, nullptr, s))) return rc;
+  if ((rc = run_nn(c, c->idx, nullptr, s))) return rc;
   return run_score(c, mode, c->idx, logits_dev ? logits_dev : c->logits, nullptr, s);
 }
 

@@ -31,7 +31,13 @@ struct ReqInfo {          // one unique request (DedupBatch.users entry)
   int32_t len[3];         // source lengths
   int32_t item_off;       // first item (candidate) of this request
   int32_t n_items;
+  int32_t glog[3];        // NN scan group size 2^glog per source (planner)
+  int32_t pad_;
 };
+
+// Approximate-score gate margin of the threshold scan: > the bf16x3 score
+// error bound 2.3e-5 for unit vectors (nn_scan.cu).
+constexpr float kGateEps = 4e-5f;
 
 struct NNWork {           // one (candidate tile, source, token chunk) unit
   int32_t tile;           // candidate tile id
@@ -47,9 +53,18 @@ struct NNTile {           // up to kTile consecutive items of one request
   int32_t nwork[3];       // number of chunks per source
 };
 
+// Device buffers of the threshold-scan NN (nn_scan.cu / nn_select.cu).
+struct NNScan {
+  float* gmax;            // [items][3][gcap] pass-1 group maxima
+  float* bound;           // [items][3] k-th largest group maximum
+  unsigned* count;        // [items][3] pass-2 survivor counts
+  uint16_t* surv;         // [items][surv_stride] survivor source indices (per-source sub-lists)
+  int gcap, surv_stride;
+};
+
 struct Plan {
   int32_t n_req, n_items, n_tok;
-  int32_t n_tiles, n_work, tile_size, p1_m;
+  int32_t n_tiles, n_work, tile_size, pad_;
   // byte offsets inside the staged region
   int64_t off_req, off_tiles, off_work, off_item_req, off_ctx, off_cand, off_action,
       off_surface, off_emb, bytes;
@@ -113,7 +128,6 @@ struct Staged {
   uint32_t* tok_bf16;      // derived: unit rows as bf16 hi/lo, 64-token tiles of 8 KB (prep_kernel)
   float* cand_unit;        // [N, 32] derived: l2_normalize_rows(cand)
   int n_req, n_items, n_tok, n_tiles, n_work;
-  int p1_m;                // pass-1 list size of the two-pass NN (8 or 16)
 };
 
 // ---------------------------------------------------------------------------
@@ -145,103 +159,19 @@ __host__ __device__ inline double key_score(uint64_t key) {
   return s;
 }
 
-// Partial top-k buffer: for tile t, source s, candidate c (0..tile_size) and
-// chunk j (0..t.nwork[s]) the chunk's k keys are contiguous; all chunks of one
-// candidate are adjacent so the merge reads them coalesced.
-__host__ __device__ inline size_t part_offset(const NNTile& t, int s, int c, int j, int kmax,
-                                              int tile_size) {
-  return ((size_t)t.work0[s] * tile_size + (size_t)c * t.nwork[s] + j) * kmax;
-}
-
-// Min-heap of `k` keys stored with stride `ld` (struct-of-arrays across the
-// threads of a block so concurrent per-thread heaps are bank-conflict free).
-__device__ __forceinline__ void heap_replace_root(uint64_t* h, int ld, int k, uint64_t key) {
-  int i = 0;
-  while (true) {
-    int l = 2 * i + 1;
-    if (l >= k) break;
-    int r = l + 1;
-    uint64_t lv = h[l * ld];
-    int c = l;
-    uint64_t cv = lv;
-    if (r < k) {
-      uint64_t rv = h[r * ld];
-      if (rv < lv) { c = r; cv = rv; }
-    }
-    if (cv >= key) break;
-    h[i * ld] = cv;
-    i = c;
-  }
-  h[i * ld] = key;
-}
-
-// Restore the min-heap property below slot i (heapify building block).
-__device__ __forceinline__ void heap_sift_min(uint64_t* h, int ld, int n, int i) {
-  const uint64_t v = h[i * ld];
-  while (true) {
-    int l = 2 * i + 1;
-    if (l >= n) break;
-    int c = l;
-    uint64_t cv = h[l * ld];
-    if (l + 1 < n) {
-      const uint64_t rv = h[(l + 1) * ld];
-      if (rv < cv) { c = l + 1; cv = rv; }
-    }
-    if (cv >= v) break;
-    h[i * ld] = cv;
-    i = c;
-  }
-  h[i * ld] = v;
-}
-
-// Max-heap sift on u32 values (used to order the final picks by index).
-__device__ __forceinline__ void heap_sift_u32(int32_t* a, int ld, int n, int i) {
-  int32_t v = a[i * ld];
-  while (true) {
-    int l = 2 * i + 1;
-    if (l >= n) break;
-    int r = l + 1;
-    int c = l;
-    int32_t cv = a[l * ld];
-    if (r < n) {
-      int32_t rv = a[r * ld];
-      if (rv > cv) { c = r; cv = rv; }
-    }
-    if (cv <= v) break;
-    a[i * ld] = cv;
-    i = c;
-  }
-  a[i * ld] = v;
-}
-
-// ascending in-place heapsort of n values with stride ld
-__device__ __forceinline__ void heapsort_u32(int32_t* a, int ld, int n) {
-  for (int i = n / 2 - 1; i >= 0; --i) heap_sift_u32(a, ld, n, i);
-  for (int e = n - 1; e > 0; --e) {
-    int32_t t = a[0];
-    a[0] = a[e * ld];
-    a[e * ld] = t;
-    heap_sift_u32(a, ld, e, 0);
-  }
-}
-
 }  // namespace tav2
 
 // Host-side launchers (defined in the kernel translation units).
 namespace tav2 {
 cudaError_t launch_prep(const Staged& st, cudaStream_t s);
-cudaError_t launch_nn_simt(const Staged& st, const NNCfg& nn, uint64_t* part, int kmax,
-                           int tile_size, cudaStream_t s);
-cudaError_t launch_nn_tc(const Staged& st, const NNCfg& nn, uint64_t* part, float* part1,
-                         const float* bound, int kmax, int tile_size, int pass, cudaStream_t s);
-cudaError_t launch_nn_bound(const Staged& st, const NNCfg& nn, const float* part1, float* bound,
-                            int tile_size, cudaStream_t s);
+cudaError_t launch_nn_scan(const Staged& st, const NNCfg& nn, const NNScan& sc, int pass,
+                           cudaStream_t s);
+cudaError_t launch_nn_bound(const Staged& st, const NNCfg& nn, const NNScan& sc, cudaStream_t s);
+cudaError_t launch_nn_select(const Staged& st, const NNCfg& nn, const NNScan& sc, int32_t* idx,
+                             float* scores, cudaStream_t s);
 cudaError_t set_debug_timeline(long long* dev, int block);
 cudaError_t set_debug_skut(long long* dev);
 bool make_rows32_map(CUtensorMap* map, const void* base, int64_t rows, int box_rows);
-
-cudaError_t launch_nn_merge(const Staged& st, const NNCfg& nn, const uint64_t* part, int kmax,
-                            int tile_size, int32_t* idx, float* scores, cudaStream_t s);
 cudaError_t launch_encode(const Staged& st, const NNCfg& nn, const Params& p, const int32_t* idx,
                           float* F, uint8_t* mask, cudaStream_t s);
 cudaError_t launch_skut_simt(const Params& p, const NNCfg& nn, const Staged* st,
