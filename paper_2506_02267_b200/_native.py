@@ -15,7 +15,9 @@ import numpy as np
 from .core import ValidationError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libtav2.so")
+# TAV2_DEBUG=1 selects the timeline-instrumented build (tools/*_timeline.py)
+LIB_PATH = os.path.join(HERE, "_lib", "libtav2_debug.so" if os.environ.get("TAV2_DEBUG") == "1"
+                        else "libtav2.so")
 
 TAV2_OK, TAV2_EINVAL, TAV2_ECUDA, TAV2_ECAP, TAV2_ESTATE = 0, 1, 2, 3, 4
 MODE_FP32, MODE_BF16 = 0, 1
@@ -25,7 +27,7 @@ EXPORTS = (
     "tav2_create", "tav2_destroy", "tav2_load_params", "tav2_stage", "tav2_nn_select",
     "tav2_encode", "tav2_forward", "tav2_score", "tav2_rank", "tav2_run_staged",
     "tav2_last_launch_count", "tav2_last_error", "tav2_build_info", "tav2_set_profiling",
-    "tav2_kernel_times", "tav2_tc_selftest", "tav2_debug_timeline",
+    "tav2_kernel_times", "tav2_tc_selftest", "tav2_debug_timeline", "tav2_debug_cta",
 )
 
 
@@ -91,6 +93,7 @@ def lib() -> ctypes.CDLL:
                                             ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32),
                                             ctypes.c_int]
             L.tav2_debug_timeline.argtypes = [vp, ctypes.c_int]
+            L.tav2_debug_cta.argtypes = [vp]
             L.tav2_tc_selftest.argtypes = [ctypes.c_int, vp, vp, vp, ctypes.c_int, ctypes.c_int, vp]
             L.tav2_last_error.restype = ctypes.c_char_p
             L.tav2_build_info.restype = ctypes.c_char_p

@@ -15,6 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libtav2.so")
+LIB_DEBUG = os.path.join(LIBDIR, "libtav2_debug.so")  # + per-CTA / per-phase timeline stamps
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -25,28 +26,32 @@ def sources() -> list[str]:
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
 
 
-def _digest() -> str:
+def _digest(extra: list[str]) -> str:
     h = hashlib.sha256()
     for p in sources() + sorted(
         os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))
     ) + [os.path.join(INCLUDE, "tav2.h")]:
         h.update(open(p, "rb").read())
-    h.update(" ".join(ARCH + FLAGS).encode())
+    h.update(" ".join(ARCH + FLAGS + extra).encode())
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every .cu under csrc/ into one shared library (parallel)."""
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    """Compile every .cu under csrc/ into one shared library (parallel).
+    debug=True builds libtav2_debug.so with the timeline stamps compiled in
+    (tools/*_timeline.py; select it with TAV2_DEBUG=1)."""
     os.makedirs(LIBDIR, exist_ok=True)
-    stamp = LIB + ".sha256"
-    dig = _digest()
-    if not force and os.path.exists(LIB) and os.path.exists(stamp):
+    lib = LIB_DEBUG if debug else LIB
+    extra = (["-DTAV2_DEBUG=1"] + os.environ.get("TAV2_EXTRA_FLAGS", "").split()) if debug else []
+    stamp = lib + ".sha256"
+    dig = _digest(extra)
+    if not force and os.path.exists(lib) and os.path.exists(stamp):
         if open(stamp).read().strip() == dig:
-            return LIB
+            return lib
     objs, procs = [], []
     for src in sources():
-        obj = os.path.join(LIBDIR, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", INCLUDE, "-Xptxas", "-v", "-c", src, "-o", obj]
+        obj = os.path.join(LIBDIR, os.path.basename(src) + (".dbg.o" if debug else ".o"))
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", INCLUDE, "-Xptxas", "-v", "-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
     for src, p in procs:
@@ -55,7 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed on {src}:\n{out}")
         if verbose:
             print(out)
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcuda"]
     out = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
     if out.returncode != 0:
         raise RuntimeError(f"link failed:\n{out.stdout.decode()}")
@@ -63,8 +68,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         os.remove(o)
     with open(stamp, "w") as fh:
         fh.write(dig)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv))

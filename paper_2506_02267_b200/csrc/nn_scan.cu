@@ -6,7 +6,7 @@
 //
 // Tensor-core part: approximate scores for every (candidate, token) as a
 // bf16x3 GEMM of the f32 unit vectors (x = hi + lo, a.b ~= ah.bh + ah.bl +
-// al.bh), M = 128 candidates x N = 64 tokens x K = 32 per tile, f32
+// al.bh), M = 128 candidates x N = 256 tokens x K = 32 per tile, f32
 // accumulation in TMEM.  |approx - exact| <= 3*2^-18*sum|a_j b_j| + f32
 // accumulation <= 2.3e-5 for unit vectors (measured max 5.7e-6,
 // tools/measure_bf16x3_err.py) < kGateEps.
@@ -15,28 +15,35 @@
 //          groups of G = 2^glog consecutive tokens (G-aligned in the global
 //          token index, glog chosen by the planner so that a source has
 //          about 4k..8k groups) and writes each group's approximate maximum.
-//   nn_bound_kernel: T = k-th largest group maximum.  k distinct groups hold
-//          a token with approx >= T, so the exact k-th best score is >= T -
-//          eps and every exact top-k token has approx >= T - 2 eps.
-//   pass 2 (compaction): every token with approx >= T - 2 eps is appended
-//          (source index, u16) to the (candidate, source) survivor list.
+//   nn_bound_kernel: T <= the k-th largest group maximum (bisection).  k
+//          distinct groups hold a token with approx >= T, so the exact k-th
+//          best score is >= T - eps and every exact top-k token has approx
+//          >= T - 2 eps.
+//   pass 2 (gate): every token with approx >= T - 2 eps is appended (source
+//          index, u16) to the (candidate, source) survivor list.
 //   nn_select_kernel (nn_select.cu) re-scores the survivors exactly (f64,
 //          the reference formula) and selects the top k.
 // Both scan passes are branch-light per score (a max or a compare), so the
 // epilogue keeps pace with the tensor core instead of running a divergent
 // per-thread insertion sort.
 //
-// Roles (320 threads): warps 0-7 epilogue (warp w reads TMEM lanes
-// 32*(w%4).. = candidates, column half w/4 of every tile), warp 8 producer
-// (one 8 KB cp.async.bulk per pre-tiled 64-token bf16 hi/lo image written by
-// prep_kernel, 8-stage ring), warp 9 MMA issuer.  TMEM: 4 accumulator
-// buffers x 64 columns.  Chunk boundaries are 64-token aligned (planner), so
+// MMA: N = 256 tokens per instruction.  One warp issues a tcgen05.mma only
+// every ~120 cycles whatever its N (tools/mma_bench.cu: the tensor core
+// itself needs 32 / 64 / 128 cycles at N = 64 / 128 / 256), so N = 256 is the
+// first shape where a single issuer keeps the tensor core busy: 6 MMAs
+// (2 k-steps x 3 terms) per 256-token tile, ~3 tensor cycles per token.
+// Roles (320 threads): warps 0-7 epilogue (warp w reads TMEM lanes 32*(w%4)..
+// = candidates, column half w/4 = 128 tokens of every tile), warp 8 producer
+// (one 32 KB cp.async.bulk per pre-tiled 256-token bf16 hi/lo image written by
+// prep_kernel, 4-stage ring), warp 9 MMA issuer.  TMEM: 2 accumulator
+// buffers x 256 columns.  Chunk boundaries are tile aligned (planner), so
 // every group is scanned by exactly one CTA.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <float.h>
 #include <stdint.h>
 
+#include "dbg.cuh"
 #include "tav2_common.cuh"
 #include "tc_common.cuh"
 
@@ -44,66 +51,123 @@ namespace tav2 {
 
 using namespace tc;
 
-constexpr int kNT = 64;          // tokens per MMA tile (N)
-constexpr int kStages = 8;       // smem ring depth
-constexpr int kAcc = 4;          // TMEM accumulator buffers
+constexpr int kNT = kScanTile;   // tokens per tile and MMA (N = 256)
+constexpr int kStages = 4;       // smem ring depth
+constexpr int kAcc = 2;          // TMEM accumulator buffers (2 x 256 columns)
 constexpr int kTcThreads = 320;
 constexpr int kProdWarp = 8, kMmaWarp = 9;
 constexpr int kEpiThreads = 256;
-
+constexpr int kBTile = kScanTileBytes;      // 8 chunks (hi 0-3, lo 4-7) x 256 rows x 16 B = 32 KB
 constexpr int kASlab = 128 * 16;            // one 16-byte K chunk of 128 candidate rows
 constexpr int kAHalf = 4 * kASlab;          // 32 bf16 of 128 rows (8 KB)
-constexpr int kBTile = 8 * kNT * 16;        // token tile: 8 chunks (hi 0-3, lo 4-7) x 64 rows (8 KB)
+constexpr int kSurvBuf = 16;                // pass-2 survivors buffered per thread before a flush
 
+// Debug timeline (tav2_debug_timeline): %globaltimer stamps of work unit
+// g_dbg_block: slot 160*(pass-1) + {0 inputs ready, 8+i producer copy of tile
+// i, 40+i MMA issue, 72+i epilogue thread 0 sees tile i, 104+i thread 0 done
+// with tile i, 150 CTA end}.
 __device__ long long* g_dbg_timeline = nullptr;
 __device__ int g_dbg_block = 0;
+#define SCAN_STAMP(slot)                                                             \
+  do {                                                                               \
+    if (kDebug && dbgp) {                                                            \
+      long long t_;                                                                  \
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                          \
+      dbgp[(slot) + 160 * (pass - 1)] = t_;                                          \
+    }                                                                                \
+  } while (0)
 
-// max over groups of G = 2^GL consecutive values of v[32] -> out[32 >> GL]
+// Store the group maxima of one 32-column quarter v[32].  dst is the
+// (candidate, source) row indexed by global group - gbase (gbase = 8-aligned
+// first group), so a quarter's 32 >> GL groups are contiguous and 16-byte
+// aligned whenever there are >= 4 of them: a quarter inside the chunk stores
+// vectors.
 template <int GL>
-__device__ __forceinline__ void group_max(const float* v, float* out) {
-  constexpr int G = 1 << GL;
+__device__ __forceinline__ void write_groups(const float* v, float* dst, int g_first, int g_lo,
+                                             int g_hi, bool whole) {
+  constexpr int G = 1 << GL, NG = 32 >> GL;
+  float m[NG];
 #pragma unroll
-  for (int g = 0; g < 32 / G; ++g) {
-    float m = v[g * G];
+  for (int g = 0; g < NG; ++g) {
+    m[g] = v[g * G];
 #pragma unroll
-    for (int e = 1; e < G; ++e) m = fmaxf(m, v[g * G + e]);
-    out[g] = m;
+    for (int e = 1; e < G; ++e) m[g] = fmaxf(m[g], v[g * G + e]);
+  }
+  float* d = dst + g_first;
+  if (whole) {
+    if constexpr (NG >= 4) {
+#pragma unroll
+      for (int g = 0; g < NG; g += 4) *reinterpret_cast<float4*>(d + g) = make_float4(m[g], m[g + 1], m[g + 2], m[g + 3]);
+    } else if constexpr (NG == 2) {
+      *reinterpret_cast<float2*>(d) = make_float2(m[0], m[1]);
+    } else {
+      d[0] = m[0];
+    }
+    return;
+  }
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    const int gg = g_first + g;  // global group index
+    if (gg >= g_lo && gg <= g_hi) d[g] = m[g];
   }
 }
 
-template <int GL>
-__device__ __forceinline__ void write_groups(const float* v, float* dst, int g_first, int g_lo,
-                                             int g_hi) {
-  float m[32 >> GL];
-  group_max<GL>(v, m);
-#pragma unroll
-  for (int g = 0; g < (32 >> GL); ++g) {
-    const int gg = g_first + g;  // global group index
-    if (gg >= g_lo && gg <= g_hi) dst[gg - g_lo] = m[g];
-  }
+// valid-column mask of the 32 columns starting at col0 within [g0, g1)
+__device__ __forceinline__ uint32_t range_mask(int col0, int g0, int g1) {
+  const int a = max(g0 - col0, 0), z = min(g1 - col0, 32);
+  if (a >= z) return 0u;
+  return (z >= 32 ? 0xffffffffu : ((1u << z) - 1u)) & ~((1u << a) - 1u);
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg nn, NNScan sc,
                                                                 int pass) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  uint8_t* As = sm;               // [hi: 4 chunks][lo: 4 chunks] x 128 rows x 16 B
-  uint8_t* Bs = sm + 2 * kAHalf;  // [kStages][bf16 image 8 chunks x 64 rows x 16 B]
+  uint8_t* As = sm;               // candidates: [hi: 4 chunks][lo: 4 chunks] x 128 rows x 16 B
+  uint8_t* Bs = sm + 2 * kAHalf;  // [kStages][32 KB token image]
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull[kAcc], tempty[kAcc];
   __shared__ uint32_t taddr_s;
+  __shared__ uint16_t sbuf[kSurvBuf][kEpiThreads];  // pass 2: per-thread survivor buffer
 
+  cta_stamp(pass == 1 ? kDbgScan1 : kDbgScan2, 0);
+  long long* const dbgp = kDebug && blockIdx.x == g_dbg_block ? g_dbg_timeline : nullptr;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const NNWork w = st.work[blockIdx.x];
   const NNTile tile = st.tiles[w.tile];
-  const ReqInfo rq = st.req[tile.req];
+  const ReqInfo& rq = st.req[tile.req];  // (global: indexed by a runtime source)
   const int src = w.source;
+  const int tok_off = rq.tok_off[src], tok_off0 = rq.tok_off[0], glog = rq.glog[src];
   // global token ranges: the source's scanned range and this chunk
-  const int s_lo = rq.tok_off[src] + (src == 1 ? nn.recent : 0);
-  const int s_hi = rq.tok_off[src] + rq.len[src];
-  const int g0 = rq.tok_off[src] + w.t0, g1 = rq.tok_off[src] + w.t1;
+  const int s_lo = tok_off + (src == 1 ? nn.recent : 0);
+  const int s_hi = tok_off + rq.len[src];
+  const int g0 = tok_off + w.t0, g1 = tok_off + w.t1;
   const int tile0 = g0 / kNT;
   const int ntiles = (g1 + kNT - 1) / kNT - tile0;
 
-  // ---- prologue: candidate hi/lo (A operand), barriers, TMEM ----
+  // ---- prologue: barriers, TMEM (input independent) ----
+  if (warp == kProdWarp) {
+    if (lane == 0) {
+      for (int s = 0; s < kStages; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);  // the MMA commit frees the stage
+      }
+      for (int b = 0; b < kAcc; ++b) {
+        mbar_init(&tfull[b], 1);
+        mbar_init(&tempty[b], kEpiThreads);
+      }
+      mbar_fence_init();
+    }
+  } else if (warp == kMmaWarp) {
+    tmem_alloc<512>(&taddr_s);
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t T = taddr_s;
+  griddep_launch();
+  griddep_wait();  // prep (cand_unit, tok_bf16) / bound (gate) complete
+  cta_stamp(pass == 1 ? kDbgScan1 : kDbgScan2, 2);
+  if (tid == 0) SCAN_STAMP(0);
+  // ---- candidate hi/lo (A operand, smem K-major slabs) ----
   if (warp < 4) {
     const int c = tid;
     const bool real = c < tile.n;
@@ -118,34 +182,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
       *reinterpret_cast<uint4*>(As + ch * kASlab + c * 16) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
       *reinterpret_cast<uint4*>(As + kAHalf + ch * kASlab + c * 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     }
-  } else if (warp == kProdWarp) {
-    if (lane == 0) {
-      for (int s = 0; s < kStages; ++s) {
-        mbar_init(&full[s], 1);
-        mbar_init(&empty[s], 1);  // the MMA commit frees the stage
-      }
-      for (int b = 0; b < kAcc; ++b) {
-        mbar_init(&tfull[b], 1);
-        mbar_init(&tempty[b], kEpiThreads);
-      }
-      mbar_fence_init();
-    }
-  } else if (warp == kMmaWarp) {
-    tmem_alloc<256>(&taddr_s);
   }
   fence_proxy_async();
-  fence_before();
   __syncthreads();
-  fence_after();
-  const uint32_t T = taddr_s;
 
   if (warp == kProdWarp) {
-    // ---- producer: one bulk copy per pre-tiled 8 KB token tile ----
+    // ---- producer: one bulk copy per pre-tiled 16 KB token tile ----
     if (lane == 0) {
       const uint8_t* img = reinterpret_cast<const uint8_t*>(st.tok_bf16);
       for (int i = 0; i < ntiles; ++i) {
         const int s = i % kStages;
         mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
+        if (i < 32) SCAN_STAMP(8 + i);
         mbar_expect_tx(&full[s], kBTile);
         bulk_g2s(Bs + s * kBTile, img + (size_t)(tile0 + i) * kBTile, kBTile, &full[s]);
       }
@@ -160,6 +208,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
         mbar_wait(&full[s], (i / kStages) & 1);
         mbar_wait(&tempty[b], ((i / kAcc) & 1) ^ 1);
         fence_after();
+        if (i < 32) SCAN_STAMP(40 + i);
         const uint32_t b_hi = smem_u32(Bs + s * kBTile), b_lo = b_hi + 4 * kNT * 16;
         const uint32_t d = T + b * kNT;
 #pragma unroll
@@ -177,166 +226,163 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
       }
     }
   } else {
-    // ---- epilogue: thread = (candidate, column half) ----
+    // ---- epilogue: thread = (candidate, 128-column half) ----
     const int c = tid & 127;
     const int half = warp >> 2;
     const bool mine = c < tile.n;
     const int item = tile.item0 + (mine ? c : 0);
-    const int glog = rq.glog[src];
     const int gl_lo = s_lo >> glog, gl_hi = (s_hi - 1) >> glog;  // the source's global groups
-    float* gdst = sc.gmax + ((size_t)item * 3 + src) * sc.gcap;
-    float gate = 0.0f;
+    float* gdst = sc.gmax + ((size_t)item * 3 + src) * sc.gcap - (gl_lo & ~7);
     unsigned* cnt = sc.count + (size_t)item * 3 + src;
-    uint16_t* sdst = sc.surv + (size_t)item * sc.surv_stride + (rq.tok_off[src] - rq.tok_off[0]);
-    if (pass == 2) gate = sc.bound[(size_t)item * 3 + src] - 2.0f * kGateEps;
-    const uint32_t lane_base = T + ((uint32_t)((warp & 3) * 32) << 16) + 32 * half;
+    uint16_t* sdst = sc.surv + (size_t)item * sc.surv_stride + (tok_off - tok_off0);
+    const float gate = pass == 2 ? sc.bound[(size_t)item * 3 + src] - 2.0f * kGateEps : 0.0f;
+    int nb = 0;  // pass 2: survivors buffered in sbuf[.][tid]
+    auto flush = [&]() {
+      const unsigned pos = atomicAdd(cnt, (unsigned)nb);
+      for (int j = 0; j < nb; ++j) sdst[pos + j] = sbuf[j][tid];
+      nb = 0;
+    };
+    const uint32_t lane_base = T + ((uint32_t)((warp & 3) * 32) << 16) + 128 * half;
     for (int i = 0; i < ntiles; ++i) {
       const int b = i % kAcc;
-      const int col0 = (tile0 + i) * kNT + 32 * half;  // global token of column 0
       mbar_wait(&tfull[b], (i / kAcc) & 1);
       fence_after();
-      float v[32];
-      tmem_ld32(lane_base + b * kNT, reinterpret_cast<uint32_t*>(v));
-      tmem_ld_wait();
-      fence_before();
-      mbar_arrive(&tempty[b]);
-      if (col0 + 32 <= g0 || col0 >= g1) continue;  // warp-uniform: half outside the chunk
-      const bool partial = col0 < g0 || col0 + 32 > g1;
-      uint32_t valid = 0xffffffffu;
-      if (partial) {
-        const int a = max(g0 - col0, 0), z = min(g1 - col0, 32);
-        valid = (z >= 32 ? 0xffffffffu : ((1u << z) - 1u)) & ~((1u << a) - 1u);
-      }
-      if (pass == 1) {
-        if (partial) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = ((valid >> e) & 1u) ? v[e] : -INFINITY;
+      if (tid == 0 && i < 32) SCAN_STAMP(72 + i);
+#pragma unroll 1
+      for (int pr = 0; pr < 2; ++pr) {  // two 64-column pieces of this thread's 128 columns
+        float v[64];
+        tmem_ld32(lane_base + b * kNT + 64 * pr, reinterpret_cast<uint32_t*>(v));
+        tmem_ld32(lane_base + b * kNT + 64 * pr + 32, reinterpret_cast<uint32_t*>(v + 32));
+        tmem_ld_wait();
+        if (pr == 1) {
+          fence_before();
+          mbar_arrive(&tempty[b]);
+          if (tid == 0 && i < 32) SCAN_STAMP(104 + i);
         }
-        if (!mine) continue;
-        const int gf = col0 >> glog;
-        switch (glog) {
-          case 0: write_groups<0>(v, gdst, gf, gl_lo, gl_hi); break;
-          case 1: write_groups<1>(v, gdst, gf, gl_lo, gl_hi); break;
-          case 2: write_groups<2>(v, gdst, gf, gl_lo, gl_hi); break;
-          case 3: write_groups<3>(v, gdst, gf, gl_lo, gl_hi); break;
-          case 4: write_groups<4>(v, gdst, gf, gl_lo, gl_hi); break;
-          default: write_groups<5>(v, gdst, gf, gl_lo, gl_hi); break;
-        }
-      } else {
-        uint32_t m = 0u;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) m |= (v[e] >= gate ? 1u : 0u) << e;
-        m &= valid;
-        if (!mine || m == 0u) continue;
-        unsigned pos = atomicAdd(cnt, (unsigned)__popc(m));
-        const int base = col0 - rq.tok_off[src];  // source index of column 0
-        while (m) {
-          const int e = __ffs(m) - 1;
-          m &= m - 1;
-          sdst[pos++] = (uint16_t)(base + e);
+        for (int qq = 0; qq < 2; ++qq) {  // two 32-column quarters
+          const int col0 = (tile0 + i) * kNT + 128 * half + 64 * pr + 32 * qq;  // global token of column 0
+          if (col0 + 32 <= g0 || col0 >= g1 || !mine) continue;
+          const bool partial = col0 < g0 || col0 + 32 > g1;
+          const uint32_t valid = partial ? range_mask(col0, g0, g1) : 0xffffffffu;
+          float* q = v + 32 * qq;
+          if (pass == 1) {
+            if (partial) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) q[e] = ((valid >> e) & 1u) ? q[e] : -INFINITY;
+            }
+            const int gf = col0 >> glog;
+            switch (glog) {
+              case 0: write_groups<0>(q, gdst, gf, gl_lo, gl_hi, !partial); break;
+              case 1: write_groups<1>(q, gdst, gf, gl_lo, gl_hi, !partial); break;
+              case 2: write_groups<2>(q, gdst, gf, gl_lo, gl_hi, !partial); break;
+              case 3: write_groups<3>(q, gdst, gf, gl_lo, gl_hi, !partial); break;
+              case 4: write_groups<4>(q, gdst, gf, gl_lo, gl_hi, !partial); break;
+              default: write_groups<5>(q, gdst, gf, gl_lo, gl_hi, !partial); break;
+            }
+          } else {
+            uint32_t m = 0u;
+#pragma unroll
+            for (int e = 0; e < 32; ++e) m |= (q[e] >= gate ? 1u : 0u) << e;
+            m &= valid;
+            const int base = col0 - tok_off;  // source index of column 0
+            while (m) {  // rare: ~k survivors per (candidate, source) in total
+              const int e = __ffs(m) - 1;
+              m &= m - 1;
+              sbuf[nb++][tid] = (uint16_t)(base + e);
+              if (nb == kSurvBuf) flush();
+            }
+          }
         }
       }
     }
+    if (pass == 2 && nb > 0) flush();
   }
   fence_before();
   __syncthreads();
-  if (warp == kMmaWarp) tmem_free<256>(T);
+  if (warp == kMmaWarp) tmem_free<512>(T);
+  cta_stamp(pass == 1 ? kDbgScan1 : kDbgScan2, 1);
+  if (tid == 0) SCAN_STAMP(150);
 }
 
-// T = k-th largest group maximum of a (candidate, source): one warp per
-// (candidate, source), MSB-first radix select over order-preserving u32
-// images (8-bit digits, early exit once the k-th is isolated).  Also resets
-// the pass-2 survivor counter.
-__device__ __forceinline__ uint32_t f2ord(float f) {
-  const uint32_t u = __float_as_uint(f);
-  return (u >> 31) ? ~u : (u | 0x80000000u);
-}
-__device__ __forceinline__ float ord2f(uint32_t u) {
-  return __uint_as_float((u >> 31) ? (u & 0x7fffffffu) : ~u);
-}
-
+// Gate bound of a (candidate, source): T <= the k-th largest group maximum,
+// by bisection on the value range with warp-wide counts (values held in
+// registers, kBoundPer per lane; no shared-memory histograms).  The
+// invariant count(g >= lo) >= k keeps lo a valid bound; 24 halvings of
+// [min, max] leave it within ~1e-7 of the exact k-th value.  Also resets the
+// pass-2 survivor counter.
 constexpr int kBoundWarps = 4;
+constexpr int kBoundPer = 72;  // values per lane: ng <= 8k + 2 <= 2304
+
+__device__ __forceinline__ void nn_bound_body(const Staged& st, const NNCfg& nn, const NNScan& sc);
 
 __global__ void __launch_bounds__(32 * kBoundWarps) nn_bound_kernel(Staged st, NNCfg nn, NNScan sc) {
-  extern __shared__ uint32_t bvals[];  // [kBoundWarps][gcap]
-  __shared__ unsigned hist_s[kBoundWarps][256];
+  nn_bound_body(st, nn, sc);
+  __syncthreads();
+  cta_stamp(kDbgBound, 1);
+}
+
+template <int PER>
+__device__ __forceinline__ float bisect_kth(const float* g, int ng, int k, int lane) {
+  float v[PER];
+  float mn = INFINITY, mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int i = j * 32 + lane;
+    v[j] = i < ng ? __ldg(g + i) : -INFINITY;
+    mx = fmaxf(mx, v[j]);
+    if (i < ng) mn = fminf(mn, v[j]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  auto count_ge = [&](float x) {
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) c += v[j] >= x ? 1 : 0;
+    return (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
+  };
+  if (count_ge(mx) >= k) return mx;
+  float lo = mn, hi = mx;  // count(>= lo) >= k > count(>= hi)
+#pragma unroll 1
+  for (int it = 0; it < 24; ++it) {
+    const float mid = 0.5f * (lo + hi);
+    if (!(mid > lo && mid < hi)) break;  // adjacent floats
+    if (count_ge(mid) >= k) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void nn_bound_body(const Staged& st, const NNCfg& nn, const NNScan& sc) {
+  cta_stamp(kDbgBound, 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * kBoundWarps + warp;
   const int s = blockIdx.y;
+  griddep_launch();
+  griddep_wait();  // scan pass 1 complete (and the previous select is done with count)
+  cta_stamp(kDbgBound, 2);
   if (item >= st.n_items) return;
   if (lane == 0) sc.count[(size_t)item * 3 + s] = 0u;
-  const ReqInfo rq = st.req[st.item_req[item]];
+  const ReqInfo& rq = st.req[st.item_req[item]];
   const int k = nn.k[s];
   const int lo = rq.tok_off[s] + (s == 1 ? nn.recent : 0), hi = rq.tok_off[s] + rq.len[s];
   if (k == 0 || hi - lo <= k) return;  // no scan: everything (or nothing) is selected
   const int glog = rq.glog[s];
   const int ng = ((hi - 1) >> glog) - (lo >> glog) + 1;
   float* out = sc.bound + (size_t)item * 3 + s;
-  if (ng < k) {
-    if (lane == 0) *out = -INFINITY;
-    return;
-  }
-  const float* g = sc.gmax + ((size_t)item * 3 + s) * sc.gcap;
-  uint32_t* a = bvals + warp * sc.gcap;
-  for (int i = lane; i < ng; i += 32) a[i] = f2ord(g[i]);
-  __syncwarp();
-  uint32_t prefix = 0u, pmask = 0u;
-  int want = k;
-  unsigned* h = hist_s[warp];
-  for (int shift = 24; shift >= 0; shift -= 8) {
-    for (int i = lane; i < 256; i += 32) h[i] = 0u;
-    __syncwarp();
-    for (int i = lane; i < ng; i += 32)
-      if ((a[i] & pmask) == prefix) atomicAdd(&h[(a[i] >> shift) & 255], 1u);
-    __syncwarp();
-    unsigned c8[8], tot = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      c8[j] = h[255 - 8 * lane - j];
-      tot += c8[j];
-    }
-    unsigned incl = tot;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const unsigned excl = incl - tot;
-    const unsigned sel = __ballot_sync(0xffffffffu, excl < (unsigned)want && (unsigned)want <= incl);
-    const int srcl = __ffs(sel) - 1;
-    int digit = 0, above = 0, inb = 0;
-    if (lane == srcl) {
-      unsigned run = excl;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (run + c8[j] >= (unsigned)want) {
-          digit = 255 - 8 * lane - j;
-          above = (int)run;
-          inb = (int)c8[j];
-          break;
-        }
-        run += c8[j];
-      }
-    }
-    digit = __shfl_sync(0xffffffffu, digit, srcl);
-    above = __shfl_sync(0xffffffffu, above, srcl);
-    inb = __shfl_sync(0xffffffffu, inb, srcl);
-    want -= above;
-    prefix |= (uint32_t)digit << shift;
-    pmask |= 255u << shift;
-    __syncwarp();
-    if (inb == want) {  // the whole bucket is in the top k: its minimum is the k-th
-      uint32_t mn = 0xffffffffu;
-      for (int i = lane; i < ng; i += 32)
-        if ((a[i] & pmask) == prefix) mn = min(mn, a[i]);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      prefix = mn;
-      break;
-    }
-  }
-  if (lane == 0) *out = ord2f(prefix);
+  const float* g = sc.gmax + ((size_t)item * 3 + s) * sc.gcap + ((lo >> glog) & 7);
+  float T;
+  if (ng < k) T = -INFINITY;
+  else if (ng <= 256) T = bisect_kth<8>(g, ng, k, lane);
+  else if (ng <= 512) T = bisect_kth<16>(g, ng, k, lane);
+  else if (ng <= 1024) T = bisect_kth<32>(g, ng, k, lane);
+  else T = bisect_kth<kBoundPer>(g, ng, k, lane);
+  if (lane == 0) *out = T;
 }
+
+cudaError_t set_dbg_cta_scan(long long* dev) { return set_dbg_cta_tu(dev); }
 
 cudaError_t set_debug_timeline(long long* dev, int block) {
   cudaError_t e = cudaMemcpyToSymbol(g_dbg_block, &block, sizeof(block));
@@ -347,21 +393,16 @@ cudaError_t set_debug_timeline(long long* dev, int block) {
 cudaError_t launch_nn_scan(const Staged& st, const NNCfg& nn, const NNScan& sc, int pass,
                            cudaStream_t s) {
   if (st.n_work == 0) return cudaSuccess;
-  const size_t smem = 2 * kAHalf + kStages * kBTile;
+  const size_t smem = 2 * kAHalf + (size_t)kStages * kBTile;
   cudaError_t e = cudaFuncSetAttribute(nn_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  nn_scan_kernel<<<st.n_work, kTcThreads, smem, s>>>(st, nn, sc, pass);
-  return cudaGetLastError();
+  return launch_pdl(nn_scan_kernel, dim3(st.n_work), dim3(kTcThreads), smem, s, st, nn, sc, pass);
 }
 
 cudaError_t launch_nn_bound(const Staged& st, const NNCfg& nn, const NNScan& sc, cudaStream_t s) {
   if (st.n_items == 0) return cudaSuccess;
-  const size_t smem = (size_t)kBoundWarps * sc.gcap * 4;
-  cudaError_t e = cudaFuncSetAttribute(nn_bound_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
   dim3 grid((st.n_items + kBoundWarps - 1) / kBoundWarps, 3);
-  nn_bound_kernel<<<grid, 32 * kBoundWarps, smem, s>>>(st, nn, sc);
-  return cudaGetLastError();
+  return launch_pdl(nn_bound_kernel, grid, dim3(32 * kBoundWarps), 0, s, st, nn, sc);
 }
 
 }  // namespace tav2

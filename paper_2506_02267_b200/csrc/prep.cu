@@ -8,6 +8,7 @@
 
 #include "tav2_common.cuh"
 #include "tc_common.cuh"
+#include "dbg.cuh"
 
 namespace tav2 {
 
@@ -30,6 +31,10 @@ __device__ __forceinline__ float sumsq8(const float* v) {
 }
 
 __global__ void __launch_bounds__(256) prep_kernel(Staged st) {
+  cta_stamp(kDbgPrep, 0);
+  griddep_launch();
+  griddep_wait();  // the previous step's kernels may still read tok_unit / cand_unit
+  cta_stamp(kDbgPrep, 2);
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < st.n_tok) {
     const int4* src = reinterpret_cast<const int4*>(st.emb + (size_t)i * kEmbed);
@@ -50,16 +55,17 @@ __global__ void __launch_bounds__(256) prep_kernel(Staged st) {
 #pragma unroll
     for (int j = 0; j < kEmbed; j += 4) dst[j / 4] = make_float4(u[j], u[j + 1], u[j + 2], u[j + 3]);
     // bf16 hi/lo image of the unit row, pre-tiled for the tensor-core NN
-    // scores: 64-token tiles of 8 KB = [8 chunks (hi 0-3, lo 4-7)][64 rows][16 B]
-    // (the UMMA K-major no-swizzle B-operand layout), one bulk copy per tile
-    uint8_t* tile = reinterpret_cast<uint8_t*>(st.tok_bf16) + (size_t)(i >> 6) * 8192 + (i & 63) * 16;
+    // scan (kScanTile-token tiles, UMMA K-major no-swizzle B-operand layout,
+    // tav2_common.cuh), one bulk copy per tile
+    uint8_t* tile = reinterpret_cast<uint8_t*>(st.tok_bf16) + (size_t)(i / kScanTile) * kScanTileBytes +
+                    (i % kScanTile) * 16;
 #pragma unroll
     for (int j = 0; j < kEmbed; j += 8) {
       uint32_t hi[4], lo[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) tc::split_pair(u[j + 2 * e], u[j + 2 * e + 1], hi[e], lo[e]);
-      *reinterpret_cast<uint4*>(tile + (j / 8) * 1024) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<uint4*>(tile + (4 + j / 8) * 1024) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      *reinterpret_cast<uint4*>(tile + (j / 8) * (kScanTile * 16)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4*>(tile + (4 + j / 8) * (kScanTile * 16)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     }
     return;
   }
@@ -82,11 +88,12 @@ __global__ void __launch_bounds__(256) prep_kernel(Staged st) {
   }
 }
 
+cudaError_t set_dbg_cta_prep(long long* dev) { return set_dbg_cta_tu(dev); }
+
 cudaError_t launch_prep(const Staged& st, cudaStream_t s) {
   int n = st.n_tok + st.n_items;
   if (n == 0) return cudaSuccess;
-  prep_kernel<<<(n + 255) / 256, 256, 0, s>>>(st);
-  return cudaGetLastError();
+  return launch_pdl(prep_kernel, dim3((n + 255) / 256), dim3(256), 0, s, st);
 }
 
 }  // namespace tav2

@@ -35,6 +35,7 @@
 #include "encode.cuh"
 #include "tav2_common.cuh"
 #include "tc_common.cuh"
+#include "dbg.cuh"
 
 namespace tav2 {
 
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
     is.bar_wb = &bar_wb;
     is.NT = NT;
     is.S_pad = S_pad;
-    is.dbg = blockIdx.x == 0 ? g_dbg_skut : nullptr;
+    is.dbg = kDebug && blockIdx.x == 0 ? g_dbg_skut : nullptr;
     is.load_wa(img.wa[0], kImgWA);
     is.load_wb(img.wb[0]);
   }
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
   const uint32_t cA = lanebase + kColA + 64 * t;
   const bool in_seq = r < S;
   uint32_t n_mma = 0, n_done = 0;
-  long long* dbg = (blockIdx.x == 0 && tid == 0) ? g_dbg_skut : nullptr;
+  long long* dbg = (kDebug && blockIdx.x == 0 && tid == 0) ? g_dbg_skut : nullptr;
   auto wait_mma = [&]() {
     __syncwarp();
     mbar_wait_sleep(&bar_mma, n_mma & 1);
@@ -312,6 +313,9 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
     ++n_done;
   };
 
+  griddep_launch();
+  griddep_wait();  // NN selection (idx) and prep (tok_unit, cand_unit) complete
+  cta_stamp(kDbgSkut, 2);
   for (int item = blockIdx.x; item < n; item += gridDim.x) {
     // ---- K3: gather + encode this row (or load caller features) ----
     float x[kDModel];
@@ -749,6 +753,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
     Params p, SkutImages img, NNCfg nn, Staged st, int use_staged, const int32_t* idx,
     const float* Fin, const uint8_t* fmask, int n, float* U, float* logits, float* pooled_out) {
   extern __shared__ __align__(1024) uint8_t sm[];
+  cta_stamp(kDbgSkut, 0);
   __shared__ uint32_t taddr_s;
   __shared__ uint32_t valid_w[8];  // key-validity bitmask, bit r of word r/32
   __shared__ __align__(16) float lnp_s[kMaxLayers][4][kDModel];
@@ -811,7 +816,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
   is.R = 256u * t;
   is.S_pad = S_pad;
   is.NK = t == 0 ? NK0 : S_pad;
-  is.dbg = issuer && blockIdx.x == 0 && t == 0 && g_dbg_skut != nullptr;
+  is.dbg = kDebug && issuer && blockIdx.x == 0 && t == 0 && g_dbg_skut != nullptr;
   if (issuer && t == 1) {  // loader: initial fills
     mbar_expect_tx(&tc2.wa_full, kImgWA);
     bulk_g2s(WA, img.wa[0], kImgWA, &tc2.wa_full);
@@ -823,7 +828,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
   const uint32_t cA = lanebase + kTA;
   const bool in_seq = mapped && r < S;
   uint32_t n_mma = 0, n_kv = 0, n_done = 0;
-  long long* dbg = (blockIdx.x == 0 && tid == 0) ? g_dbg_skut : nullptr;
+  long long* dbg = (kDebug && blockIdx.x == 0 && tid == 0) ? g_dbg_skut : nullptr;
   auto wait_mma = [&]() {
     __syncwarp();
     mbar_wait_sleep(&tc2.mma[t], n_mma & 1);
@@ -840,6 +845,9 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
   // warp-uniform causal bound: the largest row of this warp
   const int wmax_row = rpw * kb + rpw - 1;
 
+  griddep_launch();
+  griddep_wait();  // NN selection (idx) and prep (tok_unit, cand_unit) complete
+  cta_stamp(kDbgSkut, 2);
   for (int item = blockIdx.x; item < n; item += gridDim.x) {
     // ---- K3: gather + encode this row (or load caller features) ----
     float x[kDModel];
@@ -1161,7 +1169,10 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
   fence_before();
   __syncthreads();
   if (warp == 0) tmem_free<512>(0u);
+  cta_stamp(kDbgSkut, 1);
 }
+
+cudaError_t set_dbg_cta_skut(long long* dev) { return set_dbg_cta_tu(dev); }
 
 cudaError_t set_debug_skut(long long* dev) { return cudaMemcpyToSymbol(g_dbg_skut, &dev, sizeof(dev)); }
 
@@ -1180,9 +1191,8 @@ cudaError_t launch_skut_tc(const Params& p, const SkutImages& img, const NNCfg& 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   Staged dummy{};
-  kern<<<n < sms ? n : sms, kSkThreads, smem, s>>>(p, img, nn, st ? *st : dummy, st != nullptr, idx, F, fmask, n,
-                                                  U, logits, pooled);
-  e = cudaGetLastError();
+  e = launch_pdl(kern, dim3(n < sms ? n : sms), dim3(kSkThreads), smem, s, p, img, nn, st ? *st : dummy,
+                 (int)(st != nullptr), idx, F, fmask, n, U, logits, pooled);
   if (e != cudaSuccess) {
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, kern);

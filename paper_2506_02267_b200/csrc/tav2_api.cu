@@ -259,12 +259,13 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
   if ((e = cudaMalloc(&c->tok_unit, (size_t)(cdiv((int)std::max<int64_t>(T, 1), 64) + 1) * 64 * kEmbed * 4)) !=
       cudaSuccess)
     return bad(e, "tok_unit");
-  if ((e = cudaMalloc(&c->tok_bf16, (size_t)(cdiv((int)std::max<int64_t>(T, 1), 64) + 1) * 8192)) != cudaSuccess)
+  if ((e = cudaMalloc(&c->tok_bf16, (size_t)(cdiv((int)std::max<int64_t>(T, 1), kScanTile) + 1) * kScanTileBytes)) !=
+      cudaSuccess)
     return bad(e, "tok_bf16");
   if ((e = cudaMalloc(&c->cand_unit, (size_t)N * kEmbed * 4)) != cudaSuccess) return bad(e, "cand_unit");
   // scan buffers: a source has at most max(8k + 2, 16384/32 + 2) groups
   // (planner), a (candidate, source) at most its source length of survivors
-  c->scan.gcap = (std::max(8 * c->kmax + 2, kCaps[0] / 32 + 2) + 7) & ~7;
+  c->scan.gcap = (std::max(8 * c->kmax + 2, kCaps[0] / 32 + 2) + 8 + 7) & ~7;  // + 8: aligned rows
   c->scan.surv_stride =
       (int)((std::min<int64_t>(std::max<int64_t>(T, 8), kCaps[0] + kCaps[1] + kCaps[2]) + 7) & ~int64_t(7));
   if ((e = cudaMalloc(&c->scan.gmax, (size_t)N * 3 * c->scan.gcap * 4)) != cudaSuccess)
@@ -450,8 +451,8 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
   // ---- NN work decomposition: one CTA per (candidate tile, source, chunk).
   // A source with n <= k tokens needs no scan (all selected).  Otherwise the
   // threshold scan (nn_scan.cu) groups its tokens in G = 2^glog (about 4k to
-  // 8k groups, G <= 32); chunk boundaries are 64-token aligned in the global
-  // token index so every group lies in one chunk.  RT tail and IMP take one
+  // 8k groups, G <= 32); chunk boundaries are kScanTile-aligned in the global
+  // token index so every group and tile lies in one chunk.  RT tail and IMP take one
   // chunk per tile; LL chunks (>= kMinChunk tokens) fill the SMs. ----
   auto scanned = [&](const tav2_request& q, int s) {
     const int lo = s == 1 ? nn.recent : 0;
@@ -496,9 +497,10 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
           if (!scanned(q, s)) continue;
           int nch = 1;
           if (s == 0) nch = std::max(1, std::min(ll_chunks_target, (hi - lo) / kMinChunk));
-          const int64_t step = std::max<int64_t>(64, ((int64_t)cdiv(hi - lo, nch) + 63) & ~int64_t(63));
+          const int64_t step = std::max<int64_t>(kScanTile, ((int64_t)cdiv(hi - lo, nch) + kScanTile - 1) &
+                                                                   ~int64_t(kScanTile - 1));
           for (int64_t a = tok_off[s] + lo, end = tok_off[s] + hi; a < end;) {
-            const int64_t b = std::min(end, (a & ~int64_t(63)) + step);
+            const int64_t b = std::min(end, (a & ~int64_t(kScanTile - 1)) + step);
             vw.push_back(NNWork{tid, s, (int32_t)(a - tok_off[s]), (int32_t)(b - tok_off[s])});
             t.nwork[s]++;
             a = b;
@@ -713,6 +715,13 @@ int tav2_last_launch_count(const tav2_ctx* c) { return c ? c->launches : 0; }
 
 int tav2_debug_timeline(long long* dev, int block) {
   return set_debug_timeline(dev, block) == cudaSuccess && set_debug_skut(dev ? dev + 320 : nullptr) == cudaSuccess ? TAV2_OK : fail(TAV2_ECUDA, "debug timeline");
+}
+
+int tav2_debug_cta(long long* dev) {
+  if (set_dbg_cta_prep(dev) != cudaSuccess || set_dbg_cta_scan(dev) != cudaSuccess ||
+      set_dbg_cta_select(dev) != cudaSuccess || set_dbg_cta_skut(dev) != cudaSuccess)
+    return fail(TAV2_ECUDA, "debug cta stamps");
+  return TAV2_OK;
 }
 
 int tav2_set_profiling(tav2_ctx* c, int on) {

@@ -38,6 +38,10 @@ struct ReqInfo {          // one unique request (DedupBatch.users entry)
 // Approximate-score gate margin of the threshold scan: > the bf16x3 score
 // error bound 2.3e-5 for unit vectors (nn_scan.cu).
 constexpr float kGateEps = 4e-5f;
+// The scan's token operand: 128-token tiles of the bf16 hi/lo unit rows in the
+// UMMA K-major no-swizzle layout, [8 chunks (hi 0-3, lo 4-7)][128 rows][16 B].
+constexpr int kScanTile = 256;
+constexpr int kScanTileBytes = 8 * kScanTile * 16;
 
 struct NNWork {           // one (candidate tile, source, token chunk) unit
   int32_t tile;           // candidate tile id
@@ -58,7 +62,7 @@ struct NNScan {
   float* gmax;            // [items][3][gcap] pass-1 group maxima
   float* bound;           // [items][3] k-th largest group maximum
   unsigned* count;        // [items][3] pass-2 survivor counts
-  uint16_t* surv;         // [items][surv_stride] survivor source indices (per-source sub-lists)
+  uint16_t* surv;         // [items][surv_stride] survivor source indices, per-source sub-lists
   int gcap, surv_stride;
 };
 
@@ -161,6 +165,35 @@ __host__ __device__ inline double key_score(uint64_t key) {
 
 }  // namespace tav2
 
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch: every kernel of the path is launched with
+// programmatic stream serialization, lets its dependents launch as soon as
+// all of its CTAs started (griddep_launch) and runs its input-independent
+// prologue (barrier init, TMEM alloc, plan / weight loads) before
+// griddep_wait(), which returns once the preceding kernel completed and its
+// writes are visible.  Outside a PDL chain both are no-ops.
+// ---------------------------------------------------------------------------
+namespace tav2 {
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+}  // namespace tav2
+
 // Host-side launchers (defined in the kernel translation units).
 namespace tav2 {
 cudaError_t launch_prep(const Staged& st, cudaStream_t s);
@@ -171,6 +204,10 @@ cudaError_t launch_nn_select(const Staged& st, const NNCfg& nn, const NNScan& sc
                              float* scores, cudaStream_t s);
 cudaError_t set_debug_timeline(long long* dev, int block);
 cudaError_t set_debug_skut(long long* dev);
+cudaError_t set_dbg_cta_prep(long long* dev);
+cudaError_t set_dbg_cta_scan(long long* dev);
+cudaError_t set_dbg_cta_select(long long* dev);
+cudaError_t set_dbg_cta_skut(long long* dev);
 bool make_rows32_map(CUtensorMap* map, const void* base, int64_t rows, int box_rows);
 cudaError_t launch_encode(const Staged& st, const NNCfg& nn, const Params& p, const int32_t* idx,
                           float* F, uint8_t* mask, cudaStream_t s);

@@ -189,3 +189,43 @@ def test_full_size_c2_properties(mode):
 
     check_nn_contract(idx[sample], ref_idx, fn, kth, nn.segment_starts(), nn.segment_lengths())
     assert np.abs(logits[sample] - lg).max() <= TOL[mode]
+
+
+@pytest.mark.parametrize("cfg", [(32, 96, 32, 32), (32, 256, 32, 32)], ids=["k96", "k256"])
+def test_full_size_degenerate_ties(cfg):
+    """L=16384 with a zero candidate (every score ties at 0 -> the k lowest
+    indices), 3000 identical LL tokens (more survivors than the select
+    kernel caches), and that direction negated: exercises the scan's
+    streaming select path and the stable tie rule at full size."""
+    nn = P.NNConfig(*cfg)
+    r = P.generate_requests(1, 4, ll_tokens=16384, seed=5)[0]
+    ud = from_user(r.user)
+    ud["ll_emb"] = ud["ll_emb"].copy()
+    v = ud["ll_emb"][500].copy()
+    ud["ll_emb"][100:3100] = v
+    cands = r.candidates.copy()
+    cands[0] = 0.0
+    cands[1] = v.astype(np.float32)
+    cands[2] = -v.astype(np.float32)
+    eng = _engine_for(nn, cap=Capacity(1, 4, 16896))
+    logits, idx = eng.rank_requests([(to_user(ud), cands, r.ctx)], mode="bf16", return_indices=True)
+    Pd = orc.model_init(0, seq_len=nn.seq_len)
+    lg, det = orc.rank_request(ud, cands, r.ctx, Pd, cfg, return_detail=True)
+    ref_idx = np.full((4, nn.seq_len), -1, np.int32)
+    kth = np.zeros((4, 4))
+    for j in range(4):
+        for st, sg in zip(nn.segment_starts(), det["segs"][j]):
+            ref_idx[j, st:st + len(sg)] = sg
+        for g, name in ((0, "nn_lifelong"), (2, "nn_realtime_tail"), (3, "nn_impression")):
+            kth[j, g] = det["scores"][j][name][-1]
+
+    def fn(i, g, ii):
+        src = {0: "ll", 2: "rt", 3: "imp"}[g]
+        return orc.similarity_scores(ud[f"{src}_emb"], cands[i])[ii]
+
+    check_nn_contract(idx, ref_idx, fn, kth, nn.segment_starts(), nn.segment_lengths())
+    # exact ties: identical sets, not just within tolerance
+    a, b = nn.segment_starts()[0], nn.segment_starts()[0] + nn.segment_lengths()[0]
+    assert np.array_equal(idx[0, a:b], ref_idx[0, a:b])
+    assert np.array_equal(idx[1, a:b], ref_idx[1, a:b])
+    assert np.abs(logits - lg).max() <= TOL["bf16"]

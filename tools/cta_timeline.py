@@ -1,0 +1,56 @@
+"""Per-kernel CTA timeline of one C2 step (globaltimer stamps at CTA start /
+end, tav2_debug_cta): when each kernel's first CTA starts, how long CTAs run,
+when the last ends -- shows launch gaps, ramp and tails of the path.
+
+    python tools/cta_timeline.py [n_candidates] [--flush]
+"""
+import os
+import sys
+
+os.environ["TAV2_DEBUG"] = "1"  # the timeline-instrumented library
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import paper_2506_02267_b200 as P  # noqa: E402
+from paper_2506_02267_b200 import _native as N  # noqa: E402
+from paper_2506_02267_b200.runtime import Capacity, Engine  # noqa: E402
+
+KERNELS = ["prep", "nn_scan1", "nn_bound", "nn_scan2", "nn_select", "skut"]
+n_cand = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 1000
+nn = P.NNConfig()
+model = P.RankingModel.init(P.ModelConfig.for_nn(nn), seed=0)
+eng = Engine(model, capacity=Capacity(1, n_cand, 16896))
+r = P.generate_requests(1, n_cand, 16384, seed=1)[0]
+eng.stage([(r.user, r.candidates, r.ctx)])
+logits = torch.empty((n_cand, 4), device="cuda")
+flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+for _ in range(5):
+    eng.run_staged("bf16", logits)
+torch.cuda.synchronize()
+buf = torch.zeros(6 * 3 * 4096, dtype=torch.int64, device="cuda")
+N.lib().tav2_debug_cta(buf.data_ptr())
+if "--flush" in sys.argv:
+    flush.zero_()
+torch.cuda.synchronize()
+eng.run_staged("bf16", logits)
+torch.cuda.synchronize()
+N.lib().tav2_debug_cta(None)
+t = buf.cpu().numpy().reshape(6, 3, 4096)
+t0 = min(int(t[k, 0][t[k, 0] > 0].min()) for k in range(6) if (t[k, 0] > 0).any())
+for k, name in enumerate(KERNELS):
+    n = int((t[k, 0] > 0).sum())
+    if not n:
+        continue
+    st, en, rd = t[k, 0, :n], t[k, 1, :n], t[k, 2, :n]
+    us = lambda x: (x - t0) / 1e3  # noqa: E731
+    line = f"{name:10s} ctas {n:5d}  launch {us(st.min()):7.2f}..{us(st.max()):7.2f}"
+    if (rd > 0).all():
+        line += f"  ready {us(rd.min()):7.2f}..{us(rd.max()):7.2f}"
+    if (en > 0).all():
+        line += f"  end {us(en.min()):7.2f}..{us(en.max()):7.2f}"
+        if (rd > 0).all():
+            d = (en - rd) / 1e3
+            line += f"  run med {np.median(d):6.2f} max {d.max():6.2f} (argmax {int(d.argmax())})"
+    print(line)
