@@ -32,10 +32,12 @@
 // itself needs 32 / 64 / 128 cycles at N = 64 / 128 / 256), so N = 256 is the
 // first shape where a single issuer keeps the tensor core busy: 6 MMAs
 // (2 k-steps x 3 terms) per 256-token tile, ~3 tensor cycles per token.
-// Roles (320 threads): warps 0-7 epilogue (warp w reads TMEM lanes 32*(w%4)..
-// = candidates, column half w/4 = 128 tokens of every tile), warp 8 producer
+// Roles (576 threads): warps 0-15 epilogue (warp w reads TMEM lanes
+// 32*(w%4).. = candidates, column quarter w/4 = 64 tokens of every tile, two
+// tcgen05.ld + one wait per tile; four warps per SM sub-partition hide the
+// ~200-cycle TMEM load latency), warp 16 producer
 // (one 32 KB cp.async.bulk per pre-tiled 256-token bf16 hi/lo image written by
-// prep_kernel, 4-stage ring), warp 9 MMA issuer.  TMEM: 2 accumulator
+// prep_kernel, 4-stage ring), warp 17 MMA issuer.  TMEM: 2 accumulator
 // buffers x 256 columns.  Chunk boundaries are tile aligned (planner), so
 // every group is scanned by exactly one CTA.
 #include <cuda.h>
@@ -54,9 +56,9 @@ using namespace tc;
 constexpr int kNT = kScanTile;   // tokens per tile and MMA (N = 256)
 constexpr int kStages = 4;       // smem ring depth
 constexpr int kAcc = 2;          // TMEM accumulator buffers (2 x 256 columns)
-constexpr int kTcThreads = 320;
-constexpr int kProdWarp = 8, kMmaWarp = 9;
-constexpr int kEpiThreads = 256;
+constexpr int kTcThreads = 576;
+constexpr int kProdWarp = 16, kMmaWarp = 17;
+constexpr int kEpiThreads = 512;
 constexpr int kBTile = kScanTileBytes;      // 8 chunks (hi 0-3, lo 4-7) x 256 rows x 16 B = 32 KB
 constexpr int kASlab = 128 * 16;            // one 16-byte K chunk of 128 candidate rows
 constexpr int kAHalf = 4 * kASlab;          // 32 bf16 of 128 rows (8 KB)
@@ -226,9 +228,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
       }
     }
   } else {
-    // ---- epilogue: thread = (candidate, 128-column half) ----
+    // ---- epilogue: thread = (candidate, 64-column quarter) ----
     const int c = tid & 127;
-    const int half = warp >> 2;
+    const int cq = warp >> 2;
     const bool mine = c < tile.n;
     const int item = tile.item0 + (mine ? c : 0);
     const int gl_lo = s_lo >> glog, gl_hi = (s_hi - 1) >> glog;  // the source's global groups
@@ -242,26 +244,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
       for (int j = 0; j < nb; ++j) sdst[pos + j] = sbuf[j][tid];
       nb = 0;
     };
-    const uint32_t lane_base = T + ((uint32_t)((warp & 3) * 32) << 16) + 128 * half;
+    const uint32_t lane_base = T + ((uint32_t)((warp & 3) * 32) << 16) + 64 * cq;
     for (int i = 0; i < ntiles; ++i) {
       const int b = i % kAcc;
       mbar_wait(&tfull[b], (i / kAcc) & 1);
       fence_after();
       if (tid == 0 && i < 32) SCAN_STAMP(72 + i);
-#pragma unroll 1
-      for (int pr = 0; pr < 2; ++pr) {  // two 64-column pieces of this thread's 128 columns
+      {
         float v[64];
-        tmem_ld32(lane_base + b * kNT + 64 * pr, reinterpret_cast<uint32_t*>(v));
-        tmem_ld32(lane_base + b * kNT + 64 * pr + 32, reinterpret_cast<uint32_t*>(v + 32));
+        tmem_ld32(lane_base + b * kNT, reinterpret_cast<uint32_t*>(v));
+        tmem_ld32(lane_base + b * kNT + 32, reinterpret_cast<uint32_t*>(v + 32));
         tmem_ld_wait();
-        if (pr == 1) {
-          fence_before();
-          mbar_arrive(&tempty[b]);
-          if (tid == 0 && i < 32) SCAN_STAMP(104 + i);
-        }
+        fence_before();
+        mbar_arrive(&tempty[b]);
+        if (tid == 0 && i < 32) SCAN_STAMP(104 + i);
 #pragma unroll
         for (int qq = 0; qq < 2; ++qq) {  // two 32-column quarters
-          const int col0 = (tile0 + i) * kNT + 128 * half + 64 * pr + 32 * qq;  // global token of column 0
+          const int col0 = (tile0 + i) * kNT + 64 * cq + 32 * qq;  // global token of column 0
           if (col0 + 32 <= g0 || col0 >= g1 || !mine) continue;
           const bool partial = col0 < g0 || col0 + 32 > g1;
           const uint32_t valid = partial ? range_mask(col0, g0, g1) : 0xffffffffu;
