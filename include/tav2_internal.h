@@ -20,10 +20,12 @@ int tav2_tc_selftest(int which, const void* A, const void* B, void* D, int N, in
  * candidate (slots 320..447).  NULL disables.  Not thread-safe. */
 int tav2_debug_timeline(long long* dev, int block);
 
-/* Debug: device buffer (>= 6 * 2 * 4096 int64) receiving per-CTA %globaltimer
- * start/end stamps of every ranking-path kernel ([kernel][start|end][CTA];
- * kernels: prep, nn_scan pass 1, nn_bound, nn_scan pass 2, nn_select, skut).
- * NULL disables.  Not thread-safe. */
+/* Debug (libtav2_debug.so only): device buffer (>= 7 * 3 * 4096 int64)
+ * receiving per-CTA %globaltimer stamps of every ranking-path kernel
+ * ([kernel][start | end | inputs ready][CTA]; kernels: prep, nn_scan pass 1,
+ * nn_bound, nn_scan pass 2, nn_select, skut) and, at kernel 6, per
+ * (candidate, source) select time and survivor count.  NULL disables.  Not
+ * thread-safe. */
 int tav2_debug_cta(long long* dev);
 
 #ifdef __cplusplus

@@ -32,6 +32,22 @@ __device__ __forceinline__ void cta_stamp(int kid, int which) {
   }
 }
 
+// debug: a per-(candidate, source) record of the select kernel at kernel
+// id 6: [6][0][item*3+s] = warp time (ns), [6][1][item*3+s] = survivors
+__device__ __forceinline__ void sel_record(int slot, long long dur, long long n) {
+  if constexpr (!kDebug) return;
+  long long* d = g_dbg_cta;
+  if (d != nullptr && slot < kDbgCtas) {
+    d[(6 * 3 + 0) * kDbgCtas + slot] = dur;
+    d[(6 * 3 + 1) * kDbgCtas + slot] = n;
+  }
+}
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 static inline cudaError_t set_dbg_cta_tu(long long* dev) {
   return cudaMemcpyToSymbol(g_dbg_cta, &dev, sizeof(dev));
 }

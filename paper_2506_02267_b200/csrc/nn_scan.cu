@@ -4,12 +4,13 @@
 // Reference semantics (nnsearch.py:274-286, :313-347): score(t, c) =
 // f64(unit(dequantize(q_t))) . f64(unit(c)), top-k by (score desc, index asc).
 //
-// Tensor-core part: approximate scores for every (candidate, token) as a
-// bf16x3 GEMM of the f32 unit vectors (x = hi + lo, a.b ~= ah.bh + ah.bl +
-// al.bh), M = 128 candidates x N = 256 tokens x K = 32 per tile, f32
-// accumulation in TMEM.  |approx - exact| <= 3*2^-18*sum|a_j b_j| + f32
-// accumulation <= 2.3e-5 for unit vectors (measured max 5.7e-6,
-// tools/measure_bf16x3_err.py) < kGateEps.
+// Tensor-core part: approximate scores for every (candidate, token) as an
+// fp16 GEMM of the f32 unit vectors rounded to fp16, M = 128 candidates x
+// N = 256 tokens x K = 32 per tile, f32 accumulation in TMEM:
+// |approx - exact| < 9.8e-4 < kGateEps (tav2_common.cuh).  The margin only
+// widens the gate: the score density near the k-th is low, so the gate keeps
+// ~130 of 16,384 LL tokens for k = 96 (bf16x3 products would keep ~105 for
+// three times the tensor work and twice the token bytes).
 //
 //   pass 1 (group max): every (candidate, source) splits the source into
 //          groups of G = 2^glog consecutive tokens (G-aligned in the global
@@ -30,17 +31,18 @@
 // MMA: N = 256 tokens per instruction.  One warp issues a tcgen05.mma only
 // every ~120 cycles whatever its N (tools/mma_bench.cu: the tensor core
 // itself needs 32 / 64 / 128 cycles at N = 64 / 128 / 256), so N = 256 is the
-// first shape where a single issuer keeps the tensor core busy: 6 MMAs
-// (2 k-steps x 3 terms) per 256-token tile, ~3 tensor cycles per token.
+// first shape where a single issuer keeps the tensor core busy: 2 MMAs
+// (2 k-steps of 16) per 256-token tile.
 // Roles (576 threads): warps 0-15 epilogue (warp w reads TMEM lanes
 // 32*(w%4).. = candidates, column quarter w/4 = 64 tokens of every tile, two
 // tcgen05.ld + one wait per tile; four warps per SM sub-partition hide the
 // ~200-cycle TMEM load latency), warp 16 producer
-// (one 32 KB cp.async.bulk per pre-tiled 256-token bf16 hi/lo image written by
-// prep_kernel, 4-stage ring), warp 17 MMA issuer.  TMEM: 2 accumulator
+// (one 16 KB cp.async.bulk per pre-tiled 256-token fp16 image written by
+// prep_kernel, 6-stage ring), warp 17 MMA issuer.  TMEM: 2 accumulator
 // buffers x 256 columns.  Chunk boundaries are tile aligned (planner), so
 // every group is scanned by exactly one CTA.
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <float.h>
 #include <stdint.h>
@@ -54,14 +56,14 @@ namespace tav2 {
 using namespace tc;
 
 constexpr int kNT = kScanTile;   // tokens per tile and MMA (N = 256)
-constexpr int kStages = 4;       // smem ring depth
+constexpr int kStages = 6;       // smem ring depth
 constexpr int kAcc = 2;          // TMEM accumulator buffers (2 x 256 columns)
 constexpr int kTcThreads = 576;
 constexpr int kProdWarp = 16, kMmaWarp = 17;
 constexpr int kEpiThreads = 512;
-constexpr int kBTile = kScanTileBytes;      // 8 chunks (hi 0-3, lo 4-7) x 256 rows x 16 B = 32 KB
+constexpr int kBTile = kScanTileBytes;      // 4 chunks x 256 rows x 16 B = 16 KB
 constexpr int kASlab = 128 * 16;            // one 16-byte K chunk of 128 candidate rows
-constexpr int kAHalf = 4 * kASlab;          // 32 bf16 of 128 rows (8 KB)
+constexpr int kATile = 4 * kASlab;          // 32 fp16 of 128 rows (8 KB)
 constexpr int kSurvBuf = 16;                // pass-2 survivors buffered per thread before a flush
 
 // Debug timeline (tav2_debug_timeline): %globaltimer stamps of work unit
@@ -124,8 +126,8 @@ __device__ __forceinline__ uint32_t range_mask(int col0, int g0, int g1) {
 __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg nn, NNScan sc,
                                                                 int pass) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  uint8_t* As = sm;               // candidates: [hi: 4 chunks][lo: 4 chunks] x 128 rows x 16 B
-  uint8_t* Bs = sm + 2 * kAHalf;  // [kStages][32 KB token image]
+  uint8_t* As = sm;          // candidates: 4 chunks x 128 rows x 16 B (fp16)
+  uint8_t* Bs = sm + kATile;  // [kStages][16 KB token image]
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull[kAcc], tempty[kAcc];
   __shared__ uint32_t taddr_s;
   __shared__ uint16_t sbuf[kSurvBuf][kEpiThreads];  // pass 2: per-thread survivor buffer
@@ -166,10 +168,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
   fence_after();
   const uint32_t T = taddr_s;
   griddep_launch();
-  griddep_wait();  // prep (cand_unit, tok_bf16) / bound (gate) complete
+  griddep_wait();  // prep (cand_unit, tok_img) / bound (gate) complete
   cta_stamp(pass == 1 ? kDbgScan1 : kDbgScan2, 2);
   if (tid == 0) SCAN_STAMP(0);
-  // ---- candidate hi/lo (A operand, smem K-major slabs) ----
+  // ---- candidates fp16 (A operand, smem K-major slabs) ----
   if (warp < 4) {
     const int c = tid;
     const bool real = c < tile.n;
@@ -178,11 +180,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
     for (int ch = 0; ch < 4; ++ch) {  // 8 elements per 16-byte chunk
       const float4 v0 = cu[2 * ch], v1 = cu[2 * ch + 1];
       const float f[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-      uint32_t hi[4], lo[4];
+      uint32_t h[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) split_pair(real ? f[2 * i] : 0.f, real ? f[2 * i + 1] : 0.f, hi[i], lo[i]);
-      *reinterpret_cast<uint4*>(As + ch * kASlab + c * 16) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<uint4*>(As + kAHalf + ch * kASlab + c * 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      for (int i = 0; i < 4; ++i) {
+        const __half2 p = __floats2half2_rn(real ? f[2 * i] : 0.f, real ? f[2 * i + 1] : 0.f);
+        h[i] = *reinterpret_cast<const uint32_t*>(&p);
+      }
+      *reinterpret_cast<uint4*>(As + ch * kASlab + c * 16) = make_uint4(h[0], h[1], h[2], h[3]);
     }
   }
   fence_proxy_async();
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
   if (warp == kProdWarp) {
     // ---- producer: one bulk copy per pre-tiled 16 KB token tile ----
     if (lane == 0) {
-      const uint8_t* img = reinterpret_cast<const uint8_t*>(st.tok_bf16);
+      const uint8_t* img = reinterpret_cast<const uint8_t*>(st.tok_img);
       for (int i = 0; i < ntiles; ++i) {
         const int s = i % kStages;
         mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
@@ -201,28 +205,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
       }
     }
   } else if (warp == kMmaWarp) {
-    // ---- MMA issuer: 2 k-steps x 3 terms per tile ----
+    // ---- MMA issuer: 2 k-steps per tile ----
     if (lane == 0) {
-      const uint32_t id = idesc_bf16(128, kNT);
-      const uint32_t a_hi = smem_u32(As), a_lo = a_hi + kAHalf;
+      const uint32_t id = idesc_f16(128, kNT);
+      const uint32_t a0 = smem_u32(As);
       for (int i = 0; i < ntiles; ++i) {
         const int s = i % kStages, b = i % kAcc;
         mbar_wait(&full[s], (i / kStages) & 1);
         mbar_wait(&tempty[b], ((i / kAcc) & 1) ^ 1);
         fence_after();
         if (i < 32) SCAN_STAMP(40 + i);
-        const uint32_t b_hi = smem_u32(Bs + s * kBTile), b_lo = b_hi + 4 * kNT * 16;
+        const uint32_t b0 = smem_u32(Bs + s * kBTile);
         const uint32_t d = T + b * kNT;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const uint64_t ah = sdesc(a_hi + 2 * j * kASlab, kASlab, 128);
-          const uint64_t al = sdesc(a_lo + 2 * j * kASlab, kASlab, 128);
-          const uint64_t bh = sdesc(b_hi + 2 * j * kNT * 16, kNT * 16, 128);
-          const uint64_t bl = sdesc(b_lo + 2 * j * kNT * 16, kNT * 16, 128);
-          mma_bf16_ss(d, ah, bh, id, j > 0);
-          mma_bf16_ss(d, ah, bl, id, 1);
-          mma_bf16_ss(d, al, bh, id, 1);
-        }
+        for (int j = 0; j < 2; ++j)
+          mma_bf16_ss(d, sdesc(a0 + 2 * j * kASlab, kASlab, 128), sdesc(b0 + 2 * j * kNT * 16, kNT * 16, 128), id,
+                      j > 0);
         commit(&empty[s]);
         commit(&tfull[b]);
       }
@@ -247,7 +245,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
     const uint32_t lane_base = T + ((uint32_t)((warp & 3) * 32) << 16) + 64 * cq;
     for (int i = 0; i < ntiles; ++i) {
       const int b = i % kAcc;
-      mbar_wait(&tfull[b], (i / kAcc) & 1);
+      mbar_wait_sleep(&tfull[b], (i / kAcc) & 1);
       fence_after();
       if (tid == 0 && i < 32) SCAN_STAMP(72 + i);
       {
@@ -392,7 +390,7 @@ cudaError_t set_debug_timeline(long long* dev, int block) {
 cudaError_t launch_nn_scan(const Staged& st, const NNCfg& nn, const NNScan& sc, int pass,
                            cudaStream_t s) {
   if (st.n_work == 0) return cudaSuccess;
-  const size_t smem = 2 * kAHalf + (size_t)kStages * kBTile;
+  const size_t smem = kATile + (size_t)kStages * kBTile;
   cudaError_t e = cudaFuncSetAttribute(nn_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_pdl(nn_scan_kernel, dim3(st.n_work), dim3(kTcThreads), smem, s, st, nn, sc, pass);

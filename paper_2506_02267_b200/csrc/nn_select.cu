@@ -9,60 +9,28 @@
 // One warp per (candidate, source):
 //   1. a source with n <= k tokens selects all of them (no scan ran);
 //   2. otherwise every survivor of the scan's gate (nn_scan.cu) gets its
-//      exact key (reference f64 score | inverted index; lanes score
-//      survivors in parallel, two token rows in flight per lane) and the
-//      keys are sorted descending: the first k win.  n <= 256 (the normal
-//      case: about k + a few survivors) sorts in registers with a shuffle
-//      bitonic network (NP/32 keys per lane); larger n -- degenerate sources
-//      with massive ties, e.g. a zero candidate -- uses a shared-memory radix
-//      select (keys cached up to kSelCap, recomputed per pass beyond);
-//   3. the winners are re-keyed (index | f32 score) and sorted by descending
-//      storage index the same way.
+//      exact key (reference f64 score | inverted index); n <= 256 (the normal
+//      case: about k + a few dozen survivors): the survivors' token rows are
+//      staged in shared memory by cp.async (one memory round trip), scored by
+//      the lanes in parallel, and every key ranked against all others (a
+//      rolled broadcast loop); the k best win.  Larger n -- degenerate
+//      sources with massive ties, e.g. a zero candidate -- uses a radix select
+//      (keys recomputed per pass);
+//   3. the winners are marked in a bitmap over source positions and emitted
+//      in descending storage index (radix path: a shared bitonic sort).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "dbg.cuh"
 #include "tav2_common.cuh"
+#include "tc_common.cuh"
 
 namespace tav2 {
 
-constexpr int kSelWarps = 4;
-constexpr int kSelCap = 1024;  // shared-memory key cache per warp (8 KB)
-
-// Bitonic sort, descending, of NP keys held as v[j] = element j*32 + lane.
-template <int NP>
-__device__ __forceinline__ void warp_sort_desc(uint64_t* v, int lane) {
-  constexpr int R = NP / 32;
-#pragma unroll
-  for (int size = 2; size <= NP; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      if (stride >= 32) {  // partner in the same lane: register j ^ (stride / 32)
-        const int rs = stride / 32;
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-          if (j & rs) continue;
-          const int e = j * 32 + lane;
-          const bool desc = (e & size) == 0;
-          const uint64_t a = v[j], b = v[j | rs];
-          const bool sw = desc ? a < b : a > b;
-          v[j] = sw ? b : a;
-          v[j | rs] = sw ? a : b;
-        }
-      } else {  // partner lane ^ stride, same register
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-          const int e = j * 32 + lane;
-          const uint64_t o = __shfl_xor_sync(0xffffffffu, v[j], stride);
-          const bool desc = (e & size) == 0;
-          const bool lower = (lane & stride) == 0;  // element e < partner
-          const bool take_max = desc == lower;
-          v[j] = take_max ? (v[j] > o ? v[j] : o) : (v[j] < o ? v[j] : o);
-        }
-      }
-    }
-  }
-}
+constexpr int kSelWarps = 2;
+constexpr int kSelCap = 256;    // shared-memory key array per warp (2 KB)
+constexpr int kSelCache = 256;  // survivors sorted in registers
+constexpr int kCaps0 = 16384;   // LIFELONG_CAP (core.py:31): source positions per bitmap
 
 // (index + 1 | f32 score): sorts by storage index, never 0 (0 pads)
 __device__ __forceinline__ uint64_t winner_key(uint64_t key) {
@@ -71,14 +39,14 @@ __device__ __forceinline__ uint64_t winner_key(uint64_t key) {
 
 // reference score: f64 dot of the f32 unit vectors (nnsearch.py:344-347);
 // four independent chains in a fixed order, so equal rows score equal
-__device__ __forceinline__ double dot_exact(const float4* r, const double* uc) {
+__device__ __forceinline__ double dot_exact(const float4* r, const float* uc) {
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
   for (int q4 = 0; q4 < 8; ++q4) {
-    a0 = fma((double)r[q4].x, uc[4 * q4], a0);
-    a1 = fma((double)r[q4].y, uc[4 * q4 + 1], a1);
-    a2 = fma((double)r[q4].z, uc[4 * q4 + 2], a2);
-    a3 = fma((double)r[q4].w, uc[4 * q4 + 3], a3);
+    a0 = fma((double)r[q4].x, (double)uc[4 * q4], a0);
+    a1 = fma((double)r[q4].y, (double)uc[4 * q4 + 1], a1);
+    a2 = fma((double)r[q4].z, (double)uc[4 * q4 + 2], a2);
+    a3 = fma((double)r[q4].w, (double)uc[4 * q4 + 3], a3);
   }
   return (a0 + a1) + (a2 + a3);
 }
@@ -86,7 +54,7 @@ __device__ __forceinline__ double dot_exact(const float4* r, const double* uc) {
 struct KeySrc {  // survivors of one (candidate, source)
   const uint16_t* surv;
   const float* tok;  // the source's f32 unit rows
-  double uc[kEmbed];
+  float uc[kEmbed];
   __device__ __forceinline__ uint64_t key(int i) const {
     const int t = surv[i];
     float4 r[8];
@@ -96,44 +64,105 @@ struct KeySrc {  // survivors of one (candidate, source)
   }
 };
 
-// Register path: n <= NP survivors; writes the k winners sorted by index.
-template <int NP>
-__device__ __forceinline__ void select_regs(const KeySrc& ks, int n, int k, int lane, int32_t* orow,
-                                            float* srow) {
-  constexpr int R = NP / 32;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Keys of n <= kSelCache survivors into a[]: the warp stages kRowBatch token
+// rows at a time in shared memory with cp.async (8 lanes x 16 B per row, all
+// copies in flight at once; 16-byte chunk c of row r stored at chunk
+// c ^ (r & 7) so the per-lane row reads below are bank-conflict free), then
+// every lane scores its rows exactly.
+constexpr int kRowBatch = 128;
+__device__ __forceinline__ void keys_staged(const KeySrc& ks, int n, int lane, float4* rows, uint64_t* a) {
+  for (int b0 = 0; b0 < n; b0 += kRowBatch) {
+    const int nb = min(kRowBatch, n - b0);
+    for (int rr = lane >> 3; rr < nb; rr += 4) {
+      const int t = ks.surv[b0 + rr];
+      const int c = lane & 7;
+      cp_async16(rows + rr * 8 + (c ^ (rr & 7)), ks.tok + (size_t)t * kEmbed + 4 * c);
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    for (int rr = lane; rr < nb; rr += 32) {
+      float4 r[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) r[c] = rows[rr * 8 + (c ^ (rr & 7))];
+      a[b0 + rr] = score_key(dot_exact(r, ks.uc), ks.surv[b0 + rr]);
+    }
+    __syncwarp();
+  }
+}
+
+// Emit the winners marked in a per-warp bitmap over source positions in
+// descending storage index (the segment order, nnsearch.py:364): lane l
+// scans words [W - per(l+1), W - per l), high first; a warp prefix sum of the
+// per-lane counts places its bits.
+__device__ __forceinline__ void emit_bitmap(const uint32_t* bm, int words, int k, int lane, int32_t* orow,
+                                            float* srow, const KeySrc& ks) {
+  const int per = (words + 31) / 32;
+  const int w_hi = words - per * lane;  // this lane's words: [w_hi - per, w_hi)
+  int cnt = 0;
+  for (int w = w_hi - 1; w >= max(w_hi - per, 0); --w) cnt += __popc(bm[w]);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  int pos = incl - cnt;
+  for (int w = w_hi - 1; w >= max(w_hi - per, 0); --w) {
+    uint32_t m = bm[w];
+    while (m) {
+      const int b = 31 - __clz(m);
+      m &= ~(1u << b);
+      const int t = 32 * w + b;
+      if (pos < k) {
+        orow[pos] = t;
+        if (srow) {
+          float4 r[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) r[q] = __ldg(reinterpret_cast<const float4*>(ks.tok + (size_t)t * kEmbed) + q);
+          srow[pos] = (float)dot_exact(r, ks.uc);
+        }
+      }
+      ++pos;
+    }
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  for (int j = total + lane; j < k; j += 32) {
+    orow[j] = -1;
+    if (srow) srow[j] = 0.0f;
+  }
+}
+
+// The k largest of n <= 32 R keys a[0..n) (shared) win: lane-owned key
+// i = j*32 + lane has rank #{m : a[m] > key} (keys are unique), counted with a
+// rolled loop of broadcast reads -- compact code (a fully unrolled sorting
+// network runs once per SM and is bound by instruction fetch).
+template <int R>
+__device__ __forceinline__ void select_rank(const uint64_t* a, int n, int k, int lane, uint32_t* bm) {
   uint64_t v[R];
-  int t[R];
+  int rank[R];
 #pragma unroll
   for (int j = 0; j < R; ++j) {
-    const int i = j * 32 + lane;
-    t[j] = i < n ? (int)ks.surv[i] : -1;
+    v[j] = j * 32 + lane < n ? a[j * 32 + lane] : 0ull;
+    rank[j] = 0;
+  }
+#pragma unroll 4
+  for (int m = 0; m < n; ++m) {
+    const uint64_t x = a[m];
+#pragma unroll
+    for (int j = 0; j < R; ++j) rank[j] += x > v[j] ? 1 : 0;
   }
 #pragma unroll
-  for (int j = 0; j < R; j += 2) {  // two rows in flight per lane
-    float4 r0[8], r1[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      r0[q] = t[j] >= 0 ? __ldg(reinterpret_cast<const float4*>(ks.tok + (size_t)t[j] * kEmbed) + q)
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (j + 1 < R)
-        r1[q] = t[j + 1] >= 0 ? __ldg(reinterpret_cast<const float4*>(ks.tok + (size_t)t[j + 1] * kEmbed) + q)
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int j = 0; j < R; ++j)
+    if (j * 32 + lane < n && rank[j] < k) {
+      const int t = key_index(v[j]);
+      atomicOr(bm + (t >> 5), 1u << (t & 31));
     }
-    v[j] = t[j] >= 0 ? score_key(dot_exact(r0, ks.uc), t[j]) : 0ull;  // real keys are > 0
-    if (j + 1 < R) v[j + 1] = t[j + 1] >= 0 ? score_key(dot_exact(r1, ks.uc), t[j + 1]) : 0ull;
-  }
-  warp_sort_desc<NP>(v, lane);
-#pragma unroll
-  for (int j = 0; j < R; ++j) v[j] = (j * 32 + lane < k && v[j]) ? winner_key(v[j]) : 0ull;
-  warp_sort_desc<NP>(v, lane);
-#pragma unroll
-  for (int j = 0; j < R; ++j) {
-    const int i = j * 32 + lane;
-    if (i < k) {
-      orow[i] = v[j] ? (int32_t)(v[j] >> 32) - 1 : -1;
-      if (srow) srow[i] = v[j] ? __uint_as_float((uint32_t)v[j]) : 0.0f;
-    }
-  }
+  __syncwarp();
 }
 
 __device__ __forceinline__ void warp_bitonic_desc_smem(uint64_t* a, int n, int lane) {
@@ -154,7 +183,7 @@ __device__ __forceinline__ void warp_bitonic_desc_smem(uint64_t* a, int n, int l
   }
 }
 
-// Shared-memory path for n > 256: MSB-first radix select (8-bit digits,
+// Path for n > kSelCache: MSB-first radix select (8-bit digits,
 // warp-aggregated histogram) isolates the top k, then a shared bitonic sort
 // orders the winners by index.
 __device__ __forceinline__ void select_radix(const KeySrc& ks, int n, int k, int lane, uint64_t* a,
@@ -252,8 +281,11 @@ __global__ void __launch_bounds__(32 * kSelWarps) nn_select_kernel(Staged st, NN
 
 __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn, const NNScan& sc,
                                                int32_t* idx, float* scores) {
-  __shared__ uint64_t buf[kSelWarps][kSelCap];
+  __shared__ uint64_t buf[kSelWarps][kSelCap];  // radix path key cache; also the sort array
   __shared__ unsigned hist_s[kSelWarps][256];
+  __shared__ float4 rows_s[kSelWarps][kRowBatch * 8];  // staged token rows (16 KB per warp)
+  __shared__ uint32_t bm_s[kSelWarps][kCaps0 / 32];      // winner bitmap over source positions
+  uint64_t (&keys_s)[kSelWarps][kSelCap] = buf;
   cta_stamp(kDbgSelect, 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * kSelWarps + warp;
@@ -307,12 +339,22 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
     }
   }
   const int n = min((int)sc.count[(size_t)item * 3 + s], hi - lo);
-  const int np = max(n, k);
-  if (np <= 32) select_regs<32>(ks, n, k, lane, orow, srow);
-  else if (np <= 64) select_regs<64>(ks, n, k, lane, orow, srow);
-  else if (np <= 128) select_regs<128>(ks, n, k, lane, orow, srow);
-  else if (np <= 256) select_regs<256>(ks, n, k, lane, orow, srow);
-  else select_radix(ks, n, k, lane, buf[warp], hist_s[warp], orow, srow);
+  const long long t_start = kDebug ? gtimer() : 0;
+  uint64_t* a = keys_s[warp];
+  if (max(n, k) <= kSelCache) {
+    uint32_t* bm = bm_s[warp];
+    const int words = (hi + 31) >> 5;
+    for (int w = lane; w < words; w += 32) bm[w] = 0u;
+    keys_staged(ks, n, lane, rows_s[warp], a);
+    const int np = max(n, k);
+    if (np <= 64) select_rank<2>(a, n, k, lane, bm);
+    else if (np <= 128) select_rank<4>(a, n, k, lane, bm);
+    else select_rank<8>(a, n, k, lane, bm);
+    emit_bitmap(bm, words, k, lane, orow, srow, ks);
+  } else {
+    select_radix(ks, n, k, lane, buf[warp], hist_s[warp], orow, srow);
+  }
+  if (kDebug && lane == 0) sel_record(item * 3 + s, gtimer() - t_start, n);
 }
 
 cudaError_t set_dbg_cta_select(long long* dev) { return set_dbg_cta_tu(dev); }

@@ -3,6 +3,7 @@
 // Reference: nnsearch.py:274-286 (_unit_rows_into), :313-320 (candidate
 // normalisation); core.py:54-79 (dequantize / l2_normalize_rows /
 // unit_embeddings).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -54,18 +55,20 @@ __global__ void __launch_bounds__(256) prep_kernel(Staged st) {
     float4* dst = reinterpret_cast<float4*>(st.tok_unit + (size_t)i * kEmbed);
 #pragma unroll
     for (int j = 0; j < kEmbed; j += 4) dst[j / 4] = make_float4(u[j], u[j + 1], u[j + 2], u[j + 3]);
-    // bf16 hi/lo image of the unit row, pre-tiled for the tensor-core NN
-    // scan (kScanTile-token tiles, UMMA K-major no-swizzle B-operand layout,
+    // fp16 image of the unit row, pre-tiled for the tensor-core NN scan
+    // (kScanTile-token tiles, UMMA K-major no-swizzle B-operand layout,
     // tav2_common.cuh), one bulk copy per tile
-    uint8_t* tile = reinterpret_cast<uint8_t*>(st.tok_bf16) + (size_t)(i / kScanTile) * kScanTileBytes +
+    uint8_t* tile = reinterpret_cast<uint8_t*>(st.tok_img) + (size_t)(i / kScanTile) * kScanTileBytes +
                     (i % kScanTile) * 16;
 #pragma unroll
     for (int j = 0; j < kEmbed; j += 8) {
-      uint32_t hi[4], lo[4];
+      uint32_t h[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) tc::split_pair(u[j + 2 * e], u[j + 2 * e + 1], hi[e], lo[e]);
-      *reinterpret_cast<uint4*>(tile + (j / 8) * (kScanTile * 16)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<uint4*>(tile + (4 + j / 8) * (kScanTile * 16)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      for (int e = 0; e < 4; ++e) {
+        const __half2 p = __floats2half2_rn(u[j + 2 * e], u[j + 2 * e + 1]);
+        h[e] = *reinterpret_cast<const uint32_t*>(&p);
+      }
+      *reinterpret_cast<uint4*>(tile + (j / 8) * (kScanTile * 16)) = make_uint4(h[0], h[1], h[2], h[3]);
     }
     return;
   }

@@ -4,6 +4,7 @@
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <string.h>
@@ -47,6 +48,14 @@ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 
 }  // namespace
 
+bool tav2::pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TAV2_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 struct tav2_ctx {
   tav2_config cfg;
   tav2_capacity cap;
@@ -63,7 +72,7 @@ struct tav2_ctx {
   cudaEvent_t ev_staged = nullptr;
   // derived device buffers
   float* tok_unit = nullptr;
-  uint32_t* tok_bf16 = nullptr;
+  uint32_t* tok_img = nullptr;
   float* cand_unit = nullptr;
   NNScan scan{};               // threshold-scan NN buffers (nn_scan.cu)
 
@@ -109,7 +118,7 @@ Staged staged_view(tav2_ctx* c) {
   s.surface = reinterpret_cast<const uint8_t*>(b + p.off_surface);
   s.emb = reinterpret_cast<const int8_t*>(b + p.off_emb);
   s.tok_unit = c->tok_unit;
-  s.tok_bf16 = c->tok_bf16;
+  s.tok_img = c->tok_img;
   s.cand_unit = c->cand_unit;
   s.n_req = p.n_req;
   s.n_items = p.n_items;
@@ -137,7 +146,7 @@ int free_all(tav2_ctx* c) {
   cudaFreeHost(c->h_arena);
   cudaFree(c->d_staged);
   cudaFree(c->tok_unit);
-  cudaFree(c->tok_bf16);
+  cudaFree(c->tok_img);
   cudaFree(c->cand_unit);
   cudaFree(c->scan.gmax);
   cudaFree(c->scan.bound);
@@ -259,9 +268,9 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
   if ((e = cudaMalloc(&c->tok_unit, (size_t)(cdiv((int)std::max<int64_t>(T, 1), 64) + 1) * 64 * kEmbed * 4)) !=
       cudaSuccess)
     return bad(e, "tok_unit");
-  if ((e = cudaMalloc(&c->tok_bf16, (size_t)(cdiv((int)std::max<int64_t>(T, 1), kScanTile) + 1) * kScanTileBytes)) !=
+  if ((e = cudaMalloc(&c->tok_img, (size_t)(cdiv((int)std::max<int64_t>(T, 1), kScanTile) + 1) * kScanTileBytes)) !=
       cudaSuccess)
-    return bad(e, "tok_bf16");
+    return bad(e, "token image");
   if ((e = cudaMalloc(&c->cand_unit, (size_t)N * kEmbed * 4)) != cudaSuccess) return bad(e, "cand_unit");
   // scan buffers: a source has at most max(8k + 2, 16384/32 + 2) groups
   // (planner), a (candidate, source) at most its source length of survivors

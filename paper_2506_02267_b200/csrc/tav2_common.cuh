@@ -35,13 +35,15 @@ struct ReqInfo {          // one unique request (DedupBatch.users entry)
   int32_t pad_;
 };
 
-// Approximate-score gate margin of the threshold scan: > the bf16x3 score
-// error bound 2.3e-5 for unit vectors (nn_scan.cu).
-constexpr float kGateEps = 4e-5f;
-// The scan's token operand: 128-token tiles of the bf16 hi/lo unit rows in the
-// UMMA K-major no-swizzle layout, [8 chunks (hi 0-3, lo 4-7)][128 rows][16 B].
+// Approximate-score gate margin of the threshold scan (nn_scan.cu): the
+// scan scores fp16(unit(q)) . fp16(unit(c)) with f32 accumulation; fp16
+// round-to-nearest has unit roundoff u = 2^-11, so for unit vectors
+// |approx - exact| <= 2u + u^2 + 32 * 2^-24 (accumulation) < 9.8e-4.
+constexpr float kGateEps = 1.1e-3f;
+// The scan's token operand: 256-token tiles of the fp16 unit rows in the UMMA
+// K-major no-swizzle layout, [4 chunks of 8 elements][256 rows][16 B].
 constexpr int kScanTile = 256;
-constexpr int kScanTileBytes = 8 * kScanTile * 16;
+constexpr int kScanTileBytes = 4 * kScanTile * 16;
 
 struct NNWork {           // one (candidate tile, source, token chunk) unit
   int32_t tile;           // candidate tile id
@@ -129,7 +131,7 @@ struct Staged {
   const uint8_t* surface;  // [T]
   const int8_t* emb;       // [T, 32]
   float* tok_unit;         // [T, 32] derived: unit(dequantize(q)) (core.py:77-79)
-  uint32_t* tok_bf16;      // derived: unit rows as bf16 hi/lo, 64-token tiles of 8 KB (prep_kernel)
+  uint32_t* tok_img;       // derived: fp16 unit rows, kScanTile-token tiles (prep_kernel)
   float* cand_unit;        // [N, 32] derived: l2_normalize_rows(cand)
   int n_req, n_items, n_tok, n_tiles, n_work;
 };
@@ -177,6 +179,8 @@ namespace tav2 {
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+bool pdl_enabled();  // TAV2_NO_PDL=1 disables programmatic dependent launch (A/B timing)
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args&&... args) {
@@ -189,7 +193,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 }  // namespace tav2

@@ -35,12 +35,18 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 
 // ---- instruction descriptors ----
 // kind::f16 with bf16 A/B, f32 accumulate.  a_mn/b_mn: 1 = MN-major operand.
+// (mma_bf16_ss/_ts below issue kind::f16; the instruction descriptor picks
+// bf16 or fp16 operands.)
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn = 0, int b_mn = 0) {
   return (1u << 4)            // D format f32
          | (1u << 7)          // A bf16
          | (1u << 10)         // B bf16
          | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// kind::f16 with fp16 A/B, f32 accumulate (K-major operands).
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 // kind::i8 with signed int8 A/B, s32 accumulate.
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
