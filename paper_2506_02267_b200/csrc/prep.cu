@@ -15,8 +15,9 @@ namespace tav2 {
 
 // ---------------------------------------------------------------------------
 // K1: per token  unit(dequantize(q)) in f32 with the reference's rounding
-// steps (core.py:54-57 then :69-74) plus its bf16 hi/lo tile image for the
-// tensor-core scan; per candidate  l2_normalize_rows (nnsearch.py:313-320).
+// steps (core.py:54-57 then :69-74), its fp16 tile image for the tensor-core
+// scan and (with parameters) its Eq. 4 feature part for the SKUT gather; per
+// candidate  l2_normalize_rows (nnsearch.py:313-320).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float sumsq8(const float* v) {
   // 8 interleaved accumulators, adjacent-pair combine (a fixed order; the
@@ -31,7 +32,7 @@ __device__ __forceinline__ float sumsq8(const float* v) {
   return __fadd_rn(__fadd_rn(b0, b1), __fadd_rn(b2, b3));
 }
 
-__global__ void __launch_bounds__(256) prep_kernel(Staged st) {
+__global__ void __launch_bounds__(256) prep_kernel(Staged st, Params p, int with_feat) {
   cta_stamp(kDbgPrep, 0);
   griddep_launch();
   griddep_wait();  // the previous step's kernels may still read tok_unit / cand_unit
@@ -70,6 +71,36 @@ __global__ void __launch_bounds__(256) prep_kernel(Staged st) {
       }
       *reinterpret_cast<uint4*>(tile + (j / 8) * (kScanTile * 16)) = make_uint4(h[0], h[1], h[2], h[3]);
     }
+    if (with_feat) {  // token part of Eq. 4 (encoder.py:171-187): [unit(q) | 0] + bits @ action + surface
+      float f[kDModel];
+#pragma unroll
+      for (int j = 0; j < kEmbed; ++j) {
+        f[j] = u[j];
+        f[kEmbed + j] = 0.0f;
+      }
+      const unsigned act = st.action[i];
+      float asum[kDModel];
+#pragma unroll
+      for (int j = 0; j < kDModel; ++j) asum[j] = 0.0f;
+      for (int b = 0; b < p.action_rows; ++b)
+        if ((act >> b) & 1u) {
+          const float4* row = reinterpret_cast<const float4*>(p.action_table + b * kDModel);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float4 v = __ldg(row + j);
+            asum[4 * j] += v.x; asum[4 * j + 1] += v.y; asum[4 * j + 2] += v.z; asum[4 * j + 3] += v.w;
+          }
+        }
+      const int surf = min((int)st.surface[i], 3);  // SURFACE_OTHER fold (encoder.py:178)
+      const float4* srow = reinterpret_cast<const float4*>(p.surface_table + surf * kDModel);
+      float4* fd = reinterpret_cast<float4*>(st.tok_feat + (size_t)i * kDModel);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float4 sv = __ldg(srow + j);
+        fd[j] = make_float4((f[4 * j] + asum[4 * j]) + sv.x, (f[4 * j + 1] + asum[4 * j + 1]) + sv.y,
+                            (f[4 * j + 2] + asum[4 * j + 2]) + sv.z, (f[4 * j + 3] + asum[4 * j + 3]) + sv.w);
+      }
+    }
     return;
   }
   i -= st.n_tok;
@@ -93,10 +124,11 @@ __global__ void __launch_bounds__(256) prep_kernel(Staged st) {
 
 cudaError_t set_dbg_cta_prep(long long* dev) { return set_dbg_cta_tu(dev); }
 
-cudaError_t launch_prep(const Staged& st, cudaStream_t s) {
+cudaError_t launch_prep(const Staged& st, const Params* p, cudaStream_t s) {
   int n = st.n_tok + st.n_items;
   if (n == 0) return cudaSuccess;
-  return launch_pdl(prep_kernel, dim3((n + 255) / 256), dim3(256), 0, s, st);
+  const Params pz{};
+  return launch_pdl(prep_kernel, dim3((n + 255) / 256), dim3(256), 0, s, st, p ? *p : pz, (int)(p != nullptr));
 }
 
 }  // namespace tav2

@@ -126,7 +126,7 @@ __device__ __forceinline__ void mma3_kmajor(uint32_t d, uint32_t a_col, uint32_t
 
 // allowed keys k0..k0+15 for query row r: key-valid bits (low 16 of `bits`)
 // AND causal (key <= r)
-__device__ __forceinline__ uint32_t allowed16(uint32_t bits, int k0, int r) {
+static __device__ __forceinline__ uint32_t allowed16(uint32_t bits, int k0, int r) {
   const int n = r - k0 + 1;  // keys k0..r are causal-visible
   const uint32_t causal = n >= 16 ? 0xffffu : (n <= 0 ? 0u : ((1u << n) - 1u));
   return bits & causal;

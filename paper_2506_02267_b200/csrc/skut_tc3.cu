@@ -1,0 +1,544 @@
+// SKUT v3 on the 5th-gen tensor cores (S <= 192, <= 2 layers): gather +
+// Eq. 4 encode, 2 x pre-norm causal transformer layers, linear + masked
+// max-pool and the CTR head, one candidate per CTA iteration (persistent).
+//
+// Reference: encoder.py:161-188 (encode_batch), :196-211 (layer_norm,
+// masked_softmax), :221-246 / :314-462 (forward_reference / forward_fused),
+// trainer.py:354-366 (pool + head).
+//
+// Versus the reference's layer (encoder.py:229-246) the kernel uses two
+// exact algebraic re-associations, folded into the bf16x3 weight images at
+// load time (tav2_load_params, f64 products):
+//   scores  (a Wq)(a Wk)^T / 8 = (a Wqk) a^T,  Wqk = Wq Wk^T log2(e) / 8
+//           -> K is the LN1 output itself and the scores land in the exp2
+//              domain of the softmax;
+//   output  (P (a Wv)) Wo = P (a Wvo),  Wvo = Wv Wo
+//           -> no separate Wo GEMM: x += (P V') / l.
+// Per layer this is five MMA <-> SIMT round trips (tc2: six) and ~20% fewer
+// tcgen05.mma instructions.  Numerics ("bf16 mode"): every GEMM is a 3-term
+// split-bf16 product (a_hi b_hi + a_hi b_lo + a_lo b_hi, f32 accumulation
+// in TMEM); residual stream, LN, softmax statistics and the head are f32.
+//
+// Layout: thread = sequence row (the tc2 balanced row-block mapping: warp
+// (t, q) owns rows rpw*kb .. where kb = q (tile 0) or 7 - q (tile 1), so each
+// SM sub-partition carries one early and one late block).  Two independent
+// tiles (warps 4t..4t+3), each with its own TMEM half (256 columns), its own
+// simt/mma barriers and issuer (thread 128t); they couple only through the
+// K/V operands (kvready / kvfree).  All weight images stay resident in
+// shared memory for the CTA's lifetime (loaded once); the token features of
+// the gather come precomputed from prep_kernel (tok_feat).
+//
+// TMEM per tile (base 256t): D region [0, 192): QV' out [0,128) / S,P [0,NK)
+// / H = W1 out [0,32) / ReLU A2 [32,64) / W2 out [64,128) / pool out [0,64);
+// A region [192, 256): LN1 out / Q' / O' (PV out) / LN2 out / x (pool).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "dbg.cuh"
+#include "encode.cuh"
+#include "tav2_common.cuh"
+#include "tc_common.cuh"
+
+namespace tav2 {
+
+using namespace tc;
+
+constexpr int kT3Warps = 8;
+constexpr int kT3Threads = 32 * kT3Warps;
+constexpr float kLnEps3 = 1e-5f;
+constexpr uint32_t kCA = 192, kCD = 0, kCA2 = 32, kCW2 = 64;
+
+// weight image offsets inside the shared-memory weight region
+constexpr int kW3Layer = kImg3WA + kImg3WB;  // 48 KB per layer
+
+struct T3Bars {
+  uint64_t simt[2], mma[2], kvready, kvfree, wfull;
+};
+__shared__ __align__(8) T3Bars t3;
+
+// allowed keys k0..k0+15 for query row r: key-valid bits (low 16 of `bits`)
+// AND causal (key <= r)
+static __device__ __forceinline__ uint32_t allowed16(uint32_t bits, int k0, int r) {
+  const int n = r - k0 + 1;  // keys k0..r are causal-visible
+  const uint32_t causal = n >= 16 ? 0xffffu : (n <= 0 ? 0u : ((1u << n) - 1u));
+  return bits & causal;
+}
+
+__device__ __forceinline__ void t3_ld64(uint32_t ta, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  tmem_ld32(ta, r);
+  tmem_ld32(ta + 32, r + 32);
+  tmem_ld_wait();
+}
+// split n floats into packed bf16 hi/lo pairs: hi at [0, n/2), lo at [n/2, n)
+template <int N>
+__device__ __forceinline__ void t3_st_split(uint32_t ta, const float* v) {
+#pragma unroll
+  for (int c = 0; c < N / 16; ++c) {
+    uint32_t hi[8], lo[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) split_pair(v[16 * c + 2 * i], v[16 * c + 2 * i + 1], hi[i], lo[i]);
+    tmem_st8(ta + 8 * c, hi);
+    tmem_st8(ta + N / 2 + 8 * c, lo);
+  }
+}
+__device__ __forceinline__ void t3_split8_store(uint8_t* hi_dst, uint8_t* lo_dst, const float* v) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) split_pair(v[2 * i], v[2 * i + 1], h[i], l[i]);
+  *reinterpret_cast<uint4*>(hi_dst) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(lo_dst) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+// pre-norm LayerNorm (encoder.py:196-200, biased variance, eps 1e-5)
+__device__ __forceinline__ void t3_layer_norm(const float* x, const float* g, const float* b, float* y) {
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int j = 0; j < kDModel; j += 2) {
+    s0 += x[j];
+    s1 += x[j + 1];
+  }
+  const float mu = (s0 + s1) * (1.0f / 64.0f);
+  float v0 = 0.f, v1 = 0.f;
+#pragma unroll
+  for (int j = 0; j < kDModel; j += 2) {
+    const float c0 = x[j] - mu, c1 = x[j + 1] - mu;
+    v0 = fmaf(c0, c0, v0);
+    v1 = fmaf(c1, c1, v1);
+  }
+  const float rs = rsqrtf((v0 + v1) * (1.0f / 64.0f) + kLnEps3);
+#pragma unroll
+  for (int j = 0; j < kDModel; ++j) y[j] = fmaf((x[j] - mu) * rs, g[j], b[j]);
+}
+
+// D += A(TMEM hi/lo) x B(smem hi/lo, K-major slabs), 3 terms per k-step
+__device__ __forceinline__ void t3_mma3(uint32_t d, uint32_t a_col, uint32_t a_lo_off, uint32_t b_hi,
+                                        uint32_t b_lo, uint32_t lbo, int ksteps, uint32_t idesc) {
+  for (int j = 0; j < ksteps; ++j) {
+    const uint64_t bh = sdesc(b_hi + 2 * j * lbo, lbo, 128);
+    const uint64_t bl = sdesc(b_lo + 2 * j * lbo, lbo, 128);
+    mma_bf16_ts(d, a_col + 8 * j, bh, idesc, j > 0);
+    mma_bf16_ts(d, a_col + 8 * j, bl, idesc, 1);
+    mma_bf16_ts(d, a_col + a_lo_off + 8 * j, bh, idesc, 1);
+  }
+}
+
+__global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
+    Params p, SkutImages3 img, NNCfg nn, Staged st, const int32_t* idx, int n, float* logits,
+    float* pooled_out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  cta_stamp(kDbgSkut, 0);
+  __shared__ uint32_t taddr_s;
+  __shared__ uint32_t valid_w[8];  // key-validity bitmask, bit r of word r/32
+  __shared__ __align__(16) float lnp_s[2][4][kDModel];
+  __shared__ float red_s[kT3Warps][kDModel];
+  __shared__ float z_s[kDModel + kEmbed + kCtx];
+  __shared__ float hpart_s[4][kHidden];
+  __shared__ float hid_s[kHidden];
+  __shared__ int any_s;
+  __shared__ unsigned kmax_s[2];
+
+  const int S = nn.seq_len;
+  const int S_pad = (S + 15) & ~15;
+  const int NL = p.num_layers;
+  const int wbytes = NL * kW3Layer + kImg3WO;
+  uint8_t* Wsm = sm;
+  uint8_t* Khi = sm + wbytes;
+  uint8_t* Klo = Khi + S_pad * 128;
+  uint8_t* Vhi = Klo + S_pad * 128;
+  uint8_t* Vlo = Vhi + S_pad * 128;
+  const uint32_t wsm = smem_u32(Wsm);
+  const uint32_t khi = smem_u32(Khi), klo = smem_u32(Klo), vhi = smem_u32(Vhi), vlo = smem_u32(Vlo);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int t = warp >> 2, q = warp & 3;
+  const int rpw = S_pad >> 3;
+  const int kb = t == 0 ? q : 7 - q;
+  const bool mapped = lane < rpw;
+  const int r = rpw * kb + lane;
+  const int NK0 = ((S_pad >> 1) + 15) & ~15;
+  const int NK = t == 0 ? NK0 : S_pad;  // keys this tile's rows can see
+  if (tid == 0) {
+    mbar_init(&t3.simt[0], 128);
+    mbar_init(&t3.simt[1], 128);
+    mbar_init(&t3.mma[0], 1);
+    mbar_init(&t3.mma[1], 1);
+    mbar_init(&t3.kvready, kT3Threads);
+    mbar_init(&t3.kvfree, 2);
+    mbar_init(&t3.wfull, 1);
+    mbar_fence_init();
+  }
+  if (warp == 0) tmem_alloc<512>(&taddr_s);
+  if (tid < 8) valid_w[tid] = 0u;
+  if (tid < 2) kmax_s[tid] = 0u;
+  for (int i = tid; i < NL * 4 * kDModel; i += kT3Threads) {
+    const int L = i / (4 * kDModel), w = (i / kDModel) % 4, j = i % kDModel;
+    const float* src = w == 0 ? p.ln1_scale[L] : w == 1 ? p.ln1_shift[L] : w == 2 ? p.ln2_scale[L] : p.ln2_shift[L];
+    lnp_s[L][w][j] = src[j];
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (taddr_s != 0u) __trap();  // a 512-column allocation always starts at column 0
+  if (tid == 0) {  // all weight images, once per CTA (input independent: before the PDL wait)
+    mbar_expect_tx(&t3.wfull, (uint32_t)wbytes);
+    for (int L = 0; L < NL; ++L) bulk_g2s(Wsm + L * kW3Layer, img.w[L], kW3Layer, &t3.wfull);
+    bulk_g2s(Wsm + NL * kW3Layer, img.wout, kImg3WO, &t3.wfull);
+  }
+
+  const bool issuer = (tid & 127) == 0;
+  const uint32_t R = 256u * t;
+  const uint32_t lanebase = ((uint32_t)(32 * q) << 16) + R;
+  const uint32_t cA = lanebase + kCA;
+  const bool in_seq = mapped && r < S;
+  uint32_t n_mma = 0, n_kv = 0;
+  uint32_t ph_simt = 0;
+  auto wait_mma = [&]() {
+    __syncwarp();
+    mbar_wait_sleep(&t3.mma[t], n_mma & 1);
+    ++n_mma;
+    fence_after();
+  };
+  auto done = [&]() {
+    fence_before();
+    mbar_arrive(&t3.simt[t]);
+  };
+  auto issuer_wait_simt = [&]() {
+    mbar_wait(&t3.simt[t], ph_simt);
+    ph_simt ^= 1u;
+    fence_after();
+  };
+  auto wa = [&](int L) { return wsm + L * kW3Layer; };
+  auto wb = [&](int L) { return wsm + L * kW3Layer + kImg3WA; };
+
+  griddep_launch();
+  griddep_wait();  // NN selection (idx) and prep (tok_feat, cand_unit) complete
+  cta_stamp(kDbgSkut, 2);
+  if (issuer) {
+    mbar_wait(&t3.wfull, 0);
+    fence_after();
+  }
+  const float4* pos4 = reinterpret_cast<const float4*>(p.position_table + (size_t)(in_seq ? r : 0) * kDModel);
+
+  for (int item = blockIdx.x; item < n; item += gridDim.x) {
+    // ---- K3: gather + encode: x = tok_feat[tok] + pos[r] + [0 | unit(c)] ----
+    float x[kDModel];
+    bool ok = false;
+    if (in_seq) {
+      const int tok = slot_token(st, nn, idx, item, r);
+      ok = tok >= 0;
+      if (ok) {
+        const float4* tf = reinterpret_cast<const float4*>(st.tok_feat + (size_t)tok * kDModel);
+        const float4* cu = reinterpret_cast<const float4*>(st.cand_unit + (size_t)item * kEmbed);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float4 a = tf[j], b = __ldg(pos4 + j);
+          const float4 c = j >= 8 ? cu[j - 8] : make_float4(0.f, 0.f, 0.f, 0.f);
+          x[4 * j] = (a.x + c.x) + b.x;
+          x[4 * j + 1] = (a.y + c.y) + b.y;
+          x[4 * j + 2] = (a.z + c.z) + b.z;
+          x[4 * j + 3] = (a.w + c.w) + b.w;
+        }
+      }
+    }
+    if (!ok) {
+#pragma unroll
+      for (int j = 0; j < kDModel; ++j) x[j] = 0.0f;
+    }
+    {
+      const unsigned b = __ballot_sync(0xffffffffu, ok);  // lanes >= rpw are never ok
+      if (lane == 0 && b) {
+        const int r0 = rpw * kb;
+        const unsigned long long w = (unsigned long long)b << (r0 & 31);
+        atomicOr(&valid_w[r0 >> 5], (uint32_t)w);
+        if ((uint32_t)(w >> 32)) atomicOr(&valid_w[(r0 >> 5) + 1], (uint32_t)(w >> 32));
+      }
+    }
+    named_bar_sync(1, kT3Threads);  // valid_w complete
+
+    for (int L = 0; L < NL; ++L) {
+      // ---- P1: a = LN1(x) -> A (TMEM) and K = a (smem); ||a||^2 -> kmax ----
+      if (n_kv > 0) mbar_wait_sleep(&t3.kvfree, (n_kv - 1) & 1);  // both tiles' previous P.V retired
+      {
+        float a[kDModel];
+        t3_layer_norm(x, lnp_s[L][0], lnp_s[L][1], a);
+        float an2 = 0.0f;
+        if (!ok) {
+#pragma unroll
+          for (int j = 0; j < kDModel; ++j) a[j] = 0.0f;
+        }
+#pragma unroll
+        for (int j = 0; j < kDModel; ++j) an2 = fmaf(a[j], a[j], an2);
+        t3_st_split<64>(cA, a);  // warp-collective: never under a divergent branch
+        if (mapped) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {  // K-major slabs: chunk c of row r at c*(S_pad*16) + r*16
+            const int off = c * (S_pad * 16) + r * 16;
+            t3_split8_store(Khi + off, Klo + off, a + 8 * c);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) an2 = fmaxf(an2, __shfl_xor_sync(0xffffffffu, an2, o));
+        if (lane == 0) atomicMax(&kmax_s[L], __float_as_uint(an2));
+        tmem_st_wait();
+        done();
+      }
+      if (issuer) {  // M1: [Q' | V'] = A [Wqk | Wvo]   (N = 128, K = 64)
+        issuer_wait_simt();
+        t3_mma3(R + kCD, R + kCA, 32, wa(L), wa(L) + kImg3WA / 2, 128 * 16, 4, idesc_bf16(128, 128));
+        commit(&t3.mma[t]);
+      }
+      // ---- P2: Q' -> A, V' -> smem (MN-major) ----
+      wait_mma();
+      float qn2 = 0.0f;
+      {
+        float v[32];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          tmem_ld32(lanebase + kCD + 32 * h, reinterpret_cast<uint32_t*>(v));
+          tmem_ld_wait();
+          if (!ok) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) qn2 = fmaf(v[i], v[i], qn2);
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint32_t hi[8], lo[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) split_pair(v[16 * c + 2 * i], v[16 * c + 2 * i + 1], hi[i], lo[i]);
+            tmem_st8(cA + 16 * h + 8 * c, hi);
+            tmem_st8(cA + 32 + 16 * h + 8 * c, lo);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // V': (key r, d) at (r/8)*1024 + (d/8)*128 + (r%8)*16 + (d%8)*2
+          tmem_ld32(lanebase + kCD + 64 + 32 * h, reinterpret_cast<uint32_t*>(v));
+          tmem_ld_wait();
+          if (mapped) {
+            if (!ok) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int off = (r >> 3) * 1024 + (4 * h + c) * 128 + (r & 7) * 16;
+              t3_split8_store(Vhi + off, Vlo + off, v + 8 * c);
+            }
+          }
+        }
+        tmem_st_wait();
+        fence_proxy_async();
+        fence_before();
+        mbar_arrive(&t3.kvready);  // this row's K, V' and Q' are in place
+      }
+      if (issuer) {  // M2: S = Q' K^T   (N = keys of this tile, K = 64)
+        mbar_wait(&t3.kvready, n_kv & 1);
+        fence_after();
+        t3_mma3(R + kCD, R + kCA, 32, khi, klo, S_pad * 16, 4, idesc_bf16(128, NK));
+        commit(&t3.mma[t]);
+      }
+      // ---- P3: causal key-masked softmax -> P (bf16 hi/lo, in place over S) ----
+      // Single pass with the Cauchy-Schwarz shift m' = ||q'_r|| max_j ||a_j||
+      // (>= q'_r . a_j, the exp2-domain score): shift invariance makes 1/l the
+      // exact normaliser of encoder.py:203-211.
+      wait_mma();
+      float inv_l = 0.0f;
+      {
+        mbar_wait_sleep(&t3.kvready, n_kv & 1);  // kmax_s[L] complete (already passed)
+        const float mb = sqrtf(qn2 * __uint_as_float(kmax_s[L]));
+        const uint32_t cs = lanebase + kCD;
+        const int nch = NK / 16;
+        const int jlast = min(nch - 1, (rpw * kb + rpw - 1) / 16);  // warp-uniform causal bound
+        float l = 0.0f;
+        for (int j0 = 0; j0 < nch; j0 += 2) {
+          uint32_t s32[32];
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            if (j0 + u <= jlast) tmem_ld16(cs + 16 * (j0 + u), s32 + 16 * u);  // warp-uniform
+          tmem_ld_wait();
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int j = j0 + u;
+            if (j >= nch) break;
+            uint32_t hi[8], lo[8];
+            uint32_t vm = 0u;
+            if (ok && j <= jlast) vm = allowed16(valid_w[j >> 1] >> ((j & 1) * 16), 16 * j, r);
+            float pv[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              float pe;
+              asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(pe) : "f"(__uint_as_float(s32[16 * u + e]) - mb));
+              pv[e] = ((vm >> e) & 1u) ? pe : 0.0f;
+              l += pv[e];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) split_pair(pv[2 * i], pv[2 * i + 1], hi[i], lo[i]);
+            tmem_st8(cs + 16 * j, hi);
+            tmem_st8(cs + 16 * j + 8, lo);
+          }
+        }
+        inv_l = l > 0.0f ? 1.0f / l : 0.0f;  // a valid row always sees itself
+        tmem_st_wait();
+        done();
+      }
+      if (issuer) {  // M3: O' = P V'   (N = 64, K = keys; V' MN-major)
+        issuer_wait_simt();
+        const uint32_t id = idesc_bf16(128, 64, 0, 1);
+        for (int j = 0; j < NK / 16; ++j) {
+          const uint64_t bh = sdesc(vhi + 2 * j * 1024, 1024, 128);
+          const uint64_t bl = sdesc(vlo + 2 * j * 1024, 1024, 128);
+          mma_bf16_ts(R + kCA, R + kCD + 16 * j, bh, id, j > 0);
+          mma_bf16_ts(R + kCA, R + kCD + 16 * j, bl, id, 1);
+          mma_bf16_ts(R + kCA, R + kCD + 16 * j + 8, bh, id, 1);
+        }
+        commit(&t3.mma[t]);
+        commit(&t3.kvfree);  // this tile no longer reads K / V' of this layer
+      }
+      ++n_kv;
+      // ---- P4: x += O' / l ; LN2 -> A ----
+      wait_mma();
+      {
+        float d[kDModel];
+        t3_ld64(cA, d);
+        if (ok) {
+#pragma unroll
+          for (int j = 0; j < kDModel; ++j) x[j] = fmaf(d[j], inv_l, x[j]);
+        }
+        t3_layer_norm(x, lnp_s[L][2], lnp_s[L][3], d);
+        if (!ok) {
+#pragma unroll
+          for (int j = 0; j < kDModel; ++j) d[j] = 0.0f;
+        }
+        t3_st_split<64>(cA, d);
+        tmem_st_wait();
+        done();
+      }
+      if (issuer) {  // M4: H = A W1   (N = 32, K = 64)
+        issuer_wait_simt();
+        t3_mma3(R + kCD, R + kCA, 32, wb(L), wb(L) + 4096, 32 * 16, 4, idesc_bf16(128, 32));
+        commit(&t3.mma[t]);
+      }
+      // ---- P5: ReLU(H) -> A2 ----
+      wait_mma();
+      {
+        float h[kFfn];
+        tmem_ld32(lanebase + kCD, reinterpret_cast<uint32_t*>(h));
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < kFfn; ++j) h[j] = ok ? fmaxf(h[j], 0.0f) : 0.0f;
+        t3_st_split<32>(lanebase + kCA2, h);
+        tmem_st_wait();
+        done();
+      }
+      if (issuer) {  // M5: D2 = ReLU(H) W2   (N = 64, K = 32)
+        issuer_wait_simt();
+        t3_mma3(R + kCW2, R + kCA2, 16, wb(L) + 8192, wb(L) + 8192 + 4096, 64 * 16, 2, idesc_bf16(128, 64));
+        commit(&t3.mma[t]);
+      }
+      // ---- P6: x += D2 ----
+      wait_mma();
+      {
+        float d[kDModel];
+        t3_ld64(lanebase + kCW2, d);
+        if (ok) {
+#pragma unroll
+          for (int j = 0; j < kDModel; ++j) x[j] += d[j];
+        }
+      }
+    }
+
+    // ---- K5: y = x out_linear, masked max over rows, CTR head ----
+    t3_st_split<64>(cA, x);  // invalid rows carry x = 0
+    tmem_st_wait();
+    done();
+    if (issuer) {
+      issuer_wait_simt();
+      t3_mma3(R + kCD, R + kCA, 32, wsm + NL * kW3Layer, wsm + NL * kW3Layer + 8192, 64 * 16, 4,
+              idesc_bf16(128, 64));
+      commit(&t3.mma[t]);
+    }
+    wait_mma();
+    {
+      float y[kDModel];
+      t3_ld64(lanebase + kCD, y);
+      if (tid == 0) any_s = 0;
+      named_bar_sync(1, kT3Threads);  // every row is past its last softmax (valid_w, kmax_s free)
+      if (ok) any_s = 1;
+      if (tid < 8) valid_w[tid] = 0u;
+      if (tid < 2) kmax_s[tid] = 0u;
+#pragma unroll
+      for (int j = 0; j < kDModel; ++j) {
+        const float v = warp_max_f32(ok ? y[j] : -INFINITY);
+        if (lane == 0) red_s[warp][j] = v;
+      }
+    }
+    named_bar_sync(1, kT3Threads);
+    // head (trainer.py:361-365): z = [pooled | unit(c) | ctx]; 4 threads per hidden unit
+    if (tid < kDModel) {
+      float v = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < kT3Warps; ++w) v = fmaxf(v, red_s[w][tid]);
+      v = any_s ? v : 0.0f;  // empty user -> pooled = 0 (trainer.py:358-359)
+      z_s[tid] = v;
+      if (pooled_out) pooled_out[(size_t)item * kDModel + tid] = v;
+    } else if (tid < kDModel + kEmbed) {
+      z_s[tid] = st.cand_unit[(size_t)item * kEmbed + tid - kDModel];
+    } else if (tid < kDModel + kEmbed + kCtx) {
+      z_s[tid] = st.ctx[st.item_req[item] * kCtx + tid - kDModel - kEmbed];
+    }
+    named_bar_sync(1, kT3Threads);
+    {
+      const int hu = tid & 63, part = tid >> 6;  // inputs [26 part, 26 part + 26)
+      float acc = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 26; ++i) acc = fmaf(z_s[26 * part + i], __ldg(p.head_w1 + (26 * part + i) * kHidden + hu), acc);
+      hpart_s[part][hu] = acc;
+    }
+    named_bar_sync(1, kT3Threads);
+    if (tid < kHidden) {
+      const float hsum = ((hpart_s[0][tid] + hpart_s[1][tid]) + (hpart_s[2][tid] + hpart_s[3][tid])) +
+                         __ldg(p.head_b1 + tid);
+      hid_s[tid] = fmaxf(hsum, 0.0f);
+    }
+    named_bar_sync(1, kT3Threads);
+    if (warp == 0) {  // lane: head (lane & 3), hidden slice 8 * (lane >> 2) .. + 8
+      const int hd = lane & 3, j0 = 8 * (lane >> 2);
+      float o = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o = fmaf(hid_s[j0 + j], __ldg(p.head_w2 + (j0 + j) * kHeads + hd), o);
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) o += __shfl_xor_sync(0xffffffffu, o, off);
+      if (lane < kHeads) logits[(size_t)item * kHeads + lane] = o + __ldg(p.head_b2 + lane);
+    }
+    // (z_s / hid_s / red_s are rewritten only after the next item's barriers)
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_free<512>(0u);
+  cta_stamp(kDbgSkut, 1);
+}
+
+bool skut_tc3_supported(const NNCfg& nn, const Params& p) {
+  const int S_pad = (nn.seq_len + 15) & ~15;
+  return S_pad <= 192 && p.num_layers >= 1 && p.num_layers <= 2;
+}
+
+cudaError_t launch_skut_tc3(const Params& p, const SkutImages3& img, const NNCfg& nn, const Staged& st,
+                            const int32_t* idx, int n, float* logits, float* pooled, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int S_pad = (nn.seq_len + 15) & ~15;
+  const size_t smem = (size_t)p.num_layers * kW3Layer + kImg3WO + 4 * (size_t)S_pad * 128;
+  cudaError_t e = cudaFuncSetAttribute(skut_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return launch_pdl(skut_tc3_kernel, dim3(n < sms ? n : sms), dim3(kT3Threads), smem, s, p, img, nn, st, idx, n,
+                    logits, pooled);
+}
+
+}  // namespace tav2

@@ -74,6 +74,7 @@ struct tav2_ctx {
   float* tok_unit = nullptr;
   uint32_t* tok_img = nullptr;
   float* cand_unit = nullptr;
+  float* tok_feat = nullptr;   // [T, 64] Eq. 4 token features (prep, bf16 SKUT gather)
   NNScan scan{};               // threshold-scan NN buffers (nn_scan.cu)
 
   int32_t* idx = nullptr;
@@ -84,6 +85,8 @@ struct tav2_ctx {
   Params params{};
   uint8_t* d_images = nullptr;  // bf16x3 weight images (tensor-core SKUT)
   SkutImages images{};
+  uint8_t* d_images3 = nullptr;  // folded images of skut_tc3 (Wqk, Wvo)
+  SkutImages3 images3{};
   bool params_ok = false;
   // current batch
   Plan plan{};
@@ -120,6 +123,7 @@ Staged staged_view(tav2_ctx* c) {
   s.tok_unit = c->tok_unit;
   s.tok_img = c->tok_img;
   s.cand_unit = c->cand_unit;
+  s.tok_feat = c->tok_feat;
   s.n_req = p.n_req;
   s.n_items = p.n_items;
   s.n_tok = p.n_tok;
@@ -148,6 +152,8 @@ int free_all(tav2_ctx* c) {
   cudaFree(c->tok_unit);
   cudaFree(c->tok_img);
   cudaFree(c->cand_unit);
+  cudaFree(c->tok_feat);
+  cudaFree(c->d_images3);
   cudaFree(c->scan.gmax);
   cudaFree(c->scan.bound);
   cudaFree(c->scan.count);
@@ -272,6 +278,8 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
       cudaSuccess)
     return bad(e, "token image");
   if ((e = cudaMalloc(&c->cand_unit, (size_t)N * kEmbed * 4)) != cudaSuccess) return bad(e, "cand_unit");
+  if ((e = cudaMalloc(&c->tok_feat, (size_t)std::max<int64_t>(T, 1) * kDModel * 4)) != cudaSuccess)
+    return bad(e, "token features");
   // scan buffers: a source has at most max(8k + 2, 16384/32 + 2) groups
   // (planner), a (candidate, source) at most its source length of survivors
   c->scan.gcap = (std::max(8 * c->kmax + 2, kCaps[0] / 32 + 2) + 8 + 7) & ~7;  // + 8: aligned rows
@@ -424,6 +432,42 @@ int tav2_load_params(tav2_ctx* c, int n, const char* const* names, const float* 
     c->images.wb[l] = c->images.wa[l] + kImgWA;
   }
   c->images.wout = c->d_images + (size_t)L * (kImgWA + kImgWB);
+
+  // ---- folded images of skut_tc3: per layer [ [Wqk|Wvo]^T | W1^T | W2^T ] ----
+  // Wqk = Wq Wk^T * log2(e)/8 (scores in the exp2 domain), Wvo = Wv Wo; f64
+  // products rounded once to f32 before the bf16 hi/lo split.
+  {
+    const size_t lay = (size_t)kImg3WA + kImg3WB;
+    const size_t bytes3 = (size_t)L * lay + kImg3WO;
+    std::vector<uint8_t> img3(bytes3, 0);
+    std::vector<float> wqk(64 * 64), wvo(64 * 64);
+    const double sc = 1.4426950408889634 / 8.0;
+    for (int l = 0; l < L; ++l) {
+      const float *wq = host_of(P.wq[l]), *wk = host_of(P.wk[l]), *wv = host_of(P.wv[l]), *wo = host_of(P.wo[l]);
+      for (int i = 0; i < 64; ++i)
+        for (int j = 0; j < 64; ++j) {
+          double a = 0.0, b = 0.0;
+          for (int m2 = 0; m2 < 64; ++m2) {
+            a += (double)wq[i * 64 + m2] * (double)wk[j * 64 + m2];
+            b += (double)wv[i * 64 + m2] * (double)wo[m2 * 64 + j];
+          }
+          wqk[i * 64 + j] = (float)(a * sc);
+          wvo[i * 64 + j] = (float)b;
+        }
+      uint8_t* base = img3.data() + (size_t)l * lay;
+      put(base, 128, 64, 0, wqk.data(), 64, 64);
+      put(base, 128, 64, 64, wvo.data(), 64, 64);
+      put(base + kImg3WA, 32, 64, 0, host_of(P.w1[l]), 64, 32);
+      put(base + kImg3WA + 8192, 64, 32, 0, host_of(P.w2[l]), 32, 64);
+    }
+    put(img3.data() + (size_t)L * lay, 64, 64, 0, host_of(P.out_linear), 64, 64);
+    if (c->d_images3) cudaFree(c->d_images3);
+    c->d_images3 = nullptr;
+    CU(cudaMalloc(&c->d_images3, bytes3));
+    CU(cudaMemcpy(c->d_images3, img3.data(), bytes3, cudaMemcpyHostToDevice));
+    for (int l = 0; l < L; ++l) c->images3.w[l] = c->d_images3 + (size_t)l * lay;
+    c->images3.wout = c->d_images3 + (size_t)L * lay;
+  }
   c->params_ok = true;
   return TAV2_OK;
 }
@@ -608,7 +652,7 @@ int check_ready(tav2_ctx* c, int mode) {
 // the reference's f64 formula, so the index sets are the reference's).
 int run_nn(tav2_ctx* c, int32_t* idx, float* scores, cudaStream_t s) {
   Staged st = staged_view(c);
-  CU(timed(c, "prep", s, [&] { return launch_prep(st, s); }));
+  CU(timed(c, "prep", s, [&] { return launch_prep(st, c->params_ok ? &c->params : nullptr, s); }));
   CU(timed(c, "nn_scan1", s, [&] { return launch_nn_scan(st, c->nn, c->scan, 1, s); }));
   CU(timed(c, "nn_bound", s, [&] { return launch_nn_bound(st, c->nn, c->scan, s); }));
   CU(timed(c, "nn_scan2", s, [&] { return launch_nn_scan(st, c->nn, c->scan, 2, s); }));
@@ -623,6 +667,12 @@ int run_score(tav2_ctx* c, int mode, const int32_t* idx, float* logits, float* p
   // The 2-row-tile tensor-core SKUT holds K/V of <= 256 keys in shared
   // memory; longer sequences (the k_ll = 256 sweep point, S = 352) run the
   // SIMT kernel, which is f32 throughout and so also meets the bf16 budget.
+  if (mode == TAV2_MODE_BF16 && skut_tc3_supported(c->nn, c->params)) {
+    CU(timed(c, "skut_tc", s, [&] {
+      return launch_skut_tc3(c->params, c->images3, c->nn, st, idx, st.n_items, logits, pooled, s);
+    }));
+    return TAV2_OK;
+  }
   if (mode == TAV2_MODE_BF16 && c->nn.seq_len <= 256) {
     CU(timed(c, "skut_tc", s, [&] {
       return launch_skut_tc(c->params, c->images, c->nn, &st, idx, nullptr, nullptr, st.n_items,
@@ -658,7 +708,7 @@ int tav2_encode(tav2_ctx* c, const int32_t* idx_dev, float* features_dev, uint8_
   if (!idx_dev || !features_dev || !mask_dev) return fail(TAV2_EINVAL, "null device pointer");
   CU(cudaSetDevice(c->device));
   Staged st = staged_view(c);
-  CU(launch_prep(st, (cudaStream_t)stream));
+  CU(launch_prep(st, nullptr, (cudaStream_t)stream));
   CU(launch_encode(st, c->nn, c->params, idx_dev, features_dev, mask_dev, (cudaStream_t)stream));
   return TAV2_OK;
 }
@@ -691,7 +741,7 @@ int tav2_score(tav2_ctx* c, int mode, const int32_t* idx_dev, float* logits_dev,
   CU(cudaSetDevice(c->device));
   c->launches = 0;
   Staged st = staged_view(c);
-  CU(timed(c, "prep", (cudaStream_t)stream, [&] { return launch_prep(st, (cudaStream_t)stream); }));
+  CU(timed(c, "prep", (cudaStream_t)stream, [&] { return launch_prep(st, &c->params, (cudaStream_t)stream); }));
   return run_score(c, mode, idx_dev, logits_dev, pooled_dev, (cudaStream_t)stream);
 }
 

@@ -113,6 +113,17 @@ constexpr int kImgWA = 2 * 192 * 64 * 2;  // 49152
 constexpr int kImgWB = 2 * (64 * 64 + 32 * 64 + 64 * 32) * 2;  // 32768
 constexpr int kImgWO = 2 * 64 * 64 * 2;   // 16384
 
+// Images of the folded tensor-core SKUT (skut_tc3.cu), same slab layout:
+// per layer [ [Wqk|Wvo]^T N=128 K=64 (32 KB) | W1^T (8 KB) | W2^T (8 KB) ],
+// Wqk = Wq Wk^T log2(e)/8 and Wvo = Wv Wo in f64 before the split.
+struct SkutImages3 {
+  const uint8_t* w[kMaxLayers];
+  const uint8_t* wout;
+};
+constexpr int kImg3WA = 2 * 128 * 64 * 2;  // 32768
+constexpr int kImg3WB = kImgWB - kImgWO;   // 16384 (W1 | W2)
+constexpr int kImg3WO = kImgWO;
+
 struct NNCfg {
   int32_t recent, k[3];       // k[0] = k_ll, k[1] = k_rt, k[2] = k_imp
   int32_t seg_start[4];       // layout starts: NN_LL, RT_recent, NN_RT_tail, NN_IMP
@@ -133,6 +144,7 @@ struct Staged {
   float* tok_unit;         // [T, 32] derived: unit(dequantize(q)) (core.py:77-79)
   uint32_t* tok_img;       // derived: fp16 unit rows, kScanTile-token tiles (prep_kernel)
   float* cand_unit;        // [N, 32] derived: l2_normalize_rows(cand)
+  float* tok_feat;         // [T, 64] derived: [unit(q) | 0] + action rows + surface row (Eq. 4 token part)
   int n_req, n_items, n_tok, n_tiles, n_work;
 };
 
@@ -200,7 +212,10 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 
 // Host-side launchers (defined in the kernel translation units).
 namespace tav2 {
-cudaError_t launch_prep(const Staged& st, cudaStream_t s);
+cudaError_t launch_prep(const Staged& st, const Params* p, cudaStream_t s);
+bool skut_tc3_supported(const NNCfg& nn, const Params& p);
+cudaError_t launch_skut_tc3(const Params& p, const SkutImages3& img, const NNCfg& nn, const Staged& st,
+                            const int32_t* idx, int n, float* logits, float* pooled, cudaStream_t s);
 cudaError_t launch_nn_scan(const Staged& st, const NNCfg& nn, const NNScan& sc, int pass,
                            cudaStream_t s);
 cudaError_t launch_nn_bound(const Staged& st, const NNCfg& nn, const NNScan& sc, cudaStream_t s);
