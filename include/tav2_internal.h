@@ -15,9 +15,11 @@ extern "C" {
  * row-major device buffers; D: [128, N] f32 (s32 for i8).  Synchronous. */
 int tav2_tc_selftest(int which, const void* A, const void* B, void* D, int N, int K, void* stream);
 
-/* Debug: device buffer (>= 512 int64) receiving %globaltimer stamps of NN
- * work unit `block`'s CTA (slots 0..319) and of SKUT CTA 0's first
- * candidate (slots 320..447).  NULL disables.  Not thread-safe. */
+/* Debug (libtav2_debug.so only): device buffer (>= 704 int64) receiving
+ * %globaltimer stamps of NN scan work unit `block`'s CTA (slots 0..319,
+ * 520..583), the older SKUT kernels' stamps (320..511) and the per-segment
+ * clock64 accounting of skut_tc3 CTA 0 (640..703).  NULL disables.  Not
+ * thread-safe. */
 int tav2_debug_timeline(long long* dev, int block);
 
 /* Debug (libtav2_debug.so only): device buffer (>= 7 * 3 * 4096 int64)

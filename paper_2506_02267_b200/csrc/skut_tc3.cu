@@ -54,6 +54,11 @@ constexpr uint32_t kCA = 192, kCD = 0, kCA2 = 32, kCW2 = 64;
 // weight image offsets inside the shared-memory weight region
 constexpr int kW3Layer = kImg3WA + kImg3WB;  // 48 KB per layer
 
+// Debug (libtav2_debug.so): clock64 accumulated per code segment of the two
+// tile leaders (thread 0 / 128: row thread + MMA issuer) of CTA 0 over all its
+// candidates: g_dbg_skut3[32 * tile + segment], [32 * tile + 31] = items.
+__device__ long long* g_dbg_skut3 = nullptr;
+
 struct T3Bars {
   uint64_t simt[2], mma[2], kvready, kvfree, wfull;
 };
@@ -189,6 +194,15 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   }
 
   const bool issuer = (tid & 127) == 0;
+  long long* dbg = (kDebug && blockIdx.x == 0 && issuer && g_dbg_skut3) ? g_dbg_skut3 + 32 * (tid >> 7) : nullptr;
+  long long t_last = 0;
+  auto stamp = [&](int id) {
+    if (kDebug && dbg) {
+      const long long now = clock64();
+      dbg[id] += now - t_last;
+      t_last = now;
+    }
+  };
   const uint32_t R = 256u * t;
   const uint32_t lanebase = ((uint32_t)(32 * q) << 16) + R;
   const uint32_t cA = lanebase + kCA;
@@ -223,6 +237,10 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   const float4* pos4 = reinterpret_cast<const float4*>(p.position_table + (size_t)(in_seq ? r : 0) * kDModel);
 
   for (int item = blockIdx.x; item < n; item += gridDim.x) {
+    if (kDebug && dbg) {
+      dbg[31] += 1;
+      t_last = clock64();
+    }
     // ---- K3: gather + encode: x = tok_feat[tok] + pos[r] + [0 | unit(c)] ----
     float x[kDModel];
     bool ok = false;
@@ -256,11 +274,14 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         if ((uint32_t)(w >> 32)) atomicOr(&valid_w[(r0 >> 5) + 1], (uint32_t)(w >> 32));
       }
     }
+    stamp(0);
     named_bar_sync(1, kT3Threads);  // valid_w complete
+    stamp(1);
 
     for (int L = 0; L < NL; ++L) {
       // ---- P1: a = LN1(x) -> A (TMEM) and K = a (smem); ||a||^2 -> kmax ----
       if (n_kv > 0) mbar_wait_sleep(&t3.kvfree, (n_kv - 1) & 1);  // both tiles' previous P.V retired
+      stamp(2);
       {
         float a[kDModel];
         t3_layer_norm(x, lnp_s[L][0], lnp_s[L][1], a);
@@ -285,13 +306,16 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         tmem_st_wait();
         done();
       }
+      stamp(3);
       if (issuer) {  // M1: [Q' | V'] = A [Wqk | Wvo]   (N = 128, K = 64)
         issuer_wait_simt();
         t3_mma3(R + kCD, R + kCA, 32, wa(L), wa(L) + kImg3WA / 2, 128 * 16, 4, idesc_bf16(128, 128));
         commit(&t3.mma[t]);
       }
+      stamp(4);
       // ---- P2: Q' -> A, V' -> smem (MN-major) ----
       wait_mma();
+      stamp(5);
       float qn2 = 0.0f;
       {
         float v[32];
@@ -335,17 +359,20 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         fence_before();
         mbar_arrive(&t3.kvready);  // this row's K, V' and Q' are in place
       }
+      stamp(6);
       if (issuer) {  // M2: S = Q' K^T   (N = keys of this tile, K = 64)
         mbar_wait(&t3.kvready, n_kv & 1);
         fence_after();
         t3_mma3(R + kCD, R + kCA, 32, khi, klo, S_pad * 16, 4, idesc_bf16(128, NK));
         commit(&t3.mma[t]);
       }
+      stamp(7);
       // ---- P3: causal key-masked softmax -> P (bf16 hi/lo, in place over S) ----
       // Single pass with the Cauchy-Schwarz shift m' = ||q'_r|| max_j ||a_j||
       // (>= q'_r . a_j, the exp2-domain score): shift invariance makes 1/l the
       // exact normaliser of encoder.py:203-211.
       wait_mma();
+      stamp(8);
       float inv_l = 0.0f;
       {
         mbar_wait_sleep(&t3.kvready, n_kv & 1);  // kmax_s[L] complete (already passed)
@@ -385,6 +412,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         tmem_st_wait();
         done();
       }
+      stamp(9);
       if (issuer) {  // M3: O' = P V'   (N = 64, K = keys; V' MN-major)
         issuer_wait_simt();
         const uint32_t id = idesc_bf16(128, 64, 0, 1);
@@ -398,9 +426,11 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         commit(&t3.mma[t]);
         commit(&t3.kvfree);  // this tile no longer reads K / V' of this layer
       }
+      stamp(10);
       ++n_kv;
       // ---- P4: x += O' / l ; LN2 -> A ----
       wait_mma();
+      stamp(11);
       {
         float d[kDModel];
         t3_ld64(cA, d);
@@ -417,13 +447,16 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         tmem_st_wait();
         done();
       }
+      stamp(12);
       if (issuer) {  // M4: H = A W1   (N = 32, K = 64)
         issuer_wait_simt();
         t3_mma3(R + kCD, R + kCA, 32, wb(L), wb(L) + 4096, 32 * 16, 4, idesc_bf16(128, 32));
         commit(&t3.mma[t]);
       }
+      stamp(13);
       // ---- P5: ReLU(H) -> A2 ----
       wait_mma();
+      stamp(14);
       {
         float h[kFfn];
         tmem_ld32(lanebase + kCD, reinterpret_cast<uint32_t*>(h));
@@ -434,13 +467,16 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         tmem_st_wait();
         done();
       }
+      stamp(15);
       if (issuer) {  // M5: D2 = ReLU(H) W2   (N = 64, K = 32)
         issuer_wait_simt();
         t3_mma3(R + kCW2, R + kCA2, 16, wb(L) + 8192, wb(L) + 8192 + 4096, 64 * 16, 2, idesc_bf16(128, 64));
         commit(&t3.mma[t]);
       }
+      stamp(16);
       // ---- P6: x += D2 ----
       wait_mma();
+      stamp(17);
       {
         float d[kDModel];
         t3_ld64(lanebase + kCW2, d);
@@ -449,19 +485,23 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
           for (int j = 0; j < kDModel; ++j) x[j] += d[j];
         }
       }
+      stamp(18);
     }
 
     // ---- K5: y = x out_linear, masked max over rows, CTR head ----
     t3_st_split<64>(cA, x);  // invalid rows carry x = 0
     tmem_st_wait();
     done();
+    stamp(19);
     if (issuer) {
       issuer_wait_simt();
       t3_mma3(R + kCD, R + kCA, 32, wsm + NL * kW3Layer, wsm + NL * kW3Layer + 8192, 64 * 16, 4,
               idesc_bf16(128, 64));
       commit(&t3.mma[t]);
     }
+    stamp(20);
     wait_mma();
+    stamp(21);
     {
       float y[kDModel];
       t3_ld64(lanebase + kCD, y);
@@ -477,6 +517,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       }
     }
     named_bar_sync(1, kT3Threads);
+    stamp(22);
     // head (trainer.py:361-365): z = [pooled | unit(c) | ctx]; 4 threads per hidden unit
     if (tid < kDModel) {
       float v = -INFINITY;
@@ -515,12 +556,15 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       if (lane < kHeads) logits[(size_t)item * kHeads + lane] = o + __ldg(p.head_b2 + lane);
     }
     // (z_s / hid_s / red_s are rewritten only after the next item's barriers)
+    stamp(23);
   }
   fence_before();
   __syncthreads();
   if (warp == 0) tmem_free<512>(0u);
   cta_stamp(kDbgSkut, 1);
 }
+
+cudaError_t set_debug_skut3(long long* dev) { return cudaMemcpyToSymbol(g_dbg_skut3, &dev, sizeof(dev)); }
 
 bool skut_tc3_supported(const NNCfg& nn, const Params& p) {
   const int S_pad = (nn.seq_len + 15) & ~15;

@@ -773,7 +773,10 @@ int tav2_rank(tav2_ctx* c, const tav2_request* reqs, int n_req, int mode, float*
 int tav2_last_launch_count(const tav2_ctx* c) { return c ? c->launches : 0; }
 
 int tav2_debug_timeline(long long* dev, int block) {
-  return set_debug_timeline(dev, block) == cudaSuccess && set_debug_skut(dev ? dev + 320 : nullptr) == cudaSuccess ? TAV2_OK : fail(TAV2_ECUDA, "debug timeline");
+  return set_debug_timeline(dev, block) == cudaSuccess && set_debug_skut(dev ? dev + 320 : nullptr) == cudaSuccess &&
+                 set_debug_skut3(dev ? dev + 640 : nullptr) == cudaSuccess
+             ? TAV2_OK
+             : fail(TAV2_ECUDA, "debug timeline");
 }
 
 int tav2_debug_cta(long long* dev) {

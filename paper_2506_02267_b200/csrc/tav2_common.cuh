@@ -223,6 +223,7 @@ cudaError_t launch_nn_select(const Staged& st, const NNCfg& nn, const NNScan& sc
                              float* scores, cudaStream_t s);
 cudaError_t set_debug_timeline(long long* dev, int block);
 cudaError_t set_debug_skut(long long* dev);
+cudaError_t set_debug_skut3(long long* dev);
 cudaError_t set_dbg_cta_prep(long long* dev);
 cudaError_t set_dbg_cta_scan(long long* dev);
 cudaError_t set_dbg_cta_select(long long* dev);
