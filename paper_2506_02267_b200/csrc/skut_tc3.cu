@@ -19,9 +19,10 @@
 // split-bf16 product (a_hi b_hi + a_hi b_lo + a_lo b_hi, f32 accumulation
 // in TMEM); residual stream, LN, softmax statistics and the head are f32.
 //
-// Layout: thread = sequence row (the tc2 balanced row-block mapping: warp
-// (t, q) owns rows rpw*kb .. where kb = q (tile 0) or 7 - q (tile 1), so each
-// SM sub-partition carries one early and one late block).  Two independent
+// Layout: thread = sequence row; the S_pad rows form 8 blocks of rpw = S_pad/8
+// and warp (t, q) owns block q (tile 0) or 7 - q (tile 1): every SM
+// sub-partition holds one early and one late block, and tile 0 only needs
+// the keys < S_pad/2 (half the score / P.V MMA work).  Two independent
 // tiles (warps 4t..4t+3), each with its own TMEM half (256 columns), its own
 // simt/mma barriers and issuer (thread 128t); they couple only through the
 // K/V operands (kvready / kvfree).  All weight images stay resident in
@@ -160,11 +161,12 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = warp >> 2, q = warp & 3;
   const int rpw = S_pad >> 3;
+  // row blocks: tile 0 = blocks 0-3 (keys < S_pad/2 only), tile 1 = 7-4, so
+  // each SM sub-partition q holds one early and one late block
   const int kb = t == 0 ? q : 7 - q;
   const bool mapped = lane < rpw;
   const int r = rpw * kb + lane;
-  const int NK0 = ((S_pad >> 1) + 15) & ~15;
-  const int NK = t == 0 ? NK0 : S_pad;  // keys this tile's rows can see
+  const int NK = t == 0 ? (((S_pad >> 1) + 15) & ~15) : S_pad;  // keys this tile's rows can see
   if (tid == 0) {
     mbar_init(&t3.simt[0], 128);
     mbar_init(&t3.simt[1], 128);
@@ -236,6 +238,9 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   }
   const float4* pos4 = reinterpret_cast<const float4*>(p.position_table + (size_t)(in_seq ? r : 0) * kDModel);
 
+  // the gather's index chain (idx -> token) of the next candidate is resolved
+  // during the last layer of the current one
+  int tok_pf = (in_seq && (int)blockIdx.x < n) ? slot_token(st, nn, idx, blockIdx.x, r) : -1;
   for (int item = blockIdx.x; item < n; item += gridDim.x) {
     if (kDebug && dbg) {
       dbg[31] += 1;
@@ -245,7 +250,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     float x[kDModel];
     bool ok = false;
     if (in_seq) {
-      const int tok = slot_token(st, nn, idx, item, r);
+      const int tok = tok_pf;
       ok = tok >= 0;
       if (ok) {
         const float4* tf = reinterpret_cast<const float4*>(st.tok_feat + (size_t)tok * kDModel);
@@ -279,6 +284,10 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     stamp(1);
 
     for (int L = 0; L < NL; ++L) {
+      if (L == NL - 1) {
+        const int nx = item + gridDim.x;
+        tok_pf = (in_seq && nx < n) ? slot_token(st, nn, idx, nx, r) : -1;
+      }
       // ---- P1: a = LN1(x) -> A (TMEM) and K = a (smem); ||a||^2 -> kmax ----
       if (n_kv > 0) mbar_wait_sleep(&t3.kvfree, (n_kv - 1) & 1);  // both tiles' previous P.V retired
       stamp(2);
