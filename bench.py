@@ -221,7 +221,6 @@ def run_gpu(args, rank, world, local_rank):
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    eng.set_profiling(True)
     barrier()
     torch.cuda.synchronize()
     with Clocks(local_rank) as clk:
@@ -233,9 +232,19 @@ def run_gpu(args, rank, world, local_rank):
         torch.cuda.synchronize()
     barrier()
     launches_per_step = eng.last_launch_count()
-    kt = eng.kernel_times()
-    eng.set_profiling(False)
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    # per-kernel times: a separate profiled pass (CUDA events around every
+    # launch on the launch stream serialise the programmatic-dependent-launch
+    # overlap, so they are kept out of the timed steps above)
+    eng.set_profiling(True)
+    n_prof = max(10, min(args.steps, 100))
+    for i in range(n_prof):
+        flush.fill_(float(i))
+        eng.run_staged(mode, logits)
+    torch.cuda.synchronize()
+    kt = eng.kernel_times()
+    prof_ms = sum(v[0] for v in kt.values()) / n_prof
+    eng.set_profiling(False)
     dev_ms = sum(step_ms)
     t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -281,14 +290,15 @@ def run_gpu(args, rank, world, local_rank):
             ach = work / (per_launch_ms / 1e3) / 1e12
             roof = {"kernel": name, "bound": "tensor", "achieved": round(ach, 3),
                     "peak": tflops, "unit": "TFLOP/s", "frac": round(ach / tflops, 5),
-                    "peak_source": f"{src} bf16_tflops (burst)", "traffic": None,
+                    "peak_source": f"{src} bf16_tflops (burst)", "traffic": _traffic(name),
                     "kernel_ms_per_launch": round(per_launch_ms, 4),
-                    "share_of_step": round(ms / max(dev_ms, 1e-9), 3)}
+                    "share_of_step": round(per_launch_ms / max(prof_ms, 1e-9), 3)}
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16x3 (fp32-accurate split) tensor + i8 NN" if mode == "bf16" else "fp32",
+        "dtype": ("bf16x3 split GEMMs on tcgen05 (f32 accumulate); NN: fp16 tcgen05 scan + f64 exact "
+                  "re-scoring" if mode == "bf16" else "fp32 SIMT transformer; NN: fp16 scan + f64 re-scoring"),
         "mode": mode, "data": "synthetic (generate_requests, seqrank.dataset distribution), random-init weights seed 0",
         "config": {"workload": f"{args.config}: {n_req} request(s) x {n_cand} candidates, L={L}, "
                                f"RT=256, IMP=256, NNConfig{nn_t} -> S={nn.seq_len}, 2 layers d=64",
@@ -307,6 +317,16 @@ def run_gpu(args, rank, world, local_rank):
         "clocks": clk.summary(),
     }
     return out
+
+
+def _traffic(kernel):
+    """DRAM bytes per launch of `kernel` (dram__bytes_read.sum + write.sum) from
+    the committed ncu --set full capture summary, or None."""
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(kernel)
+    except (OSError, ValueError):
+        return None
 
 
 def _staged_bytes(reqs):

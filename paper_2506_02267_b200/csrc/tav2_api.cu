@@ -668,7 +668,7 @@ int run_score(tav2_ctx* c, int mode, const int32_t* idx, float* logits, float* p
   // memory; longer sequences (the k_ll = 256 sweep point, S = 352) run the
   // SIMT kernel, which is f32 throughout and so also meets the bf16 budget.
   if (mode == TAV2_MODE_BF16 && skut_tc3_supported(c->nn, c->params)) {
-    CU(timed(c, "skut_tc", s, [&] {
+    CU(timed(c, "skut_tc3", s, [&] {
       return launch_skut_tc3(c->params, c->images3, c->nn, st, idx, st.n_items, logits, pooled, s);
     }));
     return TAV2_OK;
