@@ -13,89 +13,102 @@
 
 namespace tav2 {
 
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
 // ---------------------------------------------------------------------------
 // K1: per token  unit(dequantize(q)) in f32 with the reference's rounding
 // steps (core.py:54-57 then :69-74), its fp16 tile image for the tensor-core
 // scan and (with parameters) its Eq. 4 feature part for the SKUT gather; per
 // candidate  l2_normalize_rows (nnsearch.py:313-320).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float sumsq8(const float* v) {
-  // 8 interleaved accumulators, adjacent-pair combine (a fixed order; the
-  // reference's einsum order is BLAS-internal, differences are <= 1 ulp).
+// Sum of squares of a 32-vector held by a quad of threads (thread g holds
+// elements 8g..8g+7): 8 interleaved accumulators a[l] = ((v_l^2 + v_{l+8}^2)
+// + v_{l+16}^2) + v_{l+24}^2, adjacent-pair combine -- a fixed order (the
+// reference's einsum order is BLAS-internal; differences are <= 1 ulp).
+// Every thread of the quad returns the same value.
+__device__ __forceinline__ float quad_sumsq(const float* v, unsigned qm) {
   float a[8];
 #pragma unroll
-  for (int l = 0; l < 8; ++l) a[l] = __fmul_rn(v[l], v[l]);
-#pragma unroll
-  for (int j = 8; j < kEmbed; ++j) a[j & 7] = __fadd_rn(a[j & 7], __fmul_rn(v[j], v[j]));
-  float b0 = __fadd_rn(a[0], a[1]), b1 = __fadd_rn(a[2], a[3]);
-  float b2 = __fadd_rn(a[4], a[5]), b3 = __fadd_rn(a[6], a[7]);
+  for (int l = 0; l < 8; ++l) {
+    const float sq = __fmul_rn(v[l], v[l]);
+    const float s0 = __shfl_sync(qm, sq, 0, 4);
+    const float s1 = __shfl_sync(qm, sq, 1, 4);
+    const float s2 = __shfl_sync(qm, sq, 2, 4);
+    const float s3 = __shfl_sync(qm, sq, 3, 4);
+    a[l] = __fadd_rn(__fadd_rn(__fadd_rn(s0, s1), s2), s3);
+  }
+  const float b0 = __fadd_rn(a[0], a[1]), b1 = __fadd_rn(a[2], a[3]);
+  const float b2 = __fadd_rn(a[4], a[5]), b3 = __fadd_rn(a[6], a[7]);
   return __fadd_rn(__fadd_rn(b0, b1), __fadd_rn(b2, b3));
 }
 
+// One quad of threads per token row (then per candidate row); thread g owns
+// elements 8g..8g+7 of the 32-vector and features 16g..16g+15 of the 64-d
+// Eq. 4 token part.
 __global__ void __launch_bounds__(256) prep_kernel(Staged st, Params p, int with_feat) {
   cta_stamp(kDbgPrep, 0);
   griddep_launch();
   griddep_wait();  // the previous step's kernels may still read tok_unit / cand_unit
   cta_stamp(kDbgPrep, 2);
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  int i = gt >> 2;
+  const int g = gt & 3;
+  const unsigned qm = 0xfu << (threadIdx.x & 28);  // this quad's lanes (a quad is never split)
   if (i < st.n_tok) {
-    const int4* src = reinterpret_cast<const int4*>(st.emb + (size_t)i * kEmbed);
-    int4 raw[2] = {src[0], src[1]};
-    const int8_t* q = reinterpret_cast<const int8_t*>(raw);
-    float d[kEmbed];
+    const int2 raw = reinterpret_cast<const int2*>(st.emb + (size_t)i * kEmbed)[g];
+    const int8_t* q = reinterpret_cast<const int8_t*>(&raw);
+    float d[8];
 #pragma unroll
-    for (int j = 0; j < kEmbed; ++j) {
-      int qi = q[j];
-      d[j] = __fmul_rn(__fdiv_rn((float)qi, 127.0f), 0.65f);
-    }
-    float nrm = __fsqrt_rn(sumsq8(d));
-    if (nrm == 0.0f) nrm = 1.0f;
-    float u[kEmbed];
+    for (int j = 0; j < 8; ++j) d[j] = __fmul_rn(__fdiv_rn((float)q[j], 127.0f), 0.65f);  // core.py:54-57
+    float nrm = __fsqrt_rn(quad_sumsq(d, qm));
+    if (nrm == 0.0f) nrm = 1.0f;  // zero rows stay zero (core.py:69-74)
+    float u[8];
 #pragma unroll
-    for (int j = 0; j < kEmbed; ++j) u[j] = __fdiv_rn(d[j], nrm);
-    float4* dst = reinterpret_cast<float4*>(st.tok_unit + (size_t)i * kEmbed);
-#pragma unroll
-    for (int j = 0; j < kEmbed; j += 4) dst[j / 4] = make_float4(u[j], u[j + 1], u[j + 2], u[j + 3]);
+    for (int j = 0; j < 8; ++j) u[j] = __fdiv_rn(d[j], nrm);
+    float4* dst = reinterpret_cast<float4*>(st.tok_unit + (size_t)i * kEmbed + 8 * g);
+    dst[0] = make_float4(u[0], u[1], u[2], u[3]);
+    dst[1] = make_float4(u[4], u[5], u[6], u[7]);
     // fp16 image of the unit row, pre-tiled for the tensor-core NN scan
     // (kScanTile-token tiles, UMMA K-major no-swizzle B-operand layout,
-    // tav2_common.cuh), one bulk copy per tile
+    // tav2_common.cuh): this thread's 8 elements are one 16-byte chunk
     uint8_t* tile = reinterpret_cast<uint8_t*>(st.tok_img) + (size_t)(i / kScanTile) * kScanTileBytes +
-                    (i % kScanTile) * 16;
-#pragma unroll
-    for (int j = 0; j < kEmbed; j += 8) {
-      uint32_t h[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const __half2 p = __floats2half2_rn(u[j + 2 * e], u[j + 2 * e + 1]);
-        h[e] = *reinterpret_cast<const uint32_t*>(&p);
-      }
-      *reinterpret_cast<uint4*>(tile + (j / 8) * (kScanTile * 16)) = make_uint4(h[0], h[1], h[2], h[3]);
-    }
+                    (i % kScanTile) * 16 + g * (kScanTile * 16);
+    *reinterpret_cast<uint4*>(tile) = make_uint4(pack_h2(u[0], u[1]), pack_h2(u[2], u[3]), pack_h2(u[4], u[5]),
+                                                 pack_h2(u[6], u[7]));
     if (with_feat) {  // token part of Eq. 4 (encoder.py:171-187): [unit(q) | 0] + bits @ action + surface
-      float f[kDModel];
+      float f[16];
 #pragma unroll
-      for (int j = 0; j < kEmbed; ++j) {
-        f[j] = u[j];
-        f[kEmbed + j] = 0.0f;
+      for (int j = 0; j < 16; ++j) f[j] = 0.0f;
+      // features 0..31 = unit(q): thread g < 2 takes elements 16g..16g+15,
+      // held by threads 2g and 2g+1 (all four shuffle, g >= 2 discard)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float lo = __shfl_sync(qm, u[j], 2 * (g & 1), 4);
+        const float hi = __shfl_sync(qm, u[j], 2 * (g & 1) + 1, 4);
+        f[j] = g < 2 ? lo : 0.0f;
+        f[8 + j] = g < 2 ? hi : 0.0f;
       }
       const unsigned act = st.action[i];
-      float asum[kDModel];
+      float asum[16];
 #pragma unroll
-      for (int j = 0; j < kDModel; ++j) asum[j] = 0.0f;
+      for (int j = 0; j < 16; ++j) asum[j] = 0.0f;
       for (int b = 0; b < p.action_rows; ++b)
         if ((act >> b) & 1u) {
-          const float4* row = reinterpret_cast<const float4*>(p.action_table + b * kDModel);
+          const float4* row = reinterpret_cast<const float4*>(p.action_table + b * kDModel + 16 * g);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
+          for (int j = 0; j < 4; ++j) {
             const float4 v = __ldg(row + j);
             asum[4 * j] += v.x; asum[4 * j + 1] += v.y; asum[4 * j + 2] += v.z; asum[4 * j + 3] += v.w;
           }
         }
       const int surf = min((int)st.surface[i], 3);  // SURFACE_OTHER fold (encoder.py:178)
-      const float4* srow = reinterpret_cast<const float4*>(p.surface_table + surf * kDModel);
-      float4* fd = reinterpret_cast<float4*>(st.tok_feat + (size_t)i * kDModel);
+      const float4* srow = reinterpret_cast<const float4*>(p.surface_table + surf * kDModel + 16 * g);
+      float4* fd = reinterpret_cast<float4*>(st.tok_feat + (size_t)i * kDModel + 16 * g);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
+      for (int j = 0; j < 4; ++j) {
         const float4 sv = __ldg(srow + j);
         fd[j] = make_float4((f[4 * j] + asum[4 * j]) + sv.x, (f[4 * j + 1] + asum[4 * j + 1]) + sv.y,
                             (f[4 * j + 2] + asum[4 * j + 2]) + sv.z, (f[4 * j + 3] + asum[4 * j + 3]) + sv.w);
@@ -104,21 +117,15 @@ __global__ void __launch_bounds__(256) prep_kernel(Staged st, Params p, int with
     return;
   }
   i -= st.n_tok;
-  if (i < st.n_items) {
-    const float4* src = reinterpret_cast<const float4*>(st.cand + (size_t)i * kEmbed);
-    float c[kEmbed];
-#pragma unroll
-    for (int j = 0; j < kEmbed; j += 4) {
-      float4 v = src[j / 4];
-      c[j] = v.x; c[j + 1] = v.y; c[j + 2] = v.z; c[j + 3] = v.w;
-    }
-    float nrm = __fsqrt_rn(sumsq8(c));
+  if (i < st.n_items) {  // l2_normalize_rows of the candidates (nnsearch.py:313-320)
+    const float4* src = reinterpret_cast<const float4*>(st.cand + (size_t)i * kEmbed + 8 * g);
+    const float4 v0 = src[0], v1 = src[1];
+    const float c[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    float nrm = __fsqrt_rn(quad_sumsq(c, qm));
     if (nrm == 0.0f) nrm = 1.0f;
-    float4* dst = reinterpret_cast<float4*>(st.cand_unit + (size_t)i * kEmbed);
-#pragma unroll
-    for (int j = 0; j < kEmbed; j += 4)
-      dst[j / 4] = make_float4(__fdiv_rn(c[j], nrm), __fdiv_rn(c[j + 1], nrm),
-                               __fdiv_rn(c[j + 2], nrm), __fdiv_rn(c[j + 3], nrm));
+    float4* dst = reinterpret_cast<float4*>(st.cand_unit + (size_t)i * kEmbed + 8 * g);
+    dst[0] = make_float4(__fdiv_rn(c[0], nrm), __fdiv_rn(c[1], nrm), __fdiv_rn(c[2], nrm), __fdiv_rn(c[3], nrm));
+    dst[1] = make_float4(__fdiv_rn(c[4], nrm), __fdiv_rn(c[5], nrm), __fdiv_rn(c[6], nrm), __fdiv_rn(c[7], nrm));
   }
 }
 
@@ -128,7 +135,7 @@ cudaError_t launch_prep(const Staged& st, const Params* p, cudaStream_t s) {
   int n = st.n_tok + st.n_items;
   if (n == 0) return cudaSuccess;
   const Params pz{};
-  return launch_pdl(prep_kernel, dim3((n + 255) / 256), dim3(256), 0, s, st, p ? *p : pz, (int)(p != nullptr));
+  return launch_pdl(prep_kernel, dim3((4 * n + 255) / 256), dim3(256), 0, s, st, p ? *p : pz, (int)(p != nullptr));
 }
 
 }  // namespace tav2
