@@ -99,24 +99,35 @@ __device__ __forceinline__ void t3_split8_store(uint8_t* hi_dst, uint8_t* lo_dst
   *reinterpret_cast<uint4*>(lo_dst) = make_uint4(l[0], l[1], l[2], l[3]);
 }
 // pre-norm LayerNorm (encoder.py:196-200, biased variance, eps 1e-5)
+// (paired f32x2 arithmetic: FADD2 / FMUL2 / FFMA2 on sm_100)
 __device__ __forceinline__ void t3_layer_norm(const float* x, const float* g, const float* b, float* y) {
-  float s0 = 0.f, s1 = 0.f;
+  float2 s = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < kDModel; j += 4) {
+    s = __fadd2_rn(s, make_float2(x[j], x[j + 1]));
+    s1 = __fadd2_rn(s1, make_float2(x[j + 2], x[j + 3]));
+  }
+  const float mu = ((s.x + s.y) + (s1.x + s1.y)) * (1.0f / 64.0f);
+  const float2 nmu = make_float2(-mu, -mu);
+  float2 v = make_float2(0.f, 0.f), v1 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < kDModel; j += 4) {
+    const float2 c = __fadd2_rn(make_float2(x[j], x[j + 1]), nmu);
+    const float2 c1 = __fadd2_rn(make_float2(x[j + 2], x[j + 3]), nmu);
+    v = __ffma2_rn(c, c, v);
+    v1 = __ffma2_rn(c1, c1, v1);
+  }
+  const float rs = rsqrtf(((v.x + v.y) + (v1.x + v1.y)) * (1.0f / 64.0f) + kLnEps3);
+  const float2 rs2 = make_float2(rs, rs);
+  const float2* g2 = reinterpret_cast<const float2*>(g);
+  const float2* b2 = reinterpret_cast<const float2*>(b);
 #pragma unroll
   for (int j = 0; j < kDModel; j += 2) {
-    s0 += x[j];
-    s1 += x[j + 1];
+    const float2 c = __fmul2_rn(__fadd2_rn(make_float2(x[j], x[j + 1]), nmu), rs2);
+    const float2 o = __ffma2_rn(c, g2[j / 2], b2[j / 2]);
+    y[j] = o.x;
+    y[j + 1] = o.y;
   }
-  const float mu = (s0 + s1) * (1.0f / 64.0f);
-  float v0 = 0.f, v1 = 0.f;
-#pragma unroll
-  for (int j = 0; j < kDModel; j += 2) {
-    const float c0 = x[j] - mu, c1 = x[j + 1] - mu;
-    v0 = fmaf(c0, c0, v0);
-    v1 = fmaf(c1, c1, v1);
-  }
-  const float rs = rsqrtf((v0 + v1) * (1.0f / 64.0f) + kLnEps3);
-#pragma unroll
-  for (int j = 0; j < kDModel; ++j) y[j] = fmaf((x[j] - mu) * rs, g[j], b[j]);
 }
 
 // D += A(TMEM hi/lo) x B(smem hi/lo, K-major slabs), 3 terms per k-step
@@ -385,38 +396,55 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       float inv_l = 0.0f;
       {
         mbar_wait_sleep(&t3.kvready, n_kv & 1);  // kmax_s[L] complete (already passed)
+        stamp(24);
         const float mb = sqrtf(qn2 * __uint_as_float(kmax_s[L]));
         const uint32_t cs = lanebase + kCD;
         const int nch = NK / 16;
         const int jlast = min(nch - 1, (rpw * kb + rpw - 1) / 16);  // warp-uniform causal bound
-        float l = 0.0f;
-        for (int j0 = 0; j0 < nch; j0 += 2) {
-          uint32_t s32[32];
-#pragma unroll
-          for (int u = 0; u < 2; ++u)
-            if (j0 + u <= jlast) tmem_ld16(cs + 16 * (j0 + u), s32 + 16 * u);  // warp-uniform
-          tmem_ld_wait();
+        const float2 nmb = make_float2(-mb, -mb);
+        float2 l2 = make_float2(0.f, 0.f);
+        // the causal chunks, one at a time with the next chunk's TMEM load in
+        // flight while this one is exponentiated (2-deep software pipeline)
+        uint32_t sa[16], sb[16];
+        tmem_ld16(cs, sa);
+        for (int j = 0; j <= jlast; j += 2) {
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            const int j = j0 + u;
-            if (j >= nch) break;
-            uint32_t hi[8], lo[8];
-            uint32_t vm = 0u;
-            if (ok && j <= jlast) vm = allowed16(valid_w[j >> 1] >> ((j & 1) * 16), 16 * j, r);
+            const int jj = j + u;
+            if (jj > jlast) break;
+            tmem_ld_wait();
+            uint32_t* cur = u == 0 ? sa : sb;
+            uint32_t* nxt = u == 0 ? sb : sa;
+            if (jj + 1 <= jlast) tmem_ld16(cs + 16 * (jj + 1), nxt);  // warp-uniform
+            const uint32_t vm = ok ? allowed16(valid_w[jj >> 1] >> ((jj & 1) * 16), 16 * jj, r) : 0u;
             float pv[16];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              float pe;
-              asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(pe) : "f"(__uint_as_float(s32[16 * u + e]) - mb));
-              pv[e] = ((vm >> e) & 1u) ? pe : 0.0f;
-              l += pv[e];
+            for (int e = 0; e < 16; e += 2) {  // p = exp2(s - m'), masked keys -> 0
+              const float2 d = __fadd2_rn(make_float2(__uint_as_float(cur[e]), __uint_as_float(cur[e + 1])), nmb);
+              float p0, p1;
+              asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p0) : "f"(d.x));
+              asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p1) : "f"(d.y));
+              pv[e] = ((vm >> e) & 1u) ? p0 : 0.0f;
+              pv[e + 1] = ((vm >> (e + 1)) & 1u) ? p1 : 0.0f;
+              l2 = __fadd2_rn(l2, make_float2(pv[e], pv[e + 1]));
             }
+            uint32_t hi[8], lo[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) split_pair(pv[2 * i], pv[2 * i + 1], hi[i], lo[i]);
-            tmem_st8(cs + 16 * j, hi);
-            tmem_st8(cs + 16 * j + 8, lo);
+            for (int i = 0; i < 8; ++i) split_pair_t(pv[2 * i], pv[2 * i + 1], hi[i], lo[i]);
+            tmem_st8(cs + 16 * jj, hi);
+            tmem_st8(cs + 16 * jj + 8, lo);
           }
         }
+        stamp(25);
+        {  // chunks past the warp's causal bound: P = 0 (the P.V MMA reads all NK keys)
+          const uint32_t z[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+          for (int j = jlast + 1; j < nch; ++j) {
+            tmem_st8(cs + 16 * j, z);
+            tmem_st8(cs + 16 * j + 8, z);
+          }
+        }
+        const float l = l2.x + l2.y;
+        stamp(26);
         inv_l = l > 0.0f ? 1.0f / l : 0.0f;  // a valid row always sees itself
         tmem_st_wait();
         done();
@@ -445,7 +473,11 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         t3_ld64(cA, d);
         if (ok) {
 #pragma unroll
-          for (int j = 0; j < kDModel; ++j) x[j] = fmaf(d[j], inv_l, x[j]);
+          for (int j = 0; j < kDModel; j += 2) {
+            const float2 o = __ffma2_rn(make_float2(d[j], d[j + 1]), make_float2(inv_l, inv_l), make_float2(x[j], x[j + 1]));
+            x[j] = o.x;
+            x[j + 1] = o.y;
+          }
         }
         t3_layer_norm(x, lnp_s[L][2], lnp_s[L][3], d);
         if (!ok) {
@@ -491,7 +523,11 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         t3_ld64(lanebase + kCW2, d);
         if (ok) {
 #pragma unroll
-          for (int j = 0; j < kDModel; ++j) x[j] += d[j];
+          for (int j = 0; j < kDModel; j += 2) {
+            const float2 o = __fadd2_rn(make_float2(d[j], d[j + 1]), make_float2(x[j], x[j + 1]));
+            x[j] = o.x;
+            x[j + 1] = o.y;
+          }
         }
       }
       stamp(18);

@@ -62,6 +62,17 @@ __device__ __forceinline__ void split_pair_h(float a, float b, uint32_t& hi, uin
   const float2 hf = __half22float2(h);
   lo = pack_half2(a - hf.x, b - hf.y);
 }
+// Truncating split on the integer pipes (no F2F conversions): hi = x with
+// the low 16 bits cleared (bf16 truncation), lo = the exact f32 residual
+// x - hi truncated the same way; |x - hi - lo| < 2^-14 |x| (round-to-nearest
+// split: 2^-16).  Two floats -> packed (hi pair, lo pair).
+__device__ __forceinline__ void split_pair_t(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
+  hi = __byte_perm(ua, ub, 0x7632);  // upper halves: .x (low) = a
+  const float2 h = make_float2(__uint_as_float(ua & 0xffff0000u), __uint_as_float(ub & 0xffff0000u));
+  const float2 r = __ffma2_rn(h, make_float2(-1.0f, -1.0f), make_float2(a, b));  // exact residuals
+  lo = __byte_perm(__float_as_uint(r.x), __float_as_uint(r.y), 0x7632);
+}
 // kind::i8 with signed int8 A/B, s32 accumulate.
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
@@ -238,12 +249,14 @@ __device__ __forceinline__ uint32_t pack2(__nv_bfloat16 a, __nv_bfloat16 b) {
   return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
 }
 // split a pair of floats into packed (hi pair, lo pair): two paired
-// round-to-nearest conversions (cvt.rn.bf16x2.f32), two subtractions
+// round-to-nearest conversions (cvt.rn.bf16x2.f32) and one paired f32x2
+// subtraction (sm_100 FFMA2)
 __device__ __forceinline__ void split_pair(float a, float b, uint32_t& hi, uint32_t& lo) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);  // .x (low half) = a
   hi = *reinterpret_cast<const uint32_t*>(&h);
-  const float ah = __uint_as_float(hi << 16), bh = __uint_as_float(hi & 0xffff0000u);
-  const __nv_bfloat162 l = __floats2bfloat162_rn(a - ah, b - bh);
+  const float2 hf = make_float2(__uint_as_float(hi << 16), __uint_as_float(hi & 0xffff0000u));
+  const float2 d = __ffma2_rn(hf, make_float2(-1.0f, -1.0f), make_float2(a, b));  // exact: a - bf16(a)
+  const __nv_bfloat162 l = __floats2bfloat162_rn(d.x, d.y);
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
