@@ -254,21 +254,32 @@ def run_gpu(args, rank, world, local_rank):
     value = world * cand_step * args.steps / (max_ms / 1e3)
 
     # ---- end-to-end through the public API (host buffers, H2D + D2H inside) ----
-    for i in range(args.warmup):
-        eng.rank_requests(packed[i % pool_n], mode=mode)
+    # (a) the serving loop Engine.rank_pipelined: every step's host packing,
+    #     H2D copy, kernels and D2H of the logits, with step i+1's host work
+    #     and H2D overlapping step i's kernels (two staging slots);
+    # (b) the synchronous Engine.rank_requests, one request at a time.
+    eng.rank_pipelined([packed[i % pool_n] for i in range(args.warmup)], mode=mode)
     barrier()
     torch.cuda.synchronize()
     lat = []
     t0 = time.perf_counter()
-    for i in range(args.steps):
-        ts = time.perf_counter()
-        eng.rank_requests(packed[i % pool_n], mode=mode)
-        lat.append(time.perf_counter() - ts)
+    eng.rank_pipelined([packed[i % pool_n] for i in range(args.steps)], mode=mode, latencies=lat)
     e2e_s = time.perf_counter() - t0
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * cand_step * args.steps / float(te.item())
+    for i in range(min(args.warmup, 5)):
+        eng.rank_requests(packed[i % pool_n], mode=mode)
+    torch.cuda.synchronize()
+    lat_sync = []
+    n_sync = min(args.steps, 100)
+    ts0 = time.perf_counter()
+    for i in range(n_sync):
+        ts = time.perf_counter()
+        eng.rank_requests(packed[i % pool_n], mode=mode)
+        lat_sync.append(time.perf_counter() - ts)
+    sync_value = cand_step * n_sync / (time.perf_counter() - ts0)
     h2d = _staged_bytes(packed[0])
     d2h = cand_step * 4 * 4
 
@@ -308,9 +319,12 @@ def run_gpu(args, rank, world, local_rank):
         "p50_request_ms": round(nearest_rank(step_ms, 50), 4),
         "p99_request_ms": round(nearest_rank(step_ms, 99), 4),
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h,
+                "d2h_bytes_per_step": d2h, "api": "Engine.rank_pipelined (tav2_rank_submit/collect)",
                 "p50_request_ms": round(1e3 * nearest_rank(lat, 50), 4),
-                "p99_request_ms": round(1e3 * nearest_rank(lat, 99), 4)},
+                "p99_request_ms": round(1e3 * nearest_rank(lat, 99), 4),
+                "sync": {"value": round(sync_value, 1), "api": "Engine.rank_requests (tav2_rank)",
+                         "p50_request_ms": round(1e3 * nearest_rank(lat_sync, 50), 4),
+                         "p99_request_ms": round(1e3 * nearest_rank(lat_sync, 99), 4)}},
         "gpu_launches": launches_per_step * args.steps,
         "kernels": {k: {"ms_per_launch": round(v[0] / max(v[1], 1), 4), "launches": v[1]} for k, v in kt.items()},
         "roofline": roof,

@@ -119,6 +119,20 @@ int tav2_score(tav2_ctx* ctx, int mode, const int32_t* idx_dev, float* logits_de
 int tav2_rank(tav2_ctx* ctx, const tav2_request* reqs, int n_req, int mode, float* logits_host,
               int32_t* idx_host, void* stream);
 
+/* Pipelined rank (the serving loop): stage + nn_select + score + result
+ * copies are enqueued without waiting, into one of two staging slots, so the
+ * host packing and H2D copy of the next request overlap the kernels of the
+ * current one.  Returns the slot in *slot_out; at most two submits may be in
+ * flight: collect a slot before submitting into it again (submit blocks until
+ * the slot's previous rank finished).  want_idx: also copy the NN indices
+ * (NN-feature logging). */
+int tav2_rank_submit(tav2_ctx* ctx, const tav2_request* reqs, int n_req, int mode, int want_idx,
+                     void* stream, int32_t* slot_out);
+
+/* Wait for a submitted rank and copy its results out: logits_host
+ * [n_items, 4] f32, idx_host (nullable, requires want_idx) [n_items, seq_len]. */
+int tav2_rank_collect(tav2_ctx* ctx, int slot, float* logits_host, int32_t* idx_host);
+
 /* Device-resident variant used by the throughput benchmark: nn_select +
  * score on the currently staged batch, no host traffic. */
 int tav2_run_staged(tav2_ctx* ctx, int mode, float* logits_dev, void* stream);

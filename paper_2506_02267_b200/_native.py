@@ -28,6 +28,7 @@ EXPORTS = (
     "tav2_encode", "tav2_forward", "tav2_score", "tav2_rank", "tav2_run_staged",
     "tav2_last_launch_count", "tav2_last_error", "tav2_build_info", "tav2_set_profiling",
     "tav2_kernel_times", "tav2_tc_selftest", "tav2_debug_timeline", "tav2_debug_cta",
+    "tav2_rank_submit", "tav2_rank_collect",
 )
 
 
@@ -87,6 +88,9 @@ def lib() -> ctypes.CDLL:
             L.tav2_rank.argtypes = [vp, ctypes.POINTER(Request), ctypes.c_int, ctypes.c_int, vp, vp,
                                     vp]
             L.tav2_run_staged.argtypes = [vp, ctypes.c_int, vp, vp]
+            L.tav2_rank_submit.argtypes = [vp, ctypes.POINTER(Request), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                           vp, ctypes.POINTER(i32)]
+            L.tav2_rank_collect.argtypes = [vp, ctypes.c_int, vp, vp]
             L.tav2_last_launch_count.argtypes = [vp]
             L.tav2_set_profiling.argtypes = [vp, ctypes.c_int]
             L.tav2_kernel_times.argtypes = [vp, ctypes.POINTER(ctypes.c_char_p),

@@ -65,11 +65,26 @@ struct tav2_ctx {
   int max_tiles = 0, max_work = 0;
   int sms = 148;
 
-  // pinned host arena + device mirror of the staged region
-  unsigned char* h_arena = nullptr;
-  unsigned char* d_staged = nullptr;
+  // Two staging slots (pinned host arena + device mirror of the staged
+  // region each), so the host packing and H2D copy of the next batch overlap
+  // the kernels of the current one (tav2_rank_submit).  H2D copies run on
+  // copy_stream; ev_staged[s]: slot s's copy done (host arena reusable, the
+  // compute stream may read it); ev_done[s]: the kernels (and result copies)
+  // of slot s done (device region and pinned outputs reusable).
+  static constexpr int kStageSlots = 2;
+  unsigned char* h_arena[kStageSlots] = {nullptr, nullptr};
+  unsigned char* d_staged[kStageSlots] = {nullptr, nullptr};
   int64_t staged_cap = 0;
-  cudaEvent_t ev_staged = nullptr;
+  cudaEvent_t ev_staged[kStageSlots] = {nullptr, nullptr};
+  cudaEvent_t ev_done[kStageSlots] = {nullptr, nullptr};
+  cudaStream_t copy_stream = nullptr;
+  Plan plans[kStageSlots]{};
+  int cur = 0;        // slot of the current staged batch
+  int next_slot = 0;  // slot the next stage uses
+  float* h_out[kStageSlots] = {nullptr, nullptr};     // pinned logits of a submitted rank
+  int32_t* h_idx[kStageSlots] = {nullptr, nullptr};   // pinned NN indices (optional)
+  int out_n[kStageSlots] = {0, 0};
+  bool out_idx[kStageSlots] = {false, false};
   // derived device buffers
   float* tok_unit = nullptr;
   uint32_t* tok_img = nullptr;
@@ -88,8 +103,7 @@ struct tav2_ctx {
   uint8_t* d_images3 = nullptr;  // folded images of skut_tc3 (Wqk, Wvo)
   SkutImages3 images3{};
   bool params_ok = false;
-  // current batch
-  Plan plan{};
+  // current batch: plans[cur]
   bool staged = false;
   int launches = 0;
   // per-kernel profiling (CUDA events on the launch stream)
@@ -109,8 +123,8 @@ namespace {
 
 Staged staged_view(tav2_ctx* c) {
   Staged s{};
-  const Plan& p = c->plan;
-  unsigned char* b = c->d_staged;
+  const Plan& p = c->plans[c->cur];
+  unsigned char* b = c->d_staged[c->cur];
   s.req = reinterpret_cast<const ReqInfo*>(b + p.off_req);
   s.tiles = reinterpret_cast<const NNTile*>(b + p.off_tiles);
   s.work = reinterpret_cast<const NNWork*>(b + p.off_work);
@@ -147,8 +161,15 @@ int64_t staged_bytes(int R, int N, int64_t T, int tiles, int work) {
 }
 
 int free_all(tav2_ctx* c) {
-  cudaFreeHost(c->h_arena);
-  cudaFree(c->d_staged);
+  for (int k = 0; k < tav2_ctx::kStageSlots; ++k) {
+    cudaFreeHost(c->h_arena[k]);
+    cudaFree(c->d_staged[k]);
+    cudaFreeHost(c->h_out[k]);
+    cudaFreeHost(c->h_idx[k]);
+    if (c->ev_staged[k]) cudaEventDestroy(c->ev_staged[k]);
+    if (c->ev_done[k]) cudaEventDestroy(c->ev_done[k]);
+  }
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   cudaFree(c->tok_unit);
   cudaFree(c->tok_img);
   cudaFree(c->cand_unit);
@@ -163,7 +184,6 @@ int free_all(tav2_ctx* c) {
   cudaFree(c->skut_scratch);
   cudaFree(c->d_params);
   cudaFree(c->d_images);
-  if (c->ev_staged) cudaEventDestroy(c->ev_staged);
   for (auto& sl : c->slots) {
     if (sl.a) cudaEventDestroy(sl.a);
     if (sl.b) cudaEventDestroy(sl.b);
@@ -268,8 +288,16 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
   };
   cudaError_t e;
   if ((e = cudaSetDevice(device)) != cudaSuccess) return bad(e, "cudaSetDevice");
-  if ((e = cudaMallocHost(&c->h_arena, c->staged_cap)) != cudaSuccess) return bad(e, "pinned arena");
-  if ((e = cudaMalloc(&c->d_staged, c->staged_cap)) != cudaSuccess) return bad(e, "staged region");
+  for (int k = 0; k < tav2_ctx::kStageSlots; ++k) {
+    if ((e = cudaMallocHost(&c->h_arena[k], c->staged_cap)) != cudaSuccess) return bad(e, "pinned arena");
+    if ((e = cudaMalloc(&c->d_staged[k], c->staged_cap)) != cudaSuccess) return bad(e, "staged region");
+    if ((e = cudaMallocHost(&c->h_out[k], (size_t)N * kHeads * 4)) != cudaSuccess) return bad(e, "pinned logits");
+    if ((e = cudaMallocHost(&c->h_idx[k], (size_t)N * S * 4)) != cudaSuccess) return bad(e, "pinned indices");
+    if ((e = cudaEventCreateWithFlags(&c->ev_staged[k], cudaEventDisableTiming)) != cudaSuccess) return bad(e, "event");
+    if ((e = cudaEventCreateWithFlags(&c->ev_done[k], cudaEventDisableTiming)) != cudaSuccess) return bad(e, "event");
+  }
+  if ((e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return bad(e, "copy stream");
   // padded to whole 64-token tiles (+1): the NN kernel bulk-copies full tiles
   if ((e = cudaMalloc(&c->tok_unit, (size_t)(cdiv((int)std::max<int64_t>(T, 1), 64) + 1) * 64 * kEmbed * 4)) !=
       cudaSuccess)
@@ -299,8 +327,6 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
     size_t n = (size_t)sms * skut_simt_scratch_floats(S);
     if ((e = cudaMalloc(&c->skut_scratch, n * 4)) != cudaSuccess) return bad(e, "skut scratch");
   }
-  if ((e = cudaEventCreateWithFlags(&c->ev_staged, cudaEventDisableTiming)) != cudaSuccess)
-    return bad(e, "event");
   *out = c;
   return TAV2_OK;
 }
@@ -587,10 +613,11 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
   p.off_emb = o; o = align256(o + T * kEmbed);
   p.bytes = o;
 
-  // The arena is reused: the previous batch's H2D copy must have drained
+  // The slot's arena is reused: its previous H2D copy must have drained
   // before we overwrite it (arena reset contract, arena.py:49-55).
-  CU(cudaEventSynchronize(c->ev_staged));
-  unsigned char* h = c->h_arena;
+  const int slot = c->next_slot;
+  CU(cudaEventSynchronize(c->ev_staged[slot]));
+  unsigned char* h = c->h_arena[slot];
   ReqInfo* ri = reinterpret_cast<ReqInfo*>(h + p.off_req);
   int32_t* item_req = reinterpret_cast<int32_t*>(h + p.off_item_req);
   float* ctx = reinterpret_cast<float*>(h + p.off_ctx);
@@ -628,9 +655,14 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
   if (!vw.empty()) memcpy(h + p.off_work, vw.data(), vw.size() * sizeof(NNWork));
 
   CU(cudaSetDevice(c->device));
-  CU(cudaMemcpyAsync(c->d_staged, h, p.bytes, cudaMemcpyHostToDevice, s));
-  CU(cudaEventRecord(c->ev_staged, s));
-  c->plan = p;
+  // the device region is rewritten once the kernels that read it last finished
+  CU(cudaStreamWaitEvent(c->copy_stream, c->ev_done[slot], 0));
+  CU(cudaMemcpyAsync(c->d_staged[slot], h, p.bytes, cudaMemcpyHostToDevice, c->copy_stream));
+  CU(cudaEventRecord(c->ev_staged[slot], c->copy_stream));
+  CU(cudaStreamWaitEvent(s, c->ev_staged[slot], 0));
+  c->plans[slot] = p;
+  c->cur = slot;
+  c->next_slot = slot ^ 1;
   c->staged = true;
   if (n_items) *n_items = N;
   return TAV2_OK;
@@ -639,6 +671,13 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
 }  // extern "C"
 
 namespace {
+
+// the staged slot's kernels are enqueued: its device region may be rewritten
+// (by a later stage of the same slot) once they finish
+int mark_used(tav2_ctx* c, cudaStream_t s) {
+  CU(cudaEventRecord(c->ev_done[c->cur], s));
+  return TAV2_OK;
+}
 
 int check_ready(tav2_ctx* c, int mode) {
   if (!c) return fail(TAV2_EINVAL, "null context");
@@ -697,7 +736,8 @@ int tav2_nn_select(tav2_ctx* c, int mode, int32_t* idx_dev, float* scores_dev, v
   if (!idx_dev) return fail(TAV2_EINVAL, "idx_dev is null");
   CU(cudaSetDevice(c->device));
   c->launches = 0;
-  return run_nn(c, idx_dev, scores_dev, (cudaStream_t)stream);
+  int rc2 = run_nn(c, idx_dev, scores_dev, (cudaStream_t)stream);
+  return rc2 ? rc2 : mark_used(c, (cudaStream_t)stream);
 }
 
 int tav2_encode(tav2_ctx* c, const int32_t* idx_dev, float* features_dev, uint8_t* mask_dev,
@@ -710,7 +750,7 @@ int tav2_encode(tav2_ctx* c, const int32_t* idx_dev, float* features_dev, uint8_
   Staged st = staged_view(c);
   CU(launch_prep(st, nullptr, (cudaStream_t)stream));
   CU(launch_encode(st, c->nn, c->params, idx_dev, features_dev, mask_dev, (cudaStream_t)stream));
-  return TAV2_OK;
+  return mark_used(c, (cudaStream_t)stream);
 }
 
 int tav2_forward(tav2_ctx* c, int mode, const float* features_dev, const uint8_t* mask_dev,
@@ -742,7 +782,8 @@ int tav2_score(tav2_ctx* c, int mode, const int32_t* idx_dev, float* logits_dev,
   c->launches = 0;
   Staged st = staged_view(c);
   CU(timed(c, "prep", (cudaStream_t)stream, [&] { return launch_prep(st, &c->params, (cudaStream_t)stream); }));
-  return run_score(c, mode, idx_dev, logits_dev, pooled_dev, (cudaStream_t)stream);
+  rc = run_score(c, mode, idx_dev, logits_dev, pooled_dev, (cudaStream_t)stream);
+  return rc ? rc : mark_used(c, (cudaStream_t)stream);
 }
 
 int tav2_run_staged(tav2_ctx* c, int mode, float* logits_dev, void* stream) {
@@ -752,7 +793,42 @@ int tav2_run_staged(tav2_ctx* c, int mode, float* logits_dev, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   c->launches = 0;
   if ((rc = run_nn(c, c->idx, nullptr, s))) return rc;
-  return run_score(c, mode, c->idx, logits_dev ? logits_dev : c->logits, nullptr, s);
+  if ((rc = run_score(c, mode, c->idx, logits_dev ? logits_dev : c->logits, nullptr, s))) return rc;
+  return mark_used(c, s);
+}
+
+int tav2_rank_submit(tav2_ctx* c, const tav2_request* reqs, int n_req, int mode, int want_idx, void* stream,
+                     int32_t* slot_out) {
+  if (!c || !slot_out) return fail(TAV2_EINVAL, "null argument");
+  const int slot = c->next_slot;
+  // the slot's pinned outputs are free once its previous rank finished
+  CU(cudaEventSynchronize(c->ev_done[slot]));
+  int32_t n = 0;
+  int rc = tav2_stage(c, reqs, n_req, stream, &n);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((rc = run_nn(c, c->idx, nullptr, s))) return rc;
+  if ((rc = run_score(c, mode, c->idx, c->logits, nullptr, s))) return rc;
+  CU(cudaMemcpyAsync(c->h_out[slot], c->logits, (size_t)n * kHeads * 4, cudaMemcpyDeviceToHost, s));
+  if (want_idx)
+    CU(cudaMemcpyAsync(c->h_idx[slot], c->idx, (size_t)n * c->nn.seq_len * 4, cudaMemcpyDeviceToHost, s));
+  c->out_n[slot] = n;
+  c->out_idx[slot] = want_idx != 0;
+  if ((rc = mark_used(c, s))) return rc;
+  *slot_out = slot;
+  return TAV2_OK;
+}
+
+int tav2_rank_collect(tav2_ctx* c, int slot, float* logits_host, int32_t* idx_host) {
+  if (!c || slot < 0 || slot >= tav2_ctx::kStageSlots) return fail(TAV2_EINVAL, "bad slot");
+  if (!logits_host) return fail(TAV2_EINVAL, "logits_host is null");
+  CU(cudaEventSynchronize(c->ev_done[slot]));
+  memcpy(logits_host, c->h_out[slot], (size_t)c->out_n[slot] * kHeads * 4);
+  if (idx_host) {
+    if (!c->out_idx[slot]) return fail(TAV2_ESTATE, "indices were not requested at submit");
+    memcpy(idx_host, c->h_idx[slot], (size_t)c->out_n[slot] * c->nn.seq_len * 4);
+  }
+  return TAV2_OK;
 }
 
 int tav2_rank(tav2_ctx* c, const tav2_request* reqs, int n_req, int mode, float* logits_host,

@@ -9,6 +9,7 @@ compute runs in ``libtav2.so``; there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -216,6 +217,44 @@ class Engine:
         N.check(self._lib.tav2_rank(self._ctx, pack.arr, len(requests), self._mode(mode),
                                     logits.ctypes.data, N.ptr(idx), self.stream()))
         return (logits, idx) if return_indices else logits
+
+    def rank_pipelined(self, batches, mode: str = "bf16", return_indices: bool = False,
+                       latencies: list | None = None):
+        """Serving loop (tav2_rank_submit / tav2_rank_collect): every batch of
+        (user, candidates, ctx) requests is submitted -- host packing into one
+        of two pinned staging slots, H2D copy, kernels and result copies all
+        enqueued -- before the previous batch is collected, so the host work
+        and H2D of batch i+1 overlap the kernels of batch i.  Returns the list
+        of logits arrays (with indices if requested) in batch order;
+        `latencies` (optional list) receives each batch's submit-to-collect
+        wall time in seconds."""
+        if self.model is None:
+            raise ValidationError("no model loaded")
+        mode_i = self._mode(mode)
+        out, pending = [], None
+
+        def collect(p):
+            slot, n, _pack, t0 = p
+            logits = np.empty((n, 4), np.float32)
+            idx = np.empty((n, self.config.nn.seq_len), np.int32) if return_indices else None
+            N.check(self._lib.tav2_rank_collect(self._ctx, slot, logits.ctypes.data, N.ptr(idx)))
+            if latencies is not None:
+                latencies.append(time.perf_counter() - t0)
+            out.append((logits, idx) if return_indices else logits)
+
+        for reqs in batches:
+            t0 = time.perf_counter()
+            pack = _Pack(reqs)
+            n = sum(len(c) for _, c, _ in reqs)
+            slot = ctypes.c_int32()
+            N.check(self._lib.tav2_rank_submit(self._ctx, pack.arr, len(reqs), mode_i, int(return_indices),
+                                               self.stream(), ctypes.byref(slot)))
+            if pending is not None:
+                collect(pending)
+            pending = (slot.value, n, pack, t0)
+        if pending is not None:
+            collect(pending)
+        return out
 
     def run_staged(self, mode: str, logits: torch.Tensor | None = None) -> None:
         """Device-resident path (bench ``value``): NN + score on the staged batch."""

@@ -229,3 +229,20 @@ def test_full_size_degenerate_ties(cfg):
     assert np.array_equal(idx[0, a:b], ref_idx[0, a:b])
     assert np.array_equal(idx[1, a:b], ref_idx[1, a:b])
     assert np.abs(logits - lg).max() <= TOL["bf16"]
+
+
+def test_pipelined_serving_loop_matches_sync():
+    """tav2_rank_submit / tav2_rank_collect (two staging slots, host packing
+    and H2D of batch i+1 overlapping batch i) returns exactly the synchronous
+    rank's logits and indices, batch by batch."""
+    nn = P.NNConfig()
+    eng = _engine_for(nn, cap=Capacity(2, 300, 2 * 6000))
+    batches = [[(r.user, r.candidates, r.ctx) for r in P.generate_requests(2, 60 + 17 * i, ll_tokens=3000 + 500 * i,
+                                                                           seed=40 + i)] for i in range(5)]
+    lat = []
+    piped = eng.rank_pipelined(batches, mode="bf16", return_indices=True, latencies=lat)
+    assert len(piped) == 5 and len(lat) == 5
+    for b, (lg, idx) in zip(batches, piped):
+        lg_s, idx_s = eng.rank_requests(b, mode="bf16", return_indices=True)
+        assert np.array_equal(idx, idx_s)
+        assert np.array_equal(lg, lg_s)
