@@ -200,6 +200,11 @@ def run_case(name, reqs, nn_cfg, seed=0):
         seg_valid=np.array([[g.valid for g in s.segments] for s in seqs], np.int32),
         features_head=F[:4].astype(np.float32), U_head=U[:4].astype(np.float32),
     )
+    # NN-feature logging records: the reference's own
+    # pack_assembled bytes of every assembled sequence (dataset.py:138-149)
+    packed = [rdata.pack_assembled(sq) for sq in seqs]
+    arrays["packed_assembled"] = np.frombuffer(b"".join(packed), np.uint8)
+    arrays["packed_offsets"] = np.cumsum([0] + [len(b) for b in packed]).astype(np.int64)
     for r_i, (_, user, _) in enumerate(reqs):
         for src, blk in (("ll", user.lifelong), ("rt", user.realtime), ("imp", user.impression)):
             arrays[f"r{r_i}_{src}_emb"] = blk.embeddings

@@ -91,3 +91,41 @@ def generate_requests(num_requests: int, n_candidates: int, ll_tokens: int = 163
         cands = np.where(is_near[:, None], near(n_candidates), far(n_candidates)).astype(np.float32)
         out.append(SyntheticRequest(uid, user, np.ascontiguousarray(cands), context_features(uid)))
     return out
+
+
+# ---------------------------------------------------------------------------
+# NN-feature logging (training-serving alignment): the
+# assembled sequence a request was scored with, serialised in the reference's
+# record format (dataset.py:49-66 token records, :138-149 assembled block) so
+# the logged bytes equal what the reference's own logger would write.
+# ---------------------------------------------------------------------------
+
+def token_record_dtype(embed_dim: int = 32) -> np.dtype:
+    """One token on the wire: u32 ts, u16 action, u8 surface, embed_dim x i8."""
+    return np.dtype([("ts", "<u4"), ("action", "<u2"), ("surface", "u1"), ("emb", "i1", (embed_dim,))])
+
+
+def pack_token_block(block) -> bytes:
+    rec = np.empty(len(block), dtype=token_record_dtype(block.embeddings.shape[1]))
+    rec["ts"], rec["action"], rec["surface"], rec["emb"] = (block.timestamps, block.actions, block.surfaces,
+                                                            block.embeddings)
+    return rec.tobytes()
+
+
+def pack_assembled(seq) -> bytes:
+    """<HBB> (sequence length, embed dim, segment count), one <HH> (configured
+    length, valid count) per segment, then the padded token records."""
+    import struct
+
+    head = struct.pack("<HBB", len(seq), seq.block.embeddings.shape[1], len(seq.segments))
+    segs = b"".join(struct.pack("<HH", g.stop - g.start, g.valid) for g in seq.segments)
+    return head + segs + pack_token_block(seq.block)
+
+
+def log_nn_features(users, idx: np.ndarray, offsets, cfg) -> list[bytes]:
+    """Logged records of a ranked batch: `idx` [n_items, seq_len] from
+    Engine.rank_requests(..., return_indices=True) / tav2_rank(idx_host),
+    `offsets[i]` the request index of item i."""
+    from .nnsearch import assembled_from_indices
+
+    return [pack_assembled(assembled_from_indices(users[o], idx[i], cfg)) for i, o in enumerate(offsets)]

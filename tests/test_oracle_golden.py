@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 from conftest import golden_cases, load_case
+from helpers import to_user
 from oracle import seqrank_oracle as orc
 
 CASES = golden_cases()
@@ -71,3 +72,20 @@ def test_topk_spec_examples():
     assert picked.tolist() == [0, 2, 1]
     picked, _ = orc._topk_desc_storage(np.array([0.3, 0.3]), 1)
     assert picked.tolist() == [0]
+
+
+@pytest.mark.parametrize("case", golden_cases())
+def test_nn_feature_log_bytes_match_reference(case):
+    """The package's record packer over the reference layout reproduces the
+    reference's own pack_assembled bytes (dataset.py:138-149)."""
+    import paper_2506_02267_b200 as P
+    from paper_2506_02267_b200.dataset import log_nn_features
+
+    z, reqs = load_case(case)
+    nn = P.NNConfig(*[int(v) for v in z["cfg"]])
+    users = [to_user(r["user"]) for r in reqs]
+    recs = log_nn_features(users, z["idx"], z["offsets"], nn)
+    blob, off = z["packed_assembled"].tobytes(), z["packed_offsets"]
+    assert len(recs) == len(off) - 1
+    for i, rec in enumerate(recs):
+        assert rec == blob[off[i]:off[i + 1]], f"{case}: record {i} differs"
