@@ -22,7 +22,7 @@ int tav2_tc_selftest(int which, const void* A, const void* B, void* D, int N, in
  * thread-safe. */
 int tav2_debug_timeline(long long* dev, int block);
 
-/* Debug (libtav2_debug.so only): device buffer (>= 7 * 3 * 4096 int64)
+/* Debug (libtav2_debug.so only): device buffer (>= 8 * 3 * 4096 int64)
  * receiving per-CTA %globaltimer stamps of every ranking-path kernel
  * ([kernel][start | end | inputs ready][CTA]; kernels: prep, nn_scan pass 1,
  * nn_bound, nn_scan pass 2, nn_select, skut) and, at kernel 6, per

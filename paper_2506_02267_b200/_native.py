@@ -16,7 +16,9 @@ from .core import ValidationError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 # TAV2_DEBUG=1 selects the timeline-instrumented build (tools/*_timeline.py)
+# TAV2_LIB=x selects an A/B experiment build libtav2_x.so (build.build(variant=...))
 LIB_PATH = os.path.join(HERE, "_lib", "libtav2_debug.so" if os.environ.get("TAV2_DEBUG") == "1"
+                        else f"libtav2_{os.environ['TAV2_LIB']}.so" if os.environ.get("TAV2_LIB")
                         else "libtav2.so")
 
 TAV2_OK, TAV2_EINVAL, TAV2_ECUDA, TAV2_ECAP, TAV2_ESTATE = 0, 1, 2, 3, 4

@@ -36,13 +36,19 @@ def _digest(extra: list[str]) -> str:
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug: bool = False,
+          variant: str | None = None, defines: tuple[str, ...] = ()) -> str:
     """Compile every .cu under csrc/ into one shared library (parallel).
     debug=True builds libtav2_debug.so with the timeline stamps compiled in
-    (tools/*_timeline.py; select it with TAV2_DEBUG=1)."""
+    (tools/*_timeline.py; select it with TAV2_DEBUG=1).  variant="x" with
+    defines=("-DFOO",) builds libtav2_x.so for A/B experiments (select it
+    with TAV2_LIB=x)."""
     os.makedirs(LIBDIR, exist_ok=True)
     lib = LIB_DEBUG if debug else LIB
     extra = (["-DTAV2_DEBUG=1"] + os.environ.get("TAV2_EXTRA_FLAGS", "").split()) if debug else []
+    if variant:
+        lib = os.path.join(LIBDIR, f"libtav2_{variant}.so")
+        extra = extra + list(defines)
     stamp = lib + ".sha256"
     dig = _digest(extra)
     if not force and os.path.exists(lib) and os.path.exists(stamp):
@@ -50,7 +56,7 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
             return lib
     objs, procs = [], []
     for src in sources():
-        obj = os.path.join(LIBDIR, os.path.basename(src) + (".dbg.o" if debug else ".o"))
+        obj = os.path.join(LIBDIR, os.path.basename(src) + f".{os.path.basename(lib)}.o")
         cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", INCLUDE, "-Xptxas", "-v", "-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)

@@ -42,6 +42,19 @@ __device__ __forceinline__ void sel_record(int slot, long long dur, long long n)
     d[(6 * 3 + 1) * kDbgCtas + slot] = n;
   }
 }
+// select phase end times (relative to the warp's start): 0 keys staged and
+// scored, 1 threshold found (record 7; the debug buffer holds 8 x 3 x 4096)
+__device__ __forceinline__ void sel_record_phase(int slot, int phase, long long dur) {
+  if constexpr (!kDebug) return;
+  long long* d = g_dbg_cta;
+  if (d != nullptr && slot < kDbgCtas) d[(phase == 0 ? 6 * 3 + 2 : 7 * 3 + 0) * kDbgCtas + slot] = dur;
+}
+// raw stamp array (record 7, slots 1-2 of the cta buffer: 8192 entries)
+__device__ __forceinline__ void raw_stamp(int i, long long v) {
+  if constexpr (!kDebug) return;
+  long long* d = g_dbg_cta;
+  if (d != nullptr && i < 2 * kDbgCtas) d[(7 * 3 + 1) * kDbgCtas + i] = v;
+}
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

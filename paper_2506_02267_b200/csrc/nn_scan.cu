@@ -33,10 +33,11 @@
 // itself needs 32 / 64 / 128 cycles at N = 64 / 128 / 256), so N = 256 is the
 // first shape where a single issuer keeps the tensor core busy: 2 MMAs
 // (2 k-steps of 16) per 256-token tile.
-// Roles (576 threads): warps 0-15 epilogue (warp w reads TMEM lanes
-// 32*(w%4).. = candidates, column quarter w/4 = 64 tokens of every tile, two
-// tcgen05.ld + one wait per tile; four warps per SM sub-partition hide the
-// ~200-cycle TMEM load latency), warp 16 producer
+// Roles (576 threads): warps 0-15 epilogue in two groups of 8 on alternate
+// tiles (warp w reads TMEM lanes 32*(w%4).. = candidates, column half
+// (w%8)/4 = 128 tokens of its group's tiles in two rounds of two tcgen05.ld +
+// one wait; the TMEM load latency, ~0.25 us, dominates a round, and the two
+// groups overlap it), warp 16 producer
 // (one 16 KB cp.async.bulk per pre-tiled 256-token fp16 image written by
 // prep_kernel, 6-stage ring), warp 17 MMA issuer.  TMEM: 2 accumulator
 // buffers x 256 columns.  Chunk boundaries are tile aligned (planner), so
@@ -61,6 +62,7 @@ constexpr int kAcc = 2;          // TMEM accumulator buffers (2 x 256 columns)
 constexpr int kTcThreads = 576;
 constexpr int kProdWarp = 16, kMmaWarp = 17;
 constexpr int kEpiThreads = 512;
+constexpr int kGrpThreads = 256;  // epilogue group: warps 0-7 take even tiles, 8-15 odd tiles
 constexpr int kBTile = kScanTileBytes;      // 4 chunks x 256 rows x 16 B = 16 KB
 constexpr int kASlab = 128 * 16;            // one 16-byte K chunk of 128 candidate rows
 constexpr int kATile = 4 * kASlab;          // 32 fp16 of 128 rows (8 KB)
@@ -80,6 +82,15 @@ __device__ int g_dbg_block = 0;
       dbgp[(slot) + 160 * (pass - 1)] = t_;                                          \
     }                                                                                \
   } while (0)
+// pass-1 per-warp stamps: slot 1100 + (tile * 16 + warp) * 6 + which, tiles < 4
+#define WARP_STAMP(tile_, which)                                                     \
+  do {                                                                               \
+    if (kDebug && dbgp && pass == 1 && lane == 0 && (tile_) < 4) {                   \
+      long long t_;                                                                  \
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                          \
+      dbgp[1100 + ((tile_) * 16 + warp) * 6 + (which)] = t_;                          \
+    }                                                                                \
+  } while (0)
 
 // Store the group maxima of one 32-column quarter v[32].  dst is the
 // (candidate, source) row indexed by global group - gbase (gbase = 8-aligned
@@ -92,11 +103,7 @@ __device__ __forceinline__ void write_groups(const float* v, float* dst, int g_f
   constexpr int G = 1 << GL, NG = 32 >> GL;
   float m[NG];
 #pragma unroll
-  for (int g = 0; g < NG; ++g) {
-    m[g] = v[g * G];
-#pragma unroll
-    for (int e = 1; e < G; ++e) m[g] = fmaxf(m[g], v[g * G + e]);
-  }
+  for (int g = 0; g < NG; ++g) m[g] = max_run<G>(v + g * G);
   float* d = dst + g_first;
   if (whole) {
     if constexpr (NG >= 4) {
@@ -131,6 +138,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages], tfull[kAcc], tempty[kAcc];
   __shared__ uint32_t taddr_s;
   __shared__ uint16_t sbuf[kSurvBuf][kEpiThreads];  // pass 2: per-thread survivor buffer
+  __shared__ __align__(16) float gstage[kAcc][2][128][kNT / 32];  // pass 1, G = 32: [group][tile parity]
 
   cta_stamp(pass == 1 ? kDbgScan1 : kDbgScan2, 0);
   long long* const dbgp = kDebug && blockIdx.x == g_dbg_block ? g_dbg_timeline : nullptr;
@@ -156,7 +164,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
       }
       for (int b = 0; b < kAcc; ++b) {
         mbar_init(&tfull[b], 1);
-        mbar_init(&tempty[b], kEpiThreads);
+        mbar_init(&tempty[b], kGrpThreads);
       }
       mbar_fence_init();
     }
@@ -223,12 +231,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
                       j > 0);
         commit(&empty[s]);
         commit(&tfull[b]);
+        if (kDebug && dbgp && i < 32) {  // MMA completion latency (debug builds only)
+          mbar_wait(&tfull[b], (i / kAcc) & 1);
+          SCAN_STAMP(520 - 120 * (pass - 1) + i);  // dbgp[520 + 40 * (pass - 1) + i]
+        }
       }
     }
   } else {
-    // ---- epilogue: thread = (candidate, 64-column quarter) ----
+    // ---- epilogue: two groups of 8 warps on alternate tiles (accumulator
+    // buffer = group), so one group's TMEM loads overlap the other's
+    // processing; thread = (candidate, 128-column half), two 64-column rounds
+    // per tile ----
+    const int grp = warp >> 3, gw = warp & 7, gtid = tid & (kGrpThreads - 1);
     const int c = tid & 127;
-    const int cq = warp >> 2;
     const bool mine = c < tile.n;
     const int item = tile.item0 + (mine ? c : 0);
     const int gl_lo = s_lo >> glog, gl_hi = (s_hi - 1) >> glog;  // the source's global groups
@@ -242,28 +257,49 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
       for (int j = 0; j < nb; ++j) sdst[pos + j] = sbuf[j][tid];
       nb = 0;
     };
-    const uint32_t lane_base = T + ((uint32_t)((warp & 3) * 32) << 16) + 64 * cq;
-    for (int i = 0; i < ntiles; ++i) {
-      const int b = i % kAcc;
+    const uint32_t lane_base = T + ((uint32_t)((warp & 3) * 32) << 16) + 128 * (gw >> 2);
+    for (int i = grp; i < ntiles; i += kAcc) {
+      const int b = grp;
+      float(*const gs)[kNT / 32] = gstage[b][(i / kAcc) & 1];
       mbar_wait_sleep(&tfull[b], (i / kAcc) & 1);
       fence_after();
-      if (tid == 0 && i < 32) SCAN_STAMP(72 + i);
-      {
+      if (gtid == 0 && i < 32) SCAN_STAMP(72 + i);
+#pragma unroll 1
+      for (int hq = 0; hq < 2; ++hq) {
+        const int cq = 2 * (gw >> 2) + hq;  // 64-column quarter of the tile
         float v[64];
-        tmem_ld32(lane_base + b * kNT, reinterpret_cast<uint32_t*>(v));
-        tmem_ld32(lane_base + b * kNT + 32, reinterpret_cast<uint32_t*>(v + 32));
+        tmem_ld32(lane_base + b * kNT + 64 * hq, reinterpret_cast<uint32_t*>(v));
+        tmem_ld32(lane_base + b * kNT + 64 * hq + 32, reinterpret_cast<uint32_t*>(v + 32));
         tmem_ld_wait();
-        fence_before();
-        mbar_arrive(&tempty[b]);
-        if (tid == 0 && i < 32) SCAN_STAMP(104 + i);
+        WARP_STAMP(i, 2 * hq);
+        if (hq == 1) {
+          fence_before();
+          mbar_arrive(&tempty[b]);
+          if (gtid == 0 && i < 32) SCAN_STAMP(104 + i);
+        }
 #pragma unroll
         for (int qq = 0; qq < 2; ++qq) {  // two 32-column quarters
           const int col0 = (tile0 + i) * kNT + 64 * cq + 32 * qq;  // global token of column 0
-          if (col0 + 32 <= g0 || col0 >= g1 || !mine) continue;
+          if (col0 + 32 <= g0 || col0 >= g1 || !mine) {
+            if (pass == 1 && glog == 5) gs[c][2 * cq + qq] = -INFINITY;
+            continue;
+          }
           const bool partial = col0 < g0 || col0 + 32 > g1;
           const uint32_t valid = partial ? range_mask(col0, g0, g1) : 0xffffffffu;
           float* q = v + 32 * qq;
           if (pass == 1) {
+            if (glog == 5) {  // one group per quarter: staged, written coalesced below
+              float m;
+              if (!partial) {
+                m = max_run<32>(q);
+              } else {
+                m = -INFINITY;
+#pragma unroll
+                for (int e = 0; e < 32; ++e) m = fmaxf(m, ((valid >> e) & 1u) ? q[e] : -INFINITY);
+              }
+              gs[c][2 * cq + qq] = m;
+              continue;
+            }
             if (partial) {
 #pragma unroll
               for (int e = 0; e < 32; ++e) q[e] = ((valid >> e) & 1u) ? q[e] : -INFINITY;
@@ -278,6 +314,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
               default: write_groups<5>(q, gdst, gf, gl_lo, gl_hi, !partial); break;
             }
           } else {
+            // survivors are rare: test the quarter's maximum first
+            if (!(max_run<32>(q) >= gate)) continue;
             uint32_t m = 0u;
 #pragma unroll
             for (int e = 0; e < 32; ++e) m |= (q[e] >= gate ? 1u : 0u) << e;
@@ -291,6 +329,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
             }
           }
         }
+        WARP_STAMP(i, 2 * hq + 1);
+      }
+      if (pass == 1 && glog == 5) {
+        // coalesced write-out of this tile's group maxima: thread -> (candidate,
+        // 4-group half); the group row of a candidate is contiguous in gmax
+        named_bar_sync(1 + grp, kGrpThreads);
+        WARP_STAMP(i, 4);
+        const int cc = gtid >> 1, hh = gtid & 1;
+        const int gg0 = (tile0 + i) * (kNT / 32) + 4 * hh;  // global group index of the 4
+        if (cc < tile.n) {
+          float* dst = sc.gmax + ((size_t)(tile.item0 + cc) * 3 + src) * sc.gcap - (gl_lo & ~7);
+          const float* sv = &gs[cc][4 * hh];
+          if (gg0 >= gl_lo && gg0 + 3 <= gl_hi) {
+            *reinterpret_cast<float4*>(dst + gg0) = *reinterpret_cast<const float4*>(sv);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (gg0 + k >= gl_lo && gg0 + k <= gl_hi) dst[gg0 + k] = sv[k];
+          }
+        }
+        WARP_STAMP(i, 5);
       }
     }
     if (pass == 2 && nb > 0) flush();
@@ -364,8 +423,8 @@ __device__ __forceinline__ void nn_bound_body(const Staged& st, const NNCfg& nn,
   if (lane == 0) sc.count[(size_t)item * 3 + s] = 0u;
   const ReqInfo& rq = st.req[st.item_req[item]];
   const int k = nn.k[s];
-  const int lo = rq.tok_off[s] + (s == 1 ? nn.recent : 0), hi = rq.tok_off[s] + rq.len[s];
-  if (k == 0 || hi - lo <= k) return;  // no scan: everything (or nothing) is selected
+  const int lo = rq.tok_off[s] + (s == 1 ? min(nn.recent, rq.len[1]) : 0), hi = rq.tok_off[s] + rq.len[s];
+  if (!nn_scanned(hi - lo, k)) return;  // no scan (nn_select takes every token)
   const int glog = rq.glog[s];
   const int ng = ((hi - 1) >> glog) - (lo >> glog) + 1;
   float* out = sc.bound + (size_t)item * 3 + s;

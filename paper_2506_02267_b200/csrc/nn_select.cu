@@ -9,16 +9,18 @@
 // One warp per (candidate, source):
 //   1. a source with n <= k tokens selects all of them (no scan ran);
 //   2. otherwise every survivor of the scan's gate (nn_scan.cu) gets its
-//      exact key (reference f64 score | inverted index); n <= 256 (the normal
+//      exact key (sources too small to scan: select_direct) (reference f64 score | inverted index); n <= 256 (the normal
 //      case: about k + a few dozen survivors): the survivors' token rows are
 //      staged in shared memory by cp.async (one memory round trip), scored by
-//      the lanes in parallel, and every key ranked against all others (a
-//      rolled broadcast loop); the k best win.  Larger n -- degenerate
+//      the lanes in parallel, and the k-th largest key found by bisection
+//      (warp-wide counts); the k best win.  Larger n -- degenerate
 //      sources with massive ties, e.g. a zero candidate -- uses a radix select
 //      (keys recomputed per pass);
 //   3. the winners are marked in a bitmap over source positions and emitted
 //      in descending storage index (radix path: a shared bitonic sort).
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <stdint.h>
 
 #include "dbg.cuh"
@@ -39,24 +41,26 @@ __device__ __forceinline__ uint64_t winner_key(uint64_t key) {
 
 // reference score: f64 dot of the f32 unit vectors (nnsearch.py:344-347);
 // four independent chains in a fixed order, so equal rows score equal
-__device__ __forceinline__ double dot_exact(const float4* r, const float* uc) {
+__device__ __forceinline__ double dot_exact(const float4* r, const double* uc) {
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
   for (int q4 = 0; q4 < 8; ++q4) {
-    a0 = fma((double)r[q4].x, (double)uc[4 * q4], a0);
-    a1 = fma((double)r[q4].y, (double)uc[4 * q4 + 1], a1);
-    a2 = fma((double)r[q4].z, (double)uc[4 * q4 + 2], a2);
-    a3 = fma((double)r[q4].w, (double)uc[4 * q4 + 3], a3);
+    a0 = fma((double)r[q4].x, uc[4 * q4], a0);
+    a1 = fma((double)r[q4].y, uc[4 * q4 + 1], a1);
+    a2 = fma((double)r[q4].z, uc[4 * q4 + 2], a2);
+    a3 = fma((double)r[q4].w, uc[4 * q4 + 3], a3);
   }
   return (a0 + a1) + (a2 + a3);
 }
 
 struct KeySrc {  // survivors of one (candidate, source)
-  const uint16_t* surv;
+  const uint16_t* surv;  // scan survivor list, or null: every token from `first` on
+  int first;
   const float* tok;  // the source's f32 unit rows
-  float uc[kEmbed];
+  double uc[kEmbed];  // the candidate's unit row, converted once
+  __device__ __forceinline__ int token(int i) const { return surv ? (int)surv[i] : first + i; }
   __device__ __forceinline__ uint64_t key(int i) const {
-    const int t = surv[i];
+    const int t = token(i);
     float4 r[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) r[q] = __ldg(reinterpret_cast<const float4*>(tok + (size_t)t * kEmbed) + q);
@@ -64,8 +68,9 @@ struct KeySrc {  // survivors of one (candidate, source)
   }
 };
 
+// .ca: cached in L1 -- every candidate of a request reads the same token rows
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(smem)), "l"(gmem) : "memory");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(smem)), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -74,12 +79,12 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // copies in flight at once; 16-byte chunk c of row r stored at chunk
 // c ^ (r & 7) so the per-lane row reads below are bank-conflict free), then
 // every lane scores its rows exactly.
-constexpr int kRowBatch = 128;
+constexpr int kRowBatch = 64;
 __device__ __forceinline__ void keys_staged(const KeySrc& ks, int n, int lane, float4* rows, uint64_t* a) {
   for (int b0 = 0; b0 < n; b0 += kRowBatch) {
     const int nb = min(kRowBatch, n - b0);
     for (int rr = lane >> 3; rr < nb; rr += 4) {
-      const int t = ks.surv[b0 + rr];
+      const int t = ks.token(b0 + rr);
       const int c = lane & 7;
       cp_async16(rows + rr * 8 + (c ^ (rr & 7)), ks.tok + (size_t)t * kEmbed + 4 * c);
     }
@@ -89,7 +94,7 @@ __device__ __forceinline__ void keys_staged(const KeySrc& ks, int n, int lane, f
       float4 r[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) r[c] = rows[rr * 8 + (c ^ (rr & 7))];
-      a[b0 + rr] = score_key(dot_exact(r, ks.uc), ks.surv[b0 + rr]);
+      a[b0 + rr] = score_key(dot_exact(r, ks.uc), ks.token(b0 + rr));
     }
     __syncwarp();
   }
@@ -139,8 +144,7 @@ __device__ __forceinline__ void emit_bitmap(const uint32_t* bm, int words, int k
 
 // The k largest of n <= 32 R keys a[0..n) (shared) win: lane-owned key
 // i = j*32 + lane has rank #{m : a[m] > key} (keys are unique), counted with a
-// rolled loop of broadcast reads -- compact code (a fully unrolled sorting
-// network runs once per SM and is bound by instruction fetch).
+// rolled loop of broadcast reads (cheapest for small n).
 template <int R>
 __device__ __forceinline__ void select_rank(const uint64_t* a, int n, int k, int lane, uint32_t* bm) {
   uint64_t v[R];
@@ -163,6 +167,94 @@ __device__ __forceinline__ void select_rank(const uint64_t* a, int n, int k, int
       atomicOr(bm + (t >> 5), 1u << (t & 31));
     }
   __syncwarp();
+}
+
+// The k largest of n <= 32 R keys a[0..n) (shared) win, found by bisection
+// on the keys: T_hi = the largest t
+// with #{hi32(key) >= t} >= k (32-bit halving, early exit when the count is
+// exactly k), then, among the keys tied at hi32 == T_hi, the same search on
+// the low 32 bits.  Winners = keys >= (T_hi, T_lo): exactly k (keys are
+// unique).  ~3 R instructions per halving (<= 64 halvings, usually one
+// 32-bit search ending early) instead of ranking every key against all n.
+// (keys in registers: key j * 32 + lane in kv[j])
+template <int R>
+__device__ __forceinline__ void select_bisect_regs(const uint64_t* kv, int n, int k, int lane, uint32_t* bm) {
+  if (n <= 0) return;  // (warp-uniform)
+  uint32_t vh[R], vl[R];
+  bool in[R];
+  uint32_t mn = 0xffffffffu, mx = 0u;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    in[j] = j * 32 + lane < n;
+    const uint64_t x = in[j] ? kv[j] : 0ull;
+    vh[j] = (uint32_t)(x >> 32);
+    vl[j] = (uint32_t)x;
+    if (in[j]) {
+      mn = min(mn, vh[j]);
+      mx = max(mx, vh[j]);
+    }
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  auto cnt_hi = [&](uint32_t t) {
+    unsigned c = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) c += (in[j] && vh[j] >= t) ? 1u : 0u;
+    return (int)__reduce_add_sync(0xffffffffu, c);
+  };
+  // count(>= lo) >= k > count(>= hi); hi = mx + 1 may wrap only if mx = ~0
+  uint64_t lo = mn, hi = (uint64_t)mx + 1;
+  int c_lo = n;
+  while (hi - lo > 1) {
+    const uint64_t mid = lo + ((hi - lo) >> 1);
+    const int c = cnt_hi((uint32_t)mid);
+    if (c >= k) {
+      lo = mid;
+      c_lo = c;
+      if (c == k) break;
+    } else {
+      hi = mid;
+    }
+  }
+  const uint32_t th = (uint32_t)lo;
+  uint32_t tl = 0u;
+  if (c_lo > k) {  // ties at hi32 == th: pick the k - above largest low halves
+    const int above = lo == 0xffffffffull ? 0 : cnt_hi(th + 1);
+    const int want = k - above;
+    auto cnt_lo = [&](uint32_t t) {
+      unsigned c = 0;
+#pragma unroll
+      for (int j = 0; j < R; ++j) c += (in[j] && vh[j] == th && vl[j] >= t) ? 1u : 0u;
+      return (int)__reduce_add_sync(0xffffffffu, c);
+    };
+    uint64_t l2 = 0, h2 = 0x100000000ull;
+    while (h2 - l2 > 1) {
+      const uint64_t mid = l2 + ((h2 - l2) >> 1);
+      const int c = cnt_lo((uint32_t)mid);
+      if (c >= want) {
+        l2 = mid;
+        if (c == want) break;
+      } else {
+        h2 = mid;
+      }
+    }
+    tl = (uint32_t)l2;
+  }
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+    if (in[j] && (vh[j] > th || (vh[j] == th && vl[j] >= tl))) {
+      const int t = key_index(((uint64_t)vh[j] << 32) | vl[j]);
+      atomicOr(bm + (t >> 5), 1u << (t & 31));
+    }
+  __syncwarp();
+}
+
+template <int R>
+__device__ __forceinline__ void select_bisect(const uint64_t* a, int n, int k, int lane, uint32_t* bm) {
+  uint64_t kv[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) kv[j] = j * 32 + lane < n ? a[j * 32 + lane] : 0ull;
+  select_bisect_regs<R>(kv, n, k, lane, bm);
 }
 
 __device__ __forceinline__ void warp_bitonic_desc_smem(uint64_t* a, int n, int lane) {
@@ -269,6 +361,117 @@ __device__ __forceinline__ void select_radix(const KeySrc& ks, int n, int k, int
   }
 }
 
+// Sources too small to scan (n <= kDirectMax selectable tokens: the RT tail
+// and IMP at their 256-token caps, short LL histories), two-level, so FP64
+// (DFMA issues at 1/8 the FFMA rate here) runs only where the order is in
+// doubt:
+//   1. approximate scores in f32 for every token (rows staged by cp.async;
+//      two FFMA chains of 16 products: |approx - exact| <= gamma_17 <
+//      1.02e-6 <= kDirEps / 2 for unit vectors) and a 256-bin histogram over
+//      [-1, 1]; bin b holds the k-th largest approximation;
+//   2. approx >= upper edge of b + 2 eps: certainly in the exact top k (fewer
+//      than k tokens have approx >= that edge, and any token scoring higher
+//      exactly is among them); approx < lower edge of b - 2 eps: certainly
+//      out (k tokens have approx >= the lower edge, hence exact >= edge -
+//      eps); the rest (the bin and its 2 eps margins, a handful) get the
+//      exact f64 key and the best k - (certain winners) of them win.
+constexpr float kDirEps = 2.5e-6f;
+constexpr int kDirBins = 256;
+__device__ __forceinline__ void select_direct(const KeySrc& ks, const float* ucf, int n, int k, int lane,
+                                              float4* rows, unsigned* hist, uint64_t* a, uint32_t* bm) {
+  const int lo = ks.first;
+#pragma unroll
+  for (int b = 0; b < kDirBins / 32; ++b) hist[b * 32 + lane] = 0u;
+  float ap[kDirectMax / 32];
+#pragma unroll
+  for (int bb = 0; bb < kDirectMax / kRowBatch; ++bb) {
+    const int b0 = bb * kRowBatch;
+    if (b0 < n) {  // (warp-uniform)
+      const int nb = min(kRowBatch, n - b0);
+      for (int i = lane; i < nb * 8; i += 32) {
+        const int rr = i >> 3, c = i & 7;
+        cp_async16(rows + rr * 8 + (c ^ (rr & 7)), ks.tok + (size_t)(lo + b0 + rr) * kEmbed + 4 * c);
+      }
+      cp_async_wait_all();
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < kRowBatch / 32; ++h) {
+        const int rr = 32 * h + lane;
+        float v = -INFINITY;
+        if (rr < nb) {
+          float e0 = 0.f, e1 = 0.f;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 x = rows[rr * 8 + (q ^ (rr & 7))];
+            float& e = (q & 1) ? e1 : e0;
+            e = fmaf(x.x, ucf[4 * q], e);
+            e = fmaf(x.y, ucf[4 * q + 1], e);
+            e = fmaf(x.z, ucf[4 * q + 2], e);
+            e = fmaf(x.w, ucf[4 * q + 3], e);
+          }
+          v = e0 + e1;
+          atomicAdd(hist + min(max((int)((v + 1.0f) * (kDirBins / 2)), 0), kDirBins - 1), 1u);
+        }
+        ap[bb * (kRowBatch / 32) + h] = v;
+      }
+      __syncwarp();
+    } else {
+#pragma unroll
+      for (int h = 0; h < kRowBatch / 32; ++h) ap[bb * (kRowBatch / 32) + h] = -INFINITY;
+    }
+  }
+  __syncwarp();
+  // bin of the k-th largest approximation: lane l owns bins 255 - 8l .. 248 - 8l
+  unsigned h8[8], tot = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    h8[q] = hist[kDirBins - 1 - 8 * lane - q];
+    tot += h8[q];
+  }
+  unsigned incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const unsigned sel = __ballot_sync(0xffffffffu, incl >= (unsigned)k && incl - tot < (unsigned)k);
+  const int src = __ffs(sel) - 1;
+  int kbin = 0;
+  if (lane == src) {
+    unsigned run = incl - tot;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      run += h8[q];
+      if (run >= (unsigned)k) { kbin = kDirBins - 1 - 8 * lane - q; break; }
+    }
+  }
+  kbin = __shfl_sync(0xffffffffu, kbin, src);
+  const float win_t = (float)(kbin + 1) / (kDirBins / 2) - 1.0f + 2.0f * kDirEps;
+  const float amb_t = (float)kbin / (kDirBins / 2) - 1.0f - 2.0f * kDirEps;
+  int c_w = 0, m = 0;
+#pragma unroll
+  for (int jj = 0; jj < kDirectMax / 32; ++jj) {
+    const int rr = jj * 32 + lane;
+    const bool win = ap[jj] >= win_t;  // (-inf for rr >= n)
+    const bool amb = !win && ap[jj] >= amb_t;
+    if (win) atomicOr(bm + ((lo + rr) >> 5), 1u << ((lo + rr) & 31));
+    c_w += __popc(__ballot_sync(0xffffffffu, win));
+    const unsigned ma = __ballot_sync(0xffffffffu, amb);
+    if (amb) {
+      float4 r[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) r[q] = __ldg(reinterpret_cast<const float4*>(ks.tok + (size_t)(lo + rr) * kEmbed) + q);
+      a[m + __popc(ma & ((1u << lane) - 1))] = score_key(dot_exact(r, ks.uc), lo + rr);
+    }
+    m += __popc(ma);
+  }
+  __syncwarp();
+  const int want = k - c_w;
+  if (m <= 64) select_rank<2>(a, m, want, lane, bm);
+  else if (m <= 128) select_bisect<4>(a, m, want, lane, bm);
+  else select_bisect<8>(a, m, want, lane, bm);
+}
+
 __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn, const NNScan& sc,
                                                int32_t* idx, float* scores);
 
@@ -283,7 +486,7 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
                                                int32_t* idx, float* scores) {
   __shared__ uint64_t buf[kSelWarps][kSelCap];  // radix path key cache; also the sort array
   __shared__ unsigned hist_s[kSelWarps][256];
-  __shared__ float4 rows_s[kSelWarps][kRowBatch * 8];  // staged token rows (16 KB per warp)
+  __shared__ float4 rows_s[kSelWarps][kRowBatch * 8];  // staged token rows (8 KB per warp)
   __shared__ uint32_t bm_s[kSelWarps][kCaps0 / 32];      // winner bitmap over source positions
   uint64_t (&keys_s)[kSelWarps][kSelCap] = buf;
   cta_stamp(kDbgSelect, 0);
@@ -326,30 +529,45 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
     }
     return;
   }
-  // 2./3. select over the survivors
+  // 2./3. select over the survivors (all tokens of a source too small to scan)
+  const bool scanned = nn_scanned(hi - lo, k);
   KeySrc ks;
-  ks.surv = sc.surv + (size_t)item * sc.surv_stride + (rq.tok_off[s] - rq.tok_off[0]);
+  ks.surv = scanned ? sc.surv + (size_t)item * sc.surv_stride + (rq.tok_off[s] - rq.tok_off[0]) : nullptr;
+  ks.first = lo;
   ks.tok = st.tok_unit + (size_t)rq.tok_off[s] * kEmbed;
+  float ucf[kEmbed];
   {
     const float4* cu = reinterpret_cast<const float4*>(st.cand_unit + (size_t)item * kEmbed);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float4 q = __ldg(cu + j);
-      ks.uc[4 * j] = q.x; ks.uc[4 * j + 1] = q.y; ks.uc[4 * j + 2] = q.z; ks.uc[4 * j + 3] = q.w;
+      ucf[4 * j] = q.x; ucf[4 * j + 1] = q.y; ucf[4 * j + 2] = q.z; ucf[4 * j + 3] = q.w;
     }
+#pragma unroll
+    for (int j = 0; j < kEmbed; ++j) ks.uc[j] = ucf[j];
   }
-  const int n = min((int)sc.count[(size_t)item * 3 + s], hi - lo);
+  const int n = scanned ? min((int)sc.count[(size_t)item * 3 + s], hi - lo) : hi - lo;
   const long long t_start = kDebug ? gtimer() : 0;
   uint64_t* a = keys_s[warp];
-  if (max(n, k) <= kSelCache) {
+  if (!scanned) {
+    uint32_t* bm = bm_s[warp];
+    const int words = (hi + 31) >> 5;
+    for (int w = lane; w < words; w += 32) bm[w] = 0u;
+    __syncwarp();
+    select_direct(ks, ucf, n, k, lane, rows_s[warp], hist_s[warp], a, bm);
+    if (kDebug && lane == 0) sel_record_phase(item * 3 + s, 1, gtimer() - t_start);
+    emit_bitmap(bm, words, k, lane, orow, srow, ks);
+  } else if (max(n, k) <= kSelCache) {
     uint32_t* bm = bm_s[warp];
     const int words = (hi + 31) >> 5;
     for (int w = lane; w < words; w += 32) bm[w] = 0u;
     keys_staged(ks, n, lane, rows_s[warp], a);
+    if (kDebug && lane == 0) sel_record_phase(item * 3 + s, 0, gtimer() - t_start);
     const int np = max(n, k);
-    if (np <= 64) select_rank<2>(a, n, k, lane, bm);
-    else if (np <= 128) select_rank<4>(a, n, k, lane, bm);
-    else select_rank<8>(a, n, k, lane, bm);
+    if (np <= 64) select_bisect<2>(a, n, k, lane, bm);
+    else if (np <= 128) select_bisect<4>(a, n, k, lane, bm);
+    else select_bisect<8>(a, n, k, lane, bm);
+    if (kDebug && lane == 0) sel_record_phase(item * 3 + s, 1, gtimer() - t_start);
     emit_bitmap(bm, words, k, lane, orow, srow, ks);
   } else {
     select_radix(ks, n, k, lane, buf[warp], hist_s[warp], orow, srow);

@@ -39,7 +39,7 @@ int fail(int code, const char* fmt, ...) {
                   __LINE__);                                                               \
   } while (0)
 
-constexpr int kTile = 128;        // candidates per NN tile (tcgen05 M)
+
 constexpr int kMinChunk = 256;    // minimum LL tokens per work unit
 constexpr int kCaps[3] = {16384, 256, 256};  // LIFELONG/REALTIME/IMPRESSION_CAP (core.py:31-33)
 
@@ -298,6 +298,7 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
   }
   if ((e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking)) != cudaSuccess)
     return bad(e, "copy stream");
+
   // padded to whole 64-token tiles (+1): the NN kernel bulk-copies full tiles
   if ((e = cudaMalloc(&c->tok_unit, (size_t)(cdiv((int)std::max<int64_t>(T, 1), 64) + 1) * 64 * kEmbed * 4)) !=
       cudaSuccess)
@@ -528,14 +529,15 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
     return fail(TAV2_ECAP, "%lld tokens exceed capacity %lld", (long long)T, (long long)c->cap.max_tokens);
 
   // ---- NN work decomposition: one CTA per (candidate tile, source, chunk).
-  // A source with n <= k tokens needs no scan (all selected).  Otherwise the
+  // A source with n <= k tokens needs no scan (all selected), nor one with
+  // n <= kDirectMax (nn_select scores every token exactly).  Otherwise the
   // threshold scan (nn_scan.cu) groups its tokens in G = 2^glog (about 4k to
   // 8k groups, G <= 32); chunk boundaries are kScanTile-aligned in the global
   // token index so every group and tile lies in one chunk.  RT tail and IMP take one
   // chunk per tile; LL chunks (>= kMinChunk tokens) fill the SMs. ----
   auto scanned = [&](const tav2_request& q, int s) {
-    const int lo = s == 1 ? nn.recent : 0;
-    return nn.k[s] > 0 && q.len[s] - lo > nn.k[s];
+    const int lo = s == 1 ? std::min(nn.recent, q.len[1]) : 0;
+    return nn_scanned(q.len[s] - lo, nn.k[s]);
   };
   auto group_log = [&](int n, int k) {
     int g = 0;

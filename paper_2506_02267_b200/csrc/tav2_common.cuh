@@ -44,6 +44,13 @@ constexpr float kGateEps = 1.1e-3f;
 // K-major no-swizzle layout, [4 chunks of 8 elements][256 rows][16 B].
 constexpr int kScanTile = 256;
 constexpr int kScanTileBytes = 4 * kScanTile * 16;
+// Sources with at most kDirectMax selectable tokens skip the scan: nn_select
+// scores all of them exactly (one staged batch per warp is cheaper than a
+// scan CTA whose per-token group maxima and survivor lists cost more than the
+// exact f64 dot products they prune).
+constexpr int kDirectMax = 256;
+// n_sel = selectable tokens of a source (RT: len - min(recent, len))
+__host__ __device__ inline bool nn_scanned(int n_sel, int k) { return k > 0 && n_sel > k && n_sel > kDirectMax; }
 
 struct NNWork {           // one (candidate tile, source, token chunk) unit
   int32_t tile;           // candidate tile id
@@ -51,6 +58,7 @@ struct NNWork {           // one (candidate tile, source, token chunk) unit
   int32_t t0, t1;         // token range, source-relative (RT tail: RT index)
 };
 
+constexpr int kTile = 128;  // candidates per NN tile (tcgen05 M)
 struct NNTile {           // up to kTile consecutive items of one request
   int32_t req;
   int32_t item0;

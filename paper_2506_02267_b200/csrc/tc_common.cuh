@@ -73,6 +73,28 @@ __device__ __forceinline__ void split_pair_t(float a, float b, uint32_t& hi, uin
   const float2 r = __ffma2_rn(h, make_float2(-1.0f, -1.0f), make_float2(a, b));  // exact residuals
   lo = __byte_perm(__float_as_uint(r.x), __float_as_uint(r.y), 0x7632);
 }
+// three-input max (one FMNMX3 on sm_100)
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// maximum of N (>= 1) consecutive registers: a ternary FMNMX3 tree (depth
+// log3 N; a dependent chain would leave the few epilogue warps per
+// sub-partition waiting on max latency)
+template <int N>
+__device__ __forceinline__ float max_run(const float* v) {
+  if constexpr (N == 1) {
+    return v[0];
+  } else if constexpr (N == 2) {
+    return fmaxf(v[0], v[1]);
+  } else if constexpr (N == 3) {
+    return fmax3f(v[0], v[1], v[2]);
+  } else {
+    constexpr int A = (N + 2) / 3, B = (N - A + 1) / 2;
+    return fmax3f(max_run<A>(v), max_run<B>(v + A), max_run<N - A - B>(v + A + B));
+  }
+}
 // kind::i8 with signed int8 A/B, s32 accumulate.
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
@@ -199,6 +221,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // Same, but lets the hardware suspend the thread (up to `ns` nanoseconds)
 // instead of spinning: far fewer issue slots burnt by waiting warps.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase, uint32_t ns = 20000) {
+#ifdef TAV2_SPIN_WAIT
+  mbar_wait(bar, phase);
+  return;
+#endif
   asm volatile(
       "{.reg .pred p;\n"
       "WAITS_%=:\n"

@@ -29,7 +29,7 @@ flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 for _ in range(5):
     eng.run_staged("bf16", logits)
 torch.cuda.synchronize()
-buf = torch.zeros(7 * 3 * 4096, dtype=torch.int64, device="cuda")
+buf = torch.zeros(8 * 3 * 4096, dtype=torch.int64, device="cuda")
 N.lib().tav2_debug_cta(buf.data_ptr())
 if "--flush" in sys.argv:
     flush.zero_()
@@ -37,7 +37,7 @@ torch.cuda.synchronize()
 eng.run_staged("bf16", logits)
 torch.cuda.synchronize()
 N.lib().tav2_debug_cta(None)
-t = buf.cpu().numpy().reshape(7, 3, 4096)
+t = buf.cpu().numpy().reshape(8, 3, 4096)
 t0 = min(int(t[k, 0][t[k, 0] > 0].min()) for k in range(6) if (t[k, 0] > 0).any())
 for k, name in enumerate(KERNELS):
     n = int((t[k, 0] > 0).sum())
@@ -62,3 +62,11 @@ if sel.any():
     print(f"select warps: {sel.sum()}  time med {np.median(d):.2f} p99 {np.percentile(d, 99):.2f} max {d.max():.2f} us;"
           f" survivors med {np.median(rec_n[sel]):.0f} max {rec_n[sel].max()}; slowest (item, src, n):",
           [(int(i) // 3, int(i) % 3, int(rec_n[i])) for i in np.argsort(-rec_t)[:5]])
+    st_t, bi_t = t[6, 2], t[7, 0]
+    for src in range(3):
+        m = sel & (np.arange(len(rec_t)) % 3 == src) & (st_t > 0)
+        if m.any():
+            print(f"  source {src}: warps {m.sum()} total med {np.median(rec_t[m]) / 1e3:.2f} us, keys staged+scored "
+                  f"med {np.median(st_t[m]) / 1e3:.2f} us, threshold found med {np.median(bi_t[m]) / 1e3:.2f} us, "
+                  f"n med {np.median(rec_n[m]):.0f}")
+

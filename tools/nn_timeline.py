@@ -24,7 +24,7 @@ logits = torch.empty((1000, 4), device="cuda")
 for _ in range(3):
     eng.run_staged("bf16", logits)
 torch.cuda.synchronize()
-buf = torch.zeros(1024, dtype=torch.int64, device="cuda")
+buf = torch.zeros(2048, dtype=torch.int64, device="cuda")
 blk = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 N.lib().tav2_debug_timeline(buf.data_ptr(), blk)
 eng.run_staged("bf16", logits)
@@ -39,6 +39,15 @@ for p in (1, 2):
     for i in range(32):
         if not t[b + 8 + i]:
             break
-        extra = f"  mma-thread free {f(t[520 + i]):6.2f} full {f(t[552 + i]):6.2f}" if p == 1 else ""
-        print(f"  tile {i:2d}: copy {f(t[b + 8 + i]):6.2f}{extra}  mma {f(t[b + 40 + i]):6.2f}  "
+        extra = f"  mma complete {f(t[520 + 40 * (p - 1) + i]):6.2f}"
+        print(f"  tile {i:2d}: copy {f(t[b + 8 + i]):6.2f}  mma {f(t[b + 40 + i]):6.2f}{extra}  "
               f"epi sees {f(t[b + 72 + i]):6.2f}  done {f(t[b + 104 + i]):6.2f}")
+
+b = 0
+t0 = t[0]
+print("pass 1 per-warp: r1 ld / r1 proc / r2 ld / r2 proc / barrier / write-out, us")
+for i in range(4):
+    for w in range(16):
+        row = [(t[1100 + (i * 16 + w) * 6 + j] - t0) / 1e3 if t[1100 + (i * 16 + w) * 6 + j] else float("nan")
+               for j in range(6)]
+        print(f"  tile {i} w{w}: " + " ".join(f"{x:6.2f}" for x in row))
