@@ -80,11 +80,21 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // c ^ (r & 7) so the per-lane row reads below are bank-conflict free), then
 // every lane scores its rows exactly.
 constexpr int kRowBatch = 64;
-__device__ __forceinline__ void keys_staged(const KeySrc& ks, int n, int lane, float4* rows, uint64_t* a) {
+// The survivor indices are first copied to sidx (all loads in flight at
+// once; fetching them inside the copy loop serialised one L2 round trip per
+// row group).
+__device__ __forceinline__ void keys_staged(const KeySrc& ks, int n, int lane, float4* rows, uint64_t* a,
+                                            uint16_t* sidx) {
+#pragma unroll
+  for (int j = 0; j < kSelCache / 32; ++j) {
+    const int i = j * 32 + lane;
+    if (i < n) sidx[i] = (uint16_t)ks.token(i);
+  }
+  __syncwarp();
   for (int b0 = 0; b0 < n; b0 += kRowBatch) {
     const int nb = min(kRowBatch, n - b0);
     for (int rr = lane >> 3; rr < nb; rr += 4) {
-      const int t = ks.token(b0 + rr);
+      const int t = sidx[b0 + rr];
       const int c = lane & 7;
       cp_async16(rows + rr * 8 + (c ^ (rr & 7)), ks.tok + (size_t)t * kEmbed + 4 * c);
     }
@@ -94,22 +104,37 @@ __device__ __forceinline__ void keys_staged(const KeySrc& ks, int n, int lane, f
       float4 r[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) r[c] = rows[rr * 8 + (c ^ (rr & 7))];
-      a[b0 + rr] = score_key(dot_exact(r, ks.uc), ks.token(b0 + rr));
+      a[b0 + rr] = score_key(dot_exact(r, ks.uc), sidx[b0 + rr]);
     }
     __syncwarp();
   }
 }
 
-// Emit the winners marked in a per-warp bitmap over source positions in
-// descending storage index (the segment order, nnsearch.py:364): lane l
-// scans words [W - per(l+1), W - per l), high first; a warp prefix sum of the
-// per-lane counts places its bits.
+// Winner bitmap over source positions, per warp.  Logical word w (positions
+// 32w..32w+31) of a `words`-word bitmap lives at bm_phys(w): emitting lane l
+// owns logical words words-1-per*l-j (j = 0..per-1, descending) at physical
+// j*32 + l, so its reads are bank-conflict free.  (per*32 words.)
+__device__ __forceinline__ int bm_phys(int w, int words) {
+  const int per = (words + 31) >> 5;
+  const int r = words - 1 - w;
+  return (r % per) * 32 + r / per;
+}
+__device__ __forceinline__ void bm_mark(uint32_t* bm, int words, int t) {
+  atomicOr(bm + bm_phys(t >> 5, words), 1u << (t & 31));
+}
+__device__ __forceinline__ void bm_clear(uint32_t* bm, int words, int lane) {
+  for (int w = lane; w < ((words + 31) >> 5) * 32; w += 32) bm[w] = 0u;
+}
+
+// Emit the winners marked in the bitmap in descending storage index (the
+// segment order, nnsearch.py:364): lane l scans its words high first; a warp
+// prefix sum of the per-lane counts places its bits.
 __device__ __forceinline__ void emit_bitmap(const uint32_t* bm, int words, int k, int lane, int32_t* orow,
                                             float* srow, const KeySrc& ks) {
   const int per = (words + 31) / 32;
-  const int w_hi = words - per * lane;  // this lane's words: [w_hi - per, w_hi)
+  const int w_hi = words - per * lane;  // this lane's logical words: [w_hi - per, w_hi)
   int cnt = 0;
-  for (int w = w_hi - 1; w >= max(w_hi - per, 0); --w) cnt += __popc(bm[w]);
+  for (int j = 0; j < per && w_hi - 1 - j >= 0; ++j) cnt += __popc(bm[j * 32 + lane]);
   int incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -117,8 +142,9 @@ __device__ __forceinline__ void emit_bitmap(const uint32_t* bm, int words, int k
     if (lane >= o) incl += y;
   }
   int pos = incl - cnt;
-  for (int w = w_hi - 1; w >= max(w_hi - per, 0); --w) {
-    uint32_t m = bm[w];
+  for (int j = 0; j < per && w_hi - 1 - j >= 0; ++j) {
+    const int w = w_hi - 1 - j;
+    uint32_t m = bm[j * 32 + lane];
     while (m) {
       const int b = 31 - __clz(m);
       m &= ~(1u << b);
@@ -146,7 +172,7 @@ __device__ __forceinline__ void emit_bitmap(const uint32_t* bm, int words, int k
 // i = j*32 + lane has rank #{m : a[m] > key} (keys are unique), counted with a
 // rolled loop of broadcast reads (cheapest for small n).
 template <int R>
-__device__ __forceinline__ void select_rank(const uint64_t* a, int n, int k, int lane, uint32_t* bm) {
+__device__ __forceinline__ void select_rank(const uint64_t* a, int n, int k, int lane, uint32_t* bm, int words) {
   uint64_t v[R];
   int rank[R];
 #pragma unroll
@@ -162,10 +188,7 @@ __device__ __forceinline__ void select_rank(const uint64_t* a, int n, int k, int
   }
 #pragma unroll
   for (int j = 0; j < R; ++j)
-    if (j * 32 + lane < n && rank[j] < k) {
-      const int t = key_index(v[j]);
-      atomicOr(bm + (t >> 5), 1u << (t & 31));
-    }
+    if (j * 32 + lane < n && rank[j] < k) bm_mark(bm, words, key_index(v[j]));
   __syncwarp();
 }
 
@@ -178,7 +201,8 @@ __device__ __forceinline__ void select_rank(const uint64_t* a, int n, int k, int
 // 32-bit search ending early) instead of ranking every key against all n.
 // (keys in registers: key j * 32 + lane in kv[j])
 template <int R>
-__device__ __forceinline__ void select_bisect_regs(const uint64_t* kv, int n, int k, int lane, uint32_t* bm) {
+__device__ __forceinline__ void select_bisect_regs(const uint64_t* kv, int n, int k, int lane, uint32_t* bm,
+                                                   int words) {
   if (n <= 0) return;  // (warp-uniform)
   uint32_t vh[R], vl[R];
   bool in[R];
@@ -242,19 +266,17 @@ __device__ __forceinline__ void select_bisect_regs(const uint64_t* kv, int n, in
   }
 #pragma unroll
   for (int j = 0; j < R; ++j)
-    if (in[j] && (vh[j] > th || (vh[j] == th && vl[j] >= tl))) {
-      const int t = key_index(((uint64_t)vh[j] << 32) | vl[j]);
-      atomicOr(bm + (t >> 5), 1u << (t & 31));
-    }
+    if (in[j] && (vh[j] > th || (vh[j] == th && vl[j] >= tl)))
+      bm_mark(bm, words, key_index(((uint64_t)vh[j] << 32) | vl[j]));
   __syncwarp();
 }
 
 template <int R>
-__device__ __forceinline__ void select_bisect(const uint64_t* a, int n, int k, int lane, uint32_t* bm) {
+__device__ __forceinline__ void select_bisect(const uint64_t* a, int n, int k, int lane, uint32_t* bm, int words) {
   uint64_t kv[R];
 #pragma unroll
   for (int j = 0; j < R; ++j) kv[j] = j * 32 + lane < n ? a[j * 32 + lane] : 0ull;
-  select_bisect_regs<R>(kv, n, k, lane, bm);
+  select_bisect_regs<R>(kv, n, k, lane, bm, words);
 }
 
 __device__ __forceinline__ void warp_bitonic_desc_smem(uint64_t* a, int n, int lane) {
@@ -378,7 +400,7 @@ __device__ __forceinline__ void select_radix(const KeySrc& ks, int n, int k, int
 constexpr float kDirEps = 2.5e-6f;
 constexpr int kDirBins = 256;
 __device__ __forceinline__ void select_direct(const KeySrc& ks, const float* ucf, int n, int k, int lane,
-                                              float4* rows, unsigned* hist, uint64_t* a, uint32_t* bm) {
+                                              float4* rows, unsigned* hist, uint64_t* a, uint32_t* bm, int words) {
   const int lo = ks.first;
 #pragma unroll
   for (int b = 0; b < kDirBins / 32; ++b) hist[b * 32 + lane] = 0u;
@@ -454,7 +476,7 @@ __device__ __forceinline__ void select_direct(const KeySrc& ks, const float* ucf
     const int rr = jj * 32 + lane;
     const bool win = ap[jj] >= win_t;  // (-inf for rr >= n)
     const bool amb = !win && ap[jj] >= amb_t;
-    if (win) atomicOr(bm + ((lo + rr) >> 5), 1u << ((lo + rr) & 31));
+    if (win) bm_mark(bm, words, lo + rr);
     c_w += __popc(__ballot_sync(0xffffffffu, win));
     const unsigned ma = __ballot_sync(0xffffffffu, amb);
     if (amb) {
@@ -467,9 +489,9 @@ __device__ __forceinline__ void select_direct(const KeySrc& ks, const float* ucf
   }
   __syncwarp();
   const int want = k - c_w;
-  if (m <= 64) select_rank<2>(a, m, want, lane, bm);
-  else if (m <= 128) select_bisect<4>(a, m, want, lane, bm);
-  else select_bisect<8>(a, m, want, lane, bm);
+  if (m <= 64) select_rank<2>(a, m, want, lane, bm, words);
+  else if (m <= 128) select_bisect<4>(a, m, want, lane, bm, words);
+  else select_bisect<8>(a, m, want, lane, bm, words);
 }
 
 __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn, const NNScan& sc,
@@ -488,6 +510,7 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
   __shared__ unsigned hist_s[kSelWarps][256];
   __shared__ float4 rows_s[kSelWarps][kRowBatch * 8];  // staged token rows (8 KB per warp)
   __shared__ uint32_t bm_s[kSelWarps][kCaps0 / 32];      // winner bitmap over source positions
+  __shared__ uint16_t sidx_s[kSelWarps][kSelCache];     // survivor indices
   uint64_t (&keys_s)[kSelWarps][kSelCap] = buf;
   cta_stamp(kDbgSelect, 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -552,21 +575,21 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
   if (!scanned) {
     uint32_t* bm = bm_s[warp];
     const int words = (hi + 31) >> 5;
-    for (int w = lane; w < words; w += 32) bm[w] = 0u;
+    bm_clear(bm, words, lane);
     __syncwarp();
-    select_direct(ks, ucf, n, k, lane, rows_s[warp], hist_s[warp], a, bm);
+    select_direct(ks, ucf, n, k, lane, rows_s[warp], hist_s[warp], a, bm, words);
     if (kDebug && lane == 0) sel_record_phase(item * 3 + s, 1, gtimer() - t_start);
     emit_bitmap(bm, words, k, lane, orow, srow, ks);
   } else if (max(n, k) <= kSelCache) {
     uint32_t* bm = bm_s[warp];
     const int words = (hi + 31) >> 5;
-    for (int w = lane; w < words; w += 32) bm[w] = 0u;
-    keys_staged(ks, n, lane, rows_s[warp], a);
+    bm_clear(bm, words, lane);
+    keys_staged(ks, n, lane, rows_s[warp], a, sidx_s[warp]);
     if (kDebug && lane == 0) sel_record_phase(item * 3 + s, 0, gtimer() - t_start);
     const int np = max(n, k);
-    if (np <= 64) select_bisect<2>(a, n, k, lane, bm);
-    else if (np <= 128) select_bisect<4>(a, n, k, lane, bm);
-    else select_bisect<8>(a, n, k, lane, bm);
+    if (np <= 64) select_rank<2>(a, n, k, lane, bm, words);
+    else if (np <= 128) select_bisect<4>(a, n, k, lane, bm, words);
+    else select_bisect<8>(a, n, k, lane, bm, words);
     if (kDebug && lane == 0) sel_record_phase(item * 3 + s, 1, gtimer() - t_start);
     emit_bitmap(bm, words, k, lane, orow, srow, ks);
   } else {

@@ -48,17 +48,61 @@ __device__ __forceinline__ float quad_sumsq(const float* v, unsigned qm) {
 // One quad of threads per token row (then per candidate row); thread g owns
 // elements 8g..8g+7 of the 32-vector and features 16g..16g+15 of the 64-d
 // Eq. 4 token part.
+__device__ __forceinline__ void prep_body(const Staged& st, int with_feat, const float* tab_s, int action_rows,
+                                          int2 raw, unsigned act, int surf_raw, float4 c0, float4 c1);
+
 __global__ void __launch_bounds__(256) prep_kernel(Staged st, Params p, int with_feat) {
   cta_stamp(kDbgPrep, 0);
   griddep_launch();
   griddep_wait();  // the previous step's kernels may still read tok_unit / cand_unit
   cta_stamp(kDbgPrep, 2);
+  // this thread's global inputs, requested before the table staging so the
+  // round trips overlap
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = gt >> 2;
+  int2 raw = make_int2(0, 0);
+  unsigned act = 0u;
+  int surf = 0;
+  float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0;
+  if (row < st.n_tok) {
+    raw = reinterpret_cast<const int2*>(st.emb + (size_t)row * kEmbed)[gt & 3];
+    if (with_feat) {
+      act = st.action[row];
+      surf = st.surface[row];
+    }
+  } else if (row - st.n_tok < st.n_items) {
+    const float4* src = reinterpret_cast<const float4*>(st.cand + (size_t)(row - st.n_tok) * kEmbed + 8 * (gt & 3));
+    c0 = src[0];
+    c1 = src[1];
+  }
+  // action (<= 16 rows) and surface (4 rows) tables staged in shared memory:
+  // a token sums up to 16 action rows, read from here instead of one
+  // dependent global round trip per set bit
+  __shared__ __align__(16) float tab_s[(16 + 4) * kDModel];
+  if (with_feat) {
+    for (int i = threadIdx.x; i < (p.action_rows + 4) * kDModel / 4; i += blockDim.x) {
+      const int r = i / (kDModel / 4);
+      const float4* srcp = r < p.action_rows ? reinterpret_cast<const float4*>(p.action_table) + i
+                                             : reinterpret_cast<const float4*>(p.surface_table) + (i - p.action_rows * kDModel / 4);
+      reinterpret_cast<float4*>(tab_s)[r < p.action_rows ? i : 16 * kDModel / 4 + (i - p.action_rows * kDModel / 4)] =
+          __ldg(srcp);
+    }
+    __syncthreads();
+  }
+  prep_body(st, with_feat, tab_s, p.action_rows, raw, act, surf, c0, c1);
+  if (kDebug) {
+    __syncthreads();
+    cta_stamp(kDbgPrep, 1);
+  }
+}
+
+__device__ __forceinline__ void prep_body(const Staged& st, int with_feat, const float* tab_s, int action_rows,
+                                          int2 raw, unsigned act, int surf_raw, float4 v0, float4 v1) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   int i = gt >> 2;
   const int g = gt & 3;
   const unsigned qm = 0xfu << (threadIdx.x & 28);  // this quad's lanes (a quad is never split)
   if (i < st.n_tok) {
-    const int2 raw = reinterpret_cast<const int2*>(st.emb + (size_t)i * kEmbed)[g];
     const int8_t* q = reinterpret_cast<const int8_t*>(&raw);
     float d[8];
 #pragma unroll
@@ -91,25 +135,24 @@ __global__ void __launch_bounds__(256) prep_kernel(Staged st, Params p, int with
         f[j] = g < 2 ? lo : 0.0f;
         f[8 + j] = g < 2 ? hi : 0.0f;
       }
-      const unsigned act = st.action[i];
       float asum[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) asum[j] = 0.0f;
-      for (int b = 0; b < p.action_rows; ++b)
+      for (int b = 0; b < action_rows; ++b)
         if ((act >> b) & 1u) {
-          const float4* row = reinterpret_cast<const float4*>(p.action_table + b * kDModel + 16 * g);
+          const float4* row = reinterpret_cast<const float4*>(tab_s + b * kDModel + 16 * g);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const float4 v = __ldg(row + j);
+            const float4 v = row[j];
             asum[4 * j] += v.x; asum[4 * j + 1] += v.y; asum[4 * j + 2] += v.z; asum[4 * j + 3] += v.w;
           }
         }
-      const int surf = min((int)st.surface[i], 3);  // SURFACE_OTHER fold (encoder.py:178)
-      const float4* srow = reinterpret_cast<const float4*>(p.surface_table + surf * kDModel + 16 * g);
+      const int surf = min(surf_raw, 3);  // SURFACE_OTHER fold (encoder.py:178)
+      const float4* srow = reinterpret_cast<const float4*>(tab_s + (16 + surf) * kDModel + 16 * g);
       float4* fd = reinterpret_cast<float4*>(st.tok_feat + (size_t)i * kDModel + 16 * g);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float4 sv = __ldg(srow + j);
+        const float4 sv = srow[j];
         fd[j] = make_float4((f[4 * j] + asum[4 * j]) + sv.x, (f[4 * j + 1] + asum[4 * j + 1]) + sv.y,
                             (f[4 * j + 2] + asum[4 * j + 2]) + sv.z, (f[4 * j + 3] + asum[4 * j + 3]) + sv.w);
       }
@@ -118,8 +161,6 @@ __global__ void __launch_bounds__(256) prep_kernel(Staged st, Params p, int with
   }
   i -= st.n_tok;
   if (i < st.n_items) {  // l2_normalize_rows of the candidates (nnsearch.py:313-320)
-    const float4* src = reinterpret_cast<const float4*>(st.cand + (size_t)i * kEmbed + 8 * g);
-    const float4 v0 = src[0], v1 = src[1];
     const float c[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
     float nrm = __fsqrt_rn(quad_sumsq(c, qm));
     if (nrm == 0.0f) nrm = 1.0f;
