@@ -69,6 +69,11 @@ typedef struct {
   const float* candidates;    /* [n_cand, 32] f32 candidate embeddings  */
   int32_t n_cand;
   const float* ctx;           /* [ctx_dim] request context (dataset.py:282-289) */
+  /* from_store != 0: the user's sequences are read from the HBM-resident
+   * store (tav2_store_put) under store_user; emb/action/surface/len are
+   * ignored and only the candidates, ctx and plan cross PCIe. */
+  int32_t from_store;
+  uint64_t store_user;
 } tav2_request;
 
 typedef struct tav2_ctx tav2_ctx;
@@ -148,6 +153,26 @@ int tav2_kernel_times(tav2_ctx* ctx, const char** names, double* ms, int32_t* la
 
 /* Number of kernel launches the last tav2_run_staged / tav2_rank issued. */
 int tav2_last_launch_count(const tav2_ctx* ctx);
+
+/* HBM-resident feature store (FeatureStore, serving/store.py:25-72; the
+ * .tav2 bulk load of dataset.py:91-131 feeds tav2_store_put).  One slot of
+ * LIFELONG+REALTIME+IMPRESSION cap tokens per user (35 B/token: emb i8[32],
+ * action u16, surface u8) in one device pool; a request with from_store set
+ * is staged by device-to-device copies from its user's slot instead of
+ * host->device copies of its tokens.  Writes replace a user wholesale and
+ * are ordered with staging on the context's copy stream, so a staged batch
+ * always sees one consistent snapshot of each user.
+ *
+ * tav2_store_reserve: (re)allocate the pool for max_users users (drops all
+ * users).  tav2_store_put: insert or replace user_id from seqs' token
+ * columns (seqs->len within the caps: the Python mirror truncates to the
+ * newest tokens first, store.py:19-22); returns TAV2_ECAP when the pool is
+ * full.  tav2_store_remove: TAV2_EINVAL if absent.  tav2_store_count: the
+ * number of resident users (-1 on a null context). */
+int tav2_store_reserve(tav2_ctx* ctx, int32_t max_users);
+int tav2_store_put(tav2_ctx* ctx, uint64_t user_id, const tav2_request* seqs);
+int tav2_store_remove(tav2_ctx* ctx, uint64_t user_id);
+int tav2_store_count(const tav2_ctx* ctx);
 
 /* Thread-local message for the last non-zero status. */
 const char* tav2_last_error(void);

@@ -17,8 +17,8 @@ from .core import ValidationError
 HERE = os.path.dirname(os.path.abspath(__file__))
 # TAV2_DEBUG=1 selects the timeline-instrumented build (tools/*_timeline.py)
 # TAV2_LIB=x selects an A/B experiment build libtav2_x.so (build.build(variant=...))
-LIB_PATH = os.path.join(HERE, "_lib", "libtav2_debug.so" if os.environ.get("TAV2_DEBUG") == "1"
-                        else f"libtav2_{os.environ['TAV2_LIB']}.so" if os.environ.get("TAV2_LIB")
+LIB_PATH = os.path.join(HERE, "_lib", f"libtav2_{os.environ['TAV2_LIB']}.so" if os.environ.get("TAV2_LIB")
+                        else "libtav2_debug.so" if os.environ.get("TAV2_DEBUG") == "1"
                         else "libtav2.so")
 
 TAV2_OK, TAV2_EINVAL, TAV2_ECUDA, TAV2_ECAP, TAV2_ESTATE = 0, 1, 2, 3, 4
@@ -31,6 +31,7 @@ EXPORTS = (
     "tav2_last_launch_count", "tav2_last_error", "tav2_build_info", "tav2_set_profiling",
     "tav2_kernel_times", "tav2_tc_selftest", "tav2_debug_timeline", "tav2_debug_cta",
     "tav2_rank_submit", "tav2_rank_collect",
+    "tav2_store_reserve", "tav2_store_put", "tav2_store_remove", "tav2_store_count",
 )
 
 
@@ -54,6 +55,8 @@ class Request(ctypes.Structure):
         ("candidates", ctypes.c_void_p),
         ("n_cand", ctypes.c_int32),
         ("ctx", ctypes.c_void_p),
+        ("from_store", ctypes.c_int32),
+        ("store_user", ctypes.c_uint64),
     ]
 
 
@@ -93,6 +96,10 @@ def lib() -> ctypes.CDLL:
             L.tav2_rank_submit.argtypes = [vp, ctypes.POINTER(Request), ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                            vp, ctypes.POINTER(i32)]
             L.tav2_rank_collect.argtypes = [vp, ctypes.c_int, vp, vp]
+            L.tav2_store_reserve.argtypes = [vp, i32]
+            L.tav2_store_put.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(Request)]
+            L.tav2_store_remove.argtypes = [vp, ctypes.c_uint64]
+            L.tav2_store_count.argtypes = [vp]
             L.tav2_last_launch_count.argtypes = [vp]
             L.tav2_set_profiling.argtypes = [vp, ctypes.c_int]
             L.tav2_kernel_times.argtypes = [vp, ctypes.POINTER(ctypes.c_char_p),

@@ -412,8 +412,17 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
           for (int u = 0; u < 2; ++u) {
             const int jj = j + u;
             if (jj > jlast) break;
+            const long long tw0 = kDebug && dbg ? clock64() : 0;
             tmem_ld_wait();
             uint32_t* cur = u == 0 ? sa : sb;
+            if (kDebug && dbg) {  // (segment 27: cycles blocked on the chunk's TMEM load)
+              uint32_t acc = 0;
+#pragma unroll
+              for (int e = 0; e < 16; ++e) acc |= cur[e];
+              long long tw1;
+              asm volatile("mov.u64 %0, %%clock64;" : "=l"(tw1) : "r"(acc));
+              dbg[27] += tw1 - tw0;
+            }
             uint32_t* nxt = u == 0 ? sb : sa;
             if (jj + 1 <= jlast) tmem_ld16(cs + 16 * (jj + 1), nxt);  // warp-uniform
             const uint32_t vm = ok ? allowed16(valid_w[jj >> 1] >> ((jj & 1) * 16), 16 * jj, r) : 0u;

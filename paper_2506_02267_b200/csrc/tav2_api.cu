@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "tav2_common.cuh"
@@ -42,6 +43,7 @@ int fail(int code, const char* fmt, ...) {
 
 constexpr int kMinChunk = 256;    // minimum LL tokens per work unit
 constexpr int kCaps[3] = {16384, 256, 256};  // LIFELONG/REALTIME/IMPRESSION_CAP (core.py:31-33)
+constexpr int64_t kStoreSlotTok = 16384 + 256 + 256;
 
 inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 inline int cdiv(int a, int b) { return (a + b - 1) / b; }
@@ -117,6 +119,18 @@ struct tav2_ctx {
   static constexpr int kSlots = 8;
   Slot slots[kSlots];
   bool profiling = false;
+  // HBM-resident feature store (tav2_store_*): one slot of kStoreSlotTok
+  // tokens per user, column pools [users][kStoreSlotTok][...]
+  struct StoreEntry {
+    int slot;
+    int32_t len[3];
+  };
+  int8_t* st_emb = nullptr;
+  uint16_t* st_act = nullptr;
+  uint8_t* st_surf = nullptr;
+  int st_users = 0;
+  std::unordered_map<uint64_t, StoreEntry> st_map;
+  std::vector<int> st_free;
 };
 
 namespace {
@@ -170,6 +184,9 @@ int free_all(tav2_ctx* c) {
     if (c->ev_done[k]) cudaEventDestroy(c->ev_done[k]);
   }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  cudaFree(c->st_emb);
+  cudaFree(c->st_act);
+  cudaFree(c->st_surf);
   cudaFree(c->tok_unit);
   cudaFree(c->tok_img);
   cudaFree(c->cand_unit);
@@ -499,6 +516,84 @@ int tav2_load_params(tav2_ctx* c, int n, const char* const* names, const float* 
   return TAV2_OK;
 }
 
+int tav2_store_reserve(tav2_ctx* c, int32_t max_users) {
+  if (!c) return fail(TAV2_EINVAL, "null context");
+  if (max_users < 0) return fail(TAV2_EINVAL, "max_users must be >= 0");
+  CU(cudaSetDevice(c->device));
+  CU(cudaStreamSynchronize(c->copy_stream));  // pending staging copies may read the old pool
+  cudaFree(c->st_emb);
+  cudaFree(c->st_act);
+  cudaFree(c->st_surf);
+  c->st_emb = nullptr;
+  c->st_act = nullptr;
+  c->st_surf = nullptr;
+  c->st_users = 0;
+  c->st_map.clear();
+  c->st_free.clear();
+  if (max_users == 0) return TAV2_OK;
+  const int64_t n = (int64_t)max_users * kStoreSlotTok;
+  cudaError_t e;
+  if ((e = cudaMalloc(&c->st_emb, n * kEmbed)) != cudaSuccess || (e = cudaMalloc(&c->st_act, n * 2)) != cudaSuccess ||
+      (e = cudaMalloc(&c->st_surf, n)) != cudaSuccess)
+    return fail(TAV2_ECUDA, "store pool of %d users: %s", max_users, cudaGetErrorString(e));
+  c->st_users = max_users;
+  for (int i = max_users - 1; i >= 0; --i) c->st_free.push_back(i);
+  return TAV2_OK;
+}
+
+int tav2_store_put(tav2_ctx* c, uint64_t user_id, const tav2_request* q) {
+  if (!c || !q) return fail(TAV2_EINVAL, "null argument");
+  for (int k = 0; k < 3; ++k) {
+    if (q->len[k] < 0 || q->len[k] > kCaps[k])
+      return fail(TAV2_EINVAL, "source %d length %d outside [0, %d]", k, q->len[k], kCaps[k]);
+    if (q->len[k] > 0 && (!q->emb[k] || !q->action[k] || !q->surface[k]))
+      return fail(TAV2_EINVAL, "source %d has null columns", k);
+  }
+  auto it = c->st_map.find(user_id);
+  int slot;
+  if (it != c->st_map.end()) {
+    slot = it->second.slot;  // replace wholesale (ordered after earlier staging on copy_stream)
+  } else {
+    if (c->st_free.empty())
+      return fail(TAV2_ECAP, "HBM store full (%d users; tav2_store_reserve)", c->st_users);
+    slot = c->st_free.back();
+  }
+  CU(cudaSetDevice(c->device));
+  int64_t o = (int64_t)slot * kStoreSlotTok;
+  for (int k = 0; k < 3; ++k) {
+    const int64_t n = q->len[k];
+    if (!n) continue;
+    // pageable sources: each copy has consumed the caller's buffer on return
+    CU(cudaMemcpyAsync(c->st_emb + o * kEmbed, q->emb[k], n * kEmbed, cudaMemcpyHostToDevice, c->copy_stream));
+    CU(cudaMemcpyAsync(c->st_act + o, q->action[k], n * 2, cudaMemcpyHostToDevice, c->copy_stream));
+    CU(cudaMemcpyAsync(c->st_surf + o, q->surface[k], n, cudaMemcpyHostToDevice, c->copy_stream));
+    o += n;
+  }
+  if (it == c->st_map.end()) {
+    c->st_free.pop_back();
+    it = c->st_map.emplace(user_id, tav2_ctx::StoreEntry{slot, {0, 0, 0}}).first;
+  }
+  for (int k = 0; k < 3; ++k) it->second.len[k] = q->len[k];
+  return TAV2_OK;
+}
+
+int tav2_store_remove(tav2_ctx* c, uint64_t user_id) {
+  if (!c) return fail(TAV2_EINVAL, "null context");
+  auto it = c->st_map.find(user_id);
+  if (it == c->st_map.end()) return fail(TAV2_EINVAL, "user %llu is not in the HBM store", (unsigned long long)user_id);
+  c->st_free.push_back(it->second.slot);  // reuse is ordered after pending staging copies (copy_stream)
+  c->st_map.erase(it);
+  return TAV2_OK;
+}
+
+int tav2_store_count(const tav2_ctx* c) {
+  if (!c) {
+    fail(TAV2_EINVAL, "null context");
+    return -1;
+  }
+  return (int)c->st_map.size();
+}
+
 int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, int32_t* n_items) {
   if (!c || !reqs) return fail(TAV2_EINVAL, "null argument");
   if (n_req < 1) return fail(TAV2_EINVAL, "at least one request required");  // nnsearch.py:221
@@ -509,10 +604,41 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
   int N = 0;
   int64_t T = 0;
   int tiles = 0;
+  // requests served from the HBM store: their lengths come from the store,
+  // their token columns are copied device-to-device at staging time
+  std::vector<tav2_request> rq_store;
+  const tav2_ctx::StoreEntry* const no_entry = nullptr;
+  std::vector<const tav2_ctx::StoreEntry*> ent((size_t)n_req, no_entry);
+  for (int r = 0; r < n_req; ++r) {
+    if (!reqs[r].from_store) continue;
+    auto it = c->st_map.find(reqs[r].store_user);
+    if (it == c->st_map.end())
+      return fail(TAV2_EINVAL, "request %d: user %llu is not in the HBM store", r,
+                  (unsigned long long)reqs[r].store_user);
+    ent[r] = &it->second;
+  }
+  if (std::any_of(ent.begin(), ent.end(), [](const tav2_ctx::StoreEntry* e) { return e != nullptr; })) {
+    rq_store.assign(reqs, reqs + n_req);
+    for (int r = 0; r < n_req; ++r)
+      if (ent[r])
+        for (int k = 0; k < 3; ++k) {
+          rq_store[r].len[k] = ent[r]->len[k];
+          rq_store[r].emb[k] = nullptr;
+          rq_store[r].action[k] = nullptr;
+          rq_store[r].surface[k] = nullptr;
+        }
+    reqs = rq_store.data();
+  }
   for (int r = 0; r < n_req; ++r) {
     const tav2_request& q = reqs[r];
     if (q.n_cand < 1 || !q.candidates)
       return fail(TAV2_EINVAL, "each request needs a non-empty (M, E) candidate array");
+    if (ent[r]) {
+      N += q.n_cand;
+      T += (int64_t)q.len[0] + q.len[1] + q.len[2];
+      tiles += cdiv(q.n_cand, kTile);
+      continue;
+    }
     for (int k = 0; k < 3; ++k) {
       if (q.len[k] < 0 || q.len[k] > kCaps[k])
         return fail(TAV2_EINVAL, "request %d source %d length %d outside [0, %d]", r, k, q.len[k],
@@ -550,15 +676,30 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
     other += t * ((int)scanned(reqs[r], 1) + (int)scanned(reqs[r], 2));
   }
   const int ll_chunks_target = std::max(1, (c->sms - other) / std::max(tiles, 1));
+  // token placement: the host requests' tokens first (one contiguous prefix
+  // per column section, so the H2D copies skip the store requests' ranges),
+  // then the store requests'
+  std::vector<int64_t> tok_base((size_t)n_req);
+  int64_t T_host = 0;
+  {
+    int64_t o = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int r = 0; r < n_req; ++r)
+        if ((ent[r] != nullptr) == (pass == 1)) {
+          tok_base[r] = o;
+          o += (int64_t)reqs[r].len[0] + reqs[r].len[1] + reqs[r].len[2];
+          if (pass == 0) T_host = o;
+        }
+  }
   std::vector<NNTile> vt;
   std::vector<NNWork> vw;
   std::vector<int> glogs((size_t)n_req * 3, 0);
   vt.reserve(tiles);
   {
     int item = 0;
-    int64_t tok_req = 0;
     for (int r = 0; r < n_req; ++r) {
       const tav2_request& q = reqs[r];
+      const int64_t tok_req = tok_base[r];
       int64_t tok_off[3];
       for (int s = 0, o = 0; s < 3; ++s) {
         tok_off[s] = tok_req + o;
@@ -590,7 +731,6 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
         vt.push_back(t);
       }
       item += q.n_cand;
-      tok_req += (int64_t)q.len[0] + q.len[1] + q.len[2];
     }
   }
   if ((int)vt.size() > c->max_tiles || (int)vw.size() > c->max_work)
@@ -610,6 +750,8 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
   p.off_item_req = o; o = align256(o + (int64_t)N * 4);
   p.off_ctx = o; o = align256(o + (int64_t)n_req * kCtx * 4);
   p.off_cand = o; o = align256(o + (int64_t)N * kEmbed * 4);
+  p.n_scopy = (int)std::count_if(ent.begin(), ent.end(), [](const tav2_ctx::StoreEntry* e) { return e != nullptr; });
+  p.off_scopy = o; o = align256(o + (int64_t)p.n_scopy * sizeof(StoreCopy));
   p.off_action = o; o = align256(o + T * 2);
   p.off_surface = o; o = align256(o + T);
   p.off_emb = o; o = align256(o + T * kEmbed);
@@ -627,10 +769,18 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
   uint16_t* act = reinterpret_cast<uint16_t*>(h + p.off_action);
   uint8_t* surf = h + p.off_surface;
   int8_t* emb = reinterpret_cast<int8_t*>(h + p.off_emb);
+  StoreCopy* scopy = reinterpret_cast<StoreCopy*>(h + p.off_scopy);
+  int max_store_tok = 0;
+  for (int r = 0, j = 0; r < n_req; ++r)
+    if (ent[r]) {
+      const int n = reqs[r].len[0] + reqs[r].len[1] + reqs[r].len[2];
+      scopy[j++] = StoreCopy{(int64_t)ent[r]->slot * kStoreSlotTok, tok_base[r], n, 0};
+      max_store_tok = std::max(max_store_tok, n);
+    }
   int item = 0;
-  int64_t tok = 0;
   for (int r = 0; r < n_req; ++r) {
     const tav2_request& q = reqs[r];
+    int64_t tok = tok_base[r];
     ri[r].item_off = item;
     ri[r].n_items = q.n_cand;
     ri[r].pad_ = 0;
@@ -638,7 +788,7 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
       ri[r].tok_off[s] = (int32_t)tok;
       ri[r].len[s] = q.len[s];
       ri[r].glog[s] = glogs[r * 3 + s];
-      if (q.len[s]) {
+      if (q.len[s] && !ent[r]) {
         memcpy(emb + tok * kEmbed, q.emb[s], (size_t)q.len[s] * kEmbed);
         memcpy(act + tok, q.action[s], (size_t)q.len[s] * 2);
         memcpy(surf + tok, q.surface[s], (size_t)q.len[s]);
@@ -659,7 +809,23 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
   CU(cudaSetDevice(c->device));
   // the device region is rewritten once the kernels that read it last finished
   CU(cudaStreamWaitEvent(c->copy_stream, c->ev_done[slot], 0));
-  CU(cudaMemcpyAsync(c->d_staged[slot], h, p.bytes, cudaMemcpyHostToDevice, c->copy_stream));
+  unsigned char* d = c->d_staged[slot];
+  if (T_host == T) {
+    CU(cudaMemcpyAsync(d, h, p.bytes, cudaMemcpyHostToDevice, c->copy_stream));
+  } else {  // header + the host tokens' prefix of each column section
+    CU(cudaMemcpyAsync(d, h, p.off_action, cudaMemcpyHostToDevice, c->copy_stream));
+    if (T_host > 0) {
+      CU(cudaMemcpyAsync(d + p.off_action, h + p.off_action, T_host * 2, cudaMemcpyHostToDevice, c->copy_stream));
+      CU(cudaMemcpyAsync(d + p.off_surface, h + p.off_surface, T_host, cudaMemcpyHostToDevice, c->copy_stream));
+      CU(cudaMemcpyAsync(d + p.off_emb, h + p.off_emb, T_host * kEmbed, cudaMemcpyHostToDevice, c->copy_stream));
+    }
+    // the store users' tokens, device to device: one gather launch over the
+    // copy descriptors (staged with the header)
+    CU(launch_store_gather(reinterpret_cast<const StoreCopy*>(d + p.off_scopy), p.n_scopy, max_store_tok,
+                           c->st_emb, c->st_act, c->st_surf, reinterpret_cast<int8_t*>(d + p.off_emb),
+                           reinterpret_cast<uint16_t*>(d + p.off_action), d + p.off_surface, c->copy_stream));
+    c->launches++;
+  }
   CU(cudaEventRecord(c->ev_staged[slot], c->copy_stream));
   CU(cudaStreamWaitEvent(s, c->ev_staged[slot], 0));
   c->plans[slot] = p;

@@ -78,10 +78,17 @@ struct NNScan {
 
 struct Plan {
   int32_t n_req, n_items, n_tok;
-  int32_t n_tiles, n_work, tile_size, pad_;
+  int32_t n_tiles, n_work, tile_size, n_scopy;
   // byte offsets inside the staged region
-  int64_t off_req, off_tiles, off_work, off_item_req, off_ctx, off_cand, off_action,
+  int64_t off_req, off_tiles, off_work, off_item_req, off_ctx, off_cand, off_scopy, off_action,
       off_surface, off_emb, bytes;
+};
+
+// One HBM-store user's token run copied into the staged token columns
+// (store_gather_kernel): tokens [src, src + n) of the store pool -> [dst, dst + n).
+struct StoreCopy {
+  int64_t src, dst;
+  int32_t n, pad_;
 };
 
 // Device view of the model parameters (all f32, reference names in
@@ -227,6 +234,9 @@ cudaError_t launch_skut_tc3(const Params& p, const SkutImages3& img, const NNCfg
 cudaError_t launch_nn_scan(const Staged& st, const NNCfg& nn, const NNScan& sc, int pass,
                            cudaStream_t s);
 cudaError_t launch_nn_bound(const Staged& st, const NNCfg& nn, const NNScan& sc, cudaStream_t s);
+cudaError_t launch_store_gather(const StoreCopy* d, int n, int max_tok, const int8_t* semb,
+                                const uint16_t* sact, const uint8_t* ssurf, int8_t* demb, uint16_t* dact,
+                                uint8_t* dsurf, cudaStream_t s);
 cudaError_t launch_nn_select(const Staged& st, const NNCfg& nn, const NNScan& sc, int32_t* idx,
                              float* scores, cudaStream_t s);
 cudaError_t set_debug_timeline(long long* dev, int block);

@@ -129,3 +129,69 @@ def log_nn_features(users, idx: np.ndarray, offsets, cfg) -> list[bytes]:
     from .nnsearch import assembled_from_indices
 
     return [pack_assembled(assembled_from_indices(users[o], idx[i], cfg)) for i, o in enumerate(offsets)]
+
+
+# ---------------------------------------------------------------------------
+# Sequence store (.tav2): bulk source of the HBM-resident feature store
+# (serving.DeviceFeatureStore.load).  Byte format of dataset.py:85-131:
+# <4sHQ> (magic, version, user count), then per user <QHHH> (user id,
+# ll/rt/imp lengths) followed by the three packed token blocks.
+# ---------------------------------------------------------------------------
+
+STORE_MAGIC = b"TAV2"
+FORMAT_VERSION = 1
+
+
+class FormatError(ValueError):
+    """Malformed store file; the message carries the byte offset (dataset.py:44-46)."""
+
+
+def unpack_token_block(buf: bytes, offset: int, count: int, embed_dim: int = EMBED_DIM):
+    dt = token_record_dtype(embed_dim)
+    end = offset + count * dt.itemsize
+    if end > len(buf):
+        raise FormatError(f"token block truncated at byte {offset}")
+    rec = np.frombuffer(buf, dtype=dt, count=count, offset=offset)
+    return TokenBlock(rec["ts"], rec["action"], rec["surface"], rec["emb"]), end
+
+
+def write_store(path, users) -> None:
+    """Write (user_id, UserSequences) pairs; validates every record (dataset.py:90-103)."""
+    import struct
+
+    with open(path, "wb") as fh:
+        fh.write(struct.pack("<4sHQ", STORE_MAGIC, FORMAT_VERSION, len(users)))
+        for user_id, seqs in users:
+            seqs.validate()
+            fh.write(struct.pack("<QHHH", user_id, len(seqs.lifelong), len(seqs.realtime), len(seqs.impression)))
+            for blk in seqs.blocks():
+                fh.write(pack_token_block(blk))
+
+
+def read_store(path) -> list:
+    """Read a .tav2 store back into (user_id, UserSequences) pairs (dataset.py:106-131)."""
+    import struct
+    from pathlib import Path
+
+    buf = Path(path).read_bytes()
+    fh, uh = struct.Struct("<4sHQ"), struct.Struct("<QHHH")
+    if len(buf) < fh.size:
+        raise FormatError(f"store header truncated at byte {len(buf)}")
+    magic, version, count = fh.unpack_from(buf, 0)
+    if magic != STORE_MAGIC:
+        raise FormatError(f"bad store magic {magic!r} at byte 0")
+    if version != FORMAT_VERSION:
+        raise FormatError(f"unsupported store version {version} at byte 4")
+    users, pos = [], fh.size
+    for _ in range(count):
+        if pos + uh.size > len(buf):
+            raise FormatError(f"user record truncated at byte {pos}")
+        user_id, n_ll, n_rt, n_imp = uh.unpack_from(buf, pos)
+        pos += uh.size
+        ll, pos = unpack_token_block(buf, pos, n_ll)
+        rt, pos = unpack_token_block(buf, pos, n_rt)
+        imp, pos = unpack_token_block(buf, pos, n_imp)
+        users.append((user_id, UserSequences(ll, rt, imp)))
+    if pos != len(buf):
+        raise FormatError(f"{len(buf) - pos} trailing bytes at byte {pos}")
+    return users

@@ -35,23 +35,39 @@ def _cfg_struct(mc: ModelConfig) -> N.Config:
                     nn.k_impression)
 
 
+@dataclass(frozen=True)
+class StoreUser:
+    """A request's user read from the engine's HBM-resident store
+    (``Engine.store_put``) instead of host token columns."""
+
+    user_id: int
+
+
+def _columns(user: UserSequences, r, keep) -> None:
+    for s, blk in enumerate(user.blocks()):
+        emb = np.ascontiguousarray(blk.embeddings, np.int8)
+        act = np.ascontiguousarray(blk.actions, np.uint16)
+        surf = np.ascontiguousarray(blk.surfaces, np.uint8)
+        if emb.ndim != 2 or emb.shape[1] != EMBED_DIM:
+            raise ValidationError(f"token embeddings must be (n, {EMBED_DIM}) int8")
+        keep += [emb, act, surf]
+        r.emb[s], r.action[s], r.surface[s] = emb.ctypes.data, act.ctypes.data, surf.ctypes.data
+        r.len[s] = len(blk)
+
+
 class _Pack:
-    """Keeps the numpy columns of a request list alive across a native call."""
+    """Keeps the numpy columns of a request list alive across a native call.
+    A request's user is a UserSequences (host columns) or a StoreUser."""
 
     def __init__(self, requests):
         self.keep = []
         self.arr = (N.Request * len(requests))()
         for i, (user, cands, ctx) in enumerate(requests):
             r = self.arr[i]
-            for s, blk in enumerate(user.blocks()):
-                emb = np.ascontiguousarray(blk.embeddings, np.int8)
-                act = np.ascontiguousarray(blk.actions, np.uint16)
-                surf = np.ascontiguousarray(blk.surfaces, np.uint8)
-                if emb.ndim != 2 or emb.shape[1] != EMBED_DIM:
-                    raise ValidationError(f"token embeddings must be (n, {EMBED_DIM}) int8")
-                self.keep += [emb, act, surf]
-                r.emb[s], r.action[s], r.surface[s] = emb.ctypes.data, act.ctypes.data, surf.ctypes.data
-                r.len[s] = len(blk)
+            if isinstance(user, StoreUser):
+                r.from_store, r.store_user = 1, int(user.user_id)
+            else:
+                _columns(user, r, self.keep)
             c = np.ascontiguousarray(cands, np.float32)
             if c.ndim != 2 or c.shape[1] != EMBED_DIM:
                 raise ValidationError(f"candidates must be (n, {EMBED_DIM}) float32")
@@ -124,8 +140,27 @@ class Engine:
     def stream(self) -> int:
         return torch.cuda.current_stream(self.torch_device).cuda_stream
 
+    # ------------------------------------------------------------------
+    # HBM-resident feature store (tav2_store_*; serving.DeviceFeatureStore
+    # is the FeatureStore-shaped front end)
+    def store_reserve(self, max_users: int) -> None:
+        """(Re)allocate the device pool for max_users users (drops all)."""
+        N.check(self._lib.tav2_store_reserve(self._ctx, int(max_users)))
+
+    def store_put(self, user_id: int, user: UserSequences) -> None:
+        """Insert or replace a user's sequences in HBM (lengths within the caps)."""
+        r, keep = N.Request(), []
+        _columns(user, r, keep)
+        N.check(self._lib.tav2_store_put(self._ctx, int(user_id), ctypes.byref(r)))
+
+    def store_remove(self, user_id: int) -> None:
+        N.check(self._lib.tav2_store_remove(self._ctx, int(user_id)))
+
+    def store_count(self) -> int:
+        return int(self._lib.tav2_store_count(self._ctx))
+
     def stage(self, requests) -> int:
-        """requests: list of (UserSequences, candidates[M,32], ctx[8] | None)."""
+        """requests: list of (UserSequences | StoreUser, candidates[M,32], ctx[8] | None)."""
         pack = _Pack(requests)
         n = ctypes.c_int32()
         N.check(self._lib.tav2_stage(self._ctx, pack.arr, len(requests), self.stream(),
