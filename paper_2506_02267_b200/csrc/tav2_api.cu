@@ -7,6 +7,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <cmath>
 #include <string.h>
 
 #include <string>
@@ -105,6 +106,9 @@ struct tav2_ctx {
   uint8_t* d_images3 = nullptr;  // folded images of skut_tc3 (Wqk, Wvo)
   SkutImages3 images3{};
   bool params_ok = false;
+  // Cauchy-Schwarz softmax shift range (tensor-core SKUTs): exponents stay
+  // >= -2 m' with m' <= cs_bound*; usable while 2 m' <= 120 (ex2 range)
+  double cs_bound3 = 0.0, cs_bound = 0.0;
   // current batch: plans[cur]
   bool staged = false;
   int launches = 0;
@@ -134,6 +138,31 @@ struct tav2_ctx {
 };
 
 namespace {
+
+// largest singular value of a 64x64 row-major matrix (power iteration on MᵀM)
+double spectral_norm64(const std::vector<double>& m) {
+  std::vector<double> v(64, 1.0 / 8.0), u(64), w(64);
+  double sig = 0.0;
+  for (int it = 0; it < 200; ++it) {
+    for (int i = 0; i < 64; ++i) {
+      double a = 0.0;
+      for (int j = 0; j < 64; ++j) a += m[i * 64 + j] * v[j];
+      u[i] = a;
+    }
+    double nw = 0.0;
+    for (int j = 0; j < 64; ++j) {
+      double a = 0.0;
+      for (int i = 0; i < 64; ++i) a += m[i * 64 + j] * u[i];
+      w[j] = a;
+      nw += a * a;
+    }
+    nw = std::sqrt(nw);
+    if (nw == 0.0) return 0.0;
+    for (int j = 0; j < 64; ++j) v[j] = w[j] / nw;
+    sig = std::sqrt(nw);
+  }
+  return sig * 1.0001;  // power iteration approaches from below
+}
 
 Staged staged_view(tav2_ctx* c) {
   Staged s{};
@@ -480,6 +509,7 @@ int tav2_load_params(tav2_ctx* c, int n, const char* const* names, const float* 
   // ---- folded images of skut_tc3: per layer [ [Wqk|Wvo]^T | W1^T | W2^T ] ----
   // Wqk = Wq Wk^T * log2(e)/8 (scores in the exp2 domain), Wvo = Wv Wo; f64
   // products rounded once to f32 before the bf16 hi/lo split.
+  c->cs_bound3 = c->cs_bound = 0.0;
   {
     const size_t lay = (size_t)kImg3WA + kImg3WB;
     const size_t bytes3 = (size_t)L * lay + kImg3WO;
@@ -498,6 +528,26 @@ int tav2_load_params(tav2_ctx* c, int n, const char* const* names, const float* 
           wqk[i * 64 + j] = (float)(a * sc);
           wvo[i * 64 + j] = (float)b;
         }
+      // softmax-shift range of this layer: m' = ||q'_r|| max_j ||a_j|| <=
+      // ||Wqk||_2 A^2 (folded, skut_tc3) or ||Wq||_2 ||Wk||_2 A^2 log2e/8
+      // (skut_tc), with A = max|ln1_scale| sqrt(d) + ||ln1_shift||_2 >= ||a||
+      {
+        const float *g = host_of(P.ln1_scale[l]), *bt = host_of(P.ln1_shift[l]);
+        double gm = 0.0, bn = 0.0;
+        for (int i = 0; i < 64; ++i) {
+          gm = std::max(gm, std::fabs((double)g[i]));
+          bn += (double)bt[i] * bt[i];
+        }
+        const double A = gm * 8.0 + std::sqrt(bn);
+        std::vector<double> m1(64 * 64), m2(64 * 64), m3(64 * 64);
+        for (int i = 0; i < 64 * 64; ++i) {
+          m1[i] = wqk[i];
+          m2[i] = wq[i];
+          m3[i] = wk[i];
+        }
+        c->cs_bound3 = std::max(c->cs_bound3, spectral_norm64(m1) * A * A);
+        c->cs_bound = std::max(c->cs_bound, spectral_norm64(m2) * spectral_norm64(m3) * sc * A * A);
+      }
       uint8_t* base = img3.data() + (size_t)l * lay;
       put(base, 128, 64, 0, wqk.data(), 64, 64);
       put(base, 128, 64, 64, wvo.data(), 64, 64);
@@ -874,13 +924,16 @@ int run_score(tav2_ctx* c, int mode, const int32_t* idx, float* logits, float* p
   // The 2-row-tile tensor-core SKUT holds K/V of <= 256 keys in shared
   // memory; longer sequences (the k_ll = 256 sweep point, S = 352) run the
   // SIMT kernel, which is f32 throughout and so also meets the bf16 budget.
-  if (mode == TAV2_MODE_BF16 && skut_tc3_supported(c->nn, c->params)) {
+  // tensor-core SKUTs only while their single-pass softmax shift provably
+  // stays in the exp2 range (2 m' <= 120); the SIMT kernel keeps a running max
+  const bool tc3_ok = c->cs_bound3 <= 60.0, tc_ok = c->cs_bound <= 60.0;
+  if (mode == TAV2_MODE_BF16 && tc3_ok && skut_tc3_supported(c->nn, c->params)) {
     CU(timed(c, "skut_tc3", s, [&] {
       return launch_skut_tc3(c->params, c->images3, c->nn, st, idx, st.n_items, logits, pooled, s);
     }));
     return TAV2_OK;
   }
-  if (mode == TAV2_MODE_BF16 && c->nn.seq_len <= 256) {
+  if (mode == TAV2_MODE_BF16 && tc_ok && c->nn.seq_len <= 256) {
     CU(timed(c, "skut_tc", s, [&] {
       return launch_skut_tc(c->params, c->images, c->nn, &st, idx, nullptr, nullptr, st.n_items,
                             nullptr, logits, pooled, s);
@@ -931,7 +984,7 @@ int tav2_forward(tav2_ctx* c, int mode, const float* features_dev, const uint8_t
   if (n == 0) return TAV2_OK;
   if (!features_dev || !mask_dev || !u_dev) return fail(TAV2_EINVAL, "null device pointer");
   CU(cudaSetDevice(c->device));
-  if (mode == TAV2_MODE_BF16 && c->nn.seq_len <= 256) {
+  if (mode == TAV2_MODE_BF16 && c->cs_bound <= 60.0 && c->nn.seq_len <= 256) {
     CU(launch_skut_tc(c->params, c->images, c->nn, nullptr, nullptr, features_dev, mask_dev, n,
                       u_dev, nullptr, nullptr, (cudaStream_t)stream));
     return TAV2_OK;

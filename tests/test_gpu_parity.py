@@ -266,3 +266,27 @@ def test_gpu_nn_feature_log_matches_reference_bytes(case):
     same = sum(rec == blob[off[i]:off[i + 1]] for i, rec in enumerate(recs))
     tie_items = int(np.sum(np.any(idx != z["idx"], axis=1)))
     assert same == len(recs) - tie_items and tie_items <= max(1, len(recs) // 50), (same, len(recs), tie_items)
+
+
+def test_softmax_shift_guard_falls_back_to_running_max():
+    """Weights whose LN1 gain / Wq scale push the Cauchy-Schwarz shift bound
+    ||Wqk|| A^2 past the exp2-safe range (2 m' > 120) must not run the
+    single-pass tensor-core softmax: the SIMT kernel (running max) scores
+    them, still within the bf16 budget of the oracle."""
+    nn = P.NNConfig()
+    model = P.RankingModel.init(P.ModelConfig.for_nn(nn), seed=2)
+    Pd = orc.model_init(2, seq_len=nn.seq_len)
+    for i, layer in enumerate(model.encoder.layers):
+        layer.ln1_scale = layer.ln1_scale * 4.0
+        layer.wq = layer.wq * 2.0
+        Pd[f"encoder.layer{i}.ln1_scale"] = Pd[f"encoder.layer{i}.ln1_scale"] * 4.0
+        Pd[f"encoder.layer{i}.wq"] = Pd[f"encoder.layer{i}.wq"] * 2.0
+    eng = Engine(model, capacity=Capacity(2, 256, 2 * 16896))
+    r = P.generate_requests(1, 64, ll_tokens=2048, seed=4)[0]
+    eng.set_profiling(True)
+    logits = eng.rank_requests([(r.user, r.candidates, r.ctx)], mode="bf16")
+    kt = eng.kernel_times()
+    eng.set_profiling(False)
+    assert "skut_simt" in kt and "skut_tc3" not in kt and "skut_tc" not in kt, kt
+    ref = orc.rank_request(from_user(r.user), r.candidates, r.ctx, Pd, (32, 96, 32, 32))
+    assert np.abs(logits - ref).max() <= TOL["bf16"]
