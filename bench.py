@@ -177,9 +177,27 @@ def cpu_baseline(cfg_name, steps=3, warmup=1, budget_s=60.0, procs=None, n_per_p
         "sample": (f"{procs} processes x {k} steps x {n} candidates of one L={L} request "
                    f"(oracle port of build_dedup_batch->fused_assemble->encode_batch->forward_fused"
                    f"->pool->head, OPENBLAS_NUM_THREADS=1); {wall:.1f}s timed wall"),
-        "per_process_cand_s": n / statistics.median(lats),
-        "p50_sample_ms": 1e3 * statistics.median(lats),
+        "per_process_cand_s": round(n / statistics.median(lats), 1),
+        "p50_sample_ms": round(1e3 * _nearest_rank(lats, 50), 2),
+        "p99_sample_ms": round(1e3 * _nearest_rank(lats, 99), 2),
+        "cpu_model": _cpu_model(),
     }
+
+
+def _nearest_rank(values, p):
+    v = sorted(values)
+    return v[min(len(v), max(1, -(-p * len(v) // 100))) - 1]
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 # ---------------------------------------------------------------------------
@@ -407,7 +425,9 @@ def main():
             "config": {"workload": f"{args.config}: {n_req} request(s) x {n_cand} candidates, L={L}, "
                                    f"NNConfig{nn_t} (CPU: bounded candidate sample per process)"},
             "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cb["cores"],
-                             "kind": "port", "sample": cb["sample"]},
+                             "kind": "port", "sample": cb["sample"], "cpu_model": cb["cpu_model"],
+                             "per_process_cand_s": cb["per_process_cand_s"],
+                             "p50_sample_ms": cb["p50_sample_ms"], "p99_sample_ms": cb["p99_sample_ms"]},
             "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
         }))
@@ -420,7 +440,8 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_baseline(args.config, steps=3, warmup=1, budget_s=20.0)
-            out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
+                                                       "per_process_cand_s", "p50_sample_ms", "p99_sample_ms")}
         print(json.dumps(out))
     if world > 1:
         import torch.distributed as dist
