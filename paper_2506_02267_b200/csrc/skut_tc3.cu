@@ -329,6 +329,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       stamp(3);
       if (issuer) {  // M1: [Q' | V'] = A [Wqk | Wvo]   (N = 128, K = 64)
         issuer_wait_simt();
+        stamp(28);
         t3_mma3(R + kCD, R + kCA, 32, wa(L), wa(L) + kImg3WA / 2, 128 * 16, 4, idesc_bf16(128, 128));
         commit(&t3.mma[t]);
       }
@@ -461,6 +462,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       stamp(9);
       if (issuer) {  // M3: O' = P V'   (N = 64, K = keys; V' MN-major)
         issuer_wait_simt();
+        stamp(29);
         const uint32_t id = idesc_bf16(128, 64, 0, 1);
         for (int j = 0; j < NK / 16; ++j) {
           const uint64_t bh = sdesc(vhi + 2 * j * 1024, 1024, 128);
@@ -500,6 +502,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       stamp(12);
       if (issuer) {  // M4: H = A W1   (N = 32, K = 64)
         issuer_wait_simt();
+        stamp(30);
         t3_mma3(R + kCD, R + kCA, 32, wb(L), wb(L) + 4096, 32 * 16, 4, idesc_bf16(128, 32));
         commit(&t3.mma[t]);
       }

@@ -17,7 +17,8 @@ NAMES = ["encode", "encode barrier", "kvfree wait", "P1 LN1->A,K", "issue M1 QV'
          "P2 Q'->A,V'->smem", "kvready+issue M2 S", "wait M2", "P3 softmax", "issue M3 PV",
          "wait M3", "P4 x+=O'/l,LN2", "issue M4 W1", "wait M4", "P5 ReLU", "issue M5 W2", "wait M5",
          "P6 x+=", "pool x->A", "issue pool", "wait pool", "max-pool+barriers", "head",
-         "P3a kvready wait", "P3b exp loop", "P3c zero fill", "(in P3b: TMEM load wait)"]
+         "P3a kvready wait", "P3b exp loop", "P3c zero fill", "(in P3b: TMEM load wait)",
+         "M1 simt wait", "M3 simt wait", "M4 simt wait"]
 
 n_cand = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
 nn = P.NNConfig()
@@ -38,7 +39,7 @@ t = buf.cpu().numpy()[640:704]
 for tile in (0, 1):
     s = t[32 * tile: 32 * tile + 32]
     items = max(int(s[31]), 1)
-    tot = sum(int(v) for v in s[:27])
+    tot = sum(int(v) for v in s[:27]) + sum(int(v) for v in s[28:31])
     print(f"tile {tile}: {items} items, {tot / items:.0f} cycles/item")
     for i, nm in enumerate(NAMES):
         print(f"  {i:2d} {nm:20s} {s[i] / items:8.0f} cyc/item  {100 * s[i] / max(tot, 1):5.1f}%")
