@@ -41,14 +41,16 @@ __device__ __forceinline__ uint64_t winner_key(uint64_t key) {
 
 // reference score: f64 dot of the f32 unit vectors (nnsearch.py:344-347);
 // four independent chains in a fixed order, so equal rows score equal
-__device__ __forceinline__ double dot_exact(const float4* r, const double* uc) {
+// (both operands converted on the fly: a register-resident f64 copy of the
+// candidate costs 64 registers, i.e. select-kernel occupancy)
+__device__ __forceinline__ double dot_exact(const float4* r, const float* uc) {
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
   for (int q4 = 0; q4 < 8; ++q4) {
-    a0 = fma((double)r[q4].x, uc[4 * q4], a0);
-    a1 = fma((double)r[q4].y, uc[4 * q4 + 1], a1);
-    a2 = fma((double)r[q4].z, uc[4 * q4 + 2], a2);
-    a3 = fma((double)r[q4].w, uc[4 * q4 + 3], a3);
+    a0 = fma((double)r[q4].x, (double)uc[4 * q4], a0);
+    a1 = fma((double)r[q4].y, (double)uc[4 * q4 + 1], a1);
+    a2 = fma((double)r[q4].z, (double)uc[4 * q4 + 2], a2);
+    a3 = fma((double)r[q4].w, (double)uc[4 * q4 + 3], a3);
   }
   return (a0 + a1) + (a2 + a3);
 }
@@ -57,7 +59,7 @@ struct KeySrc {  // survivors of one (candidate, source)
   const uint16_t* surv;  // scan survivor list, or null: every token from `first` on
   int first;
   const float* tok;  // the source's f32 unit rows
-  double uc[kEmbed];  // the candidate's unit row, converted once
+  float uc[kEmbed];  // the candidate's unit row
   __device__ __forceinline__ int token(int i) const { return surv ? (int)surv[i] : first + i; }
   __device__ __forceinline__ uint64_t key(int i) const {
     const int t = token(i);
@@ -558,17 +560,15 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
   ks.surv = scanned ? sc.surv + (size_t)item * sc.surv_stride + (rq.tok_off[s] - rq.tok_off[0]) : nullptr;
   ks.first = lo;
   ks.tok = st.tok_unit + (size_t)rq.tok_off[s] * kEmbed;
-  float ucf[kEmbed];
   {
     const float4* cu = reinterpret_cast<const float4*>(st.cand_unit + (size_t)item * kEmbed);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float4 q = __ldg(cu + j);
-      ucf[4 * j] = q.x; ucf[4 * j + 1] = q.y; ucf[4 * j + 2] = q.z; ucf[4 * j + 3] = q.w;
+      ks.uc[4 * j] = q.x; ks.uc[4 * j + 1] = q.y; ks.uc[4 * j + 2] = q.z; ks.uc[4 * j + 3] = q.w;
     }
-#pragma unroll
-    for (int j = 0; j < kEmbed; ++j) ks.uc[j] = ucf[j];
   }
+  const float* ucf = ks.uc;
   const int n = scanned ? min((int)sc.count[(size_t)item * 3 + s], hi - lo) : hi - lo;
   const long long t_start = kDebug ? gtimer() : 0;
   uint64_t* a = keys_s[warp];
