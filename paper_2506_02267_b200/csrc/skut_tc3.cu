@@ -408,25 +408,20 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         // flight while this one is exponentiated (2-deep software pipeline)
         uint32_t sa[16], sb[16];
         tmem_ld16(cs, sa);
+        // key-validity word of the chunk pair, read one pair ahead (its
+        // shared-memory latency otherwise sits on every chunk's mask)
+        uint32_t vw_cur = valid_w[0];
         for (int j = 0; j <= jlast; j += 2) {
+          const uint32_t vw_next = valid_w[min((j >> 1) + 1, 7)];
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const int jj = j + u;
             if (jj > jlast) break;
-            const long long tw0 = kDebug && dbg ? clock64() : 0;
             tmem_ld_wait();
             uint32_t* cur = u == 0 ? sa : sb;
-            if (kDebug && dbg) {  // (segment 27: cycles blocked on the chunk's TMEM load)
-              uint32_t acc = 0;
-#pragma unroll
-              for (int e = 0; e < 16; ++e) acc |= cur[e];
-              long long tw1;
-              asm volatile("mov.u64 %0, %%clock64;" : "=l"(tw1) : "r"(acc));
-              dbg[27] += tw1 - tw0;
-            }
             uint32_t* nxt = u == 0 ? sb : sa;
             if (jj + 1 <= jlast) tmem_ld16(cs + 16 * (jj + 1), nxt);  // warp-uniform
-            const uint32_t vm = ok ? allowed16(valid_w[jj >> 1] >> ((jj & 1) * 16), 16 * jj, r) : 0u;
+            const uint32_t vm = ok ? allowed16(vw_cur >> (u * 16), 16 * jj, r) : 0u;
             float pv[16];
 #pragma unroll
             for (int e = 0; e < 16; e += 2) {  // p = exp2(s - m'), masked keys -> 0
@@ -444,6 +439,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
             tmem_st8(cs + 16 * jj, hi);
             tmem_st8(cs + 16 * jj + 8, lo);
           }
+          vw_cur = vw_next;
         }
         stamp(25);
         {  // chunks past the warp's causal bound: P = 0 (the P.V MMA reads all NK keys)
