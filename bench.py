@@ -41,6 +41,9 @@ CONFIGS = {
     "c2": (1, 1000, 16384, (32, 96, 32, 32)),
     "c1": (1, 64, 1024, (32, 32, 0, 0)),
     "c3": (32, 500, 16384, (32, 96, 32, 32)),
+    # long tail: one request's 8,192 candidates split across the ranks, one
+    # NCCL all-gather of the logits per step (strong scaling)
+    "c4": (1, 8192, 16384, (32, 96, 32, 32)),
 }
 
 
@@ -215,18 +218,42 @@ def run_gpu(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     n_req, n_cand, L, nn_t = CONFIGS[args.config]
+    split = args.config == "c4"  # candidate split of one request (parallel.rank_split's layout)
+    n_total = n_cand
+    if split:
+        from paper_2506_02267_b200.parallel import split_bounds
+
+        c_lo, c_hi = split_bounds(n_cand, world)[rank]
+        width = max(h - l for l, h in split_bounds(n_cand, world))
+        n_cand = c_hi - c_lo
     nn = P.NNConfig(*nn_t)
     model = P.RankingModel.init(P.ModelConfig.for_nn(nn), seed=0)
-    cap = Capacity(n_req, n_req * n_cand, n_req * (L + 512))
+    cap = Capacity(n_req, n_req * n_total, n_req * (L + 512))
     eng = Engine(model, capacity=cap, device=local_rank)
-    # a pool of distinct requests per rank (different seeds per rank)
+    # a pool of distinct requests per rank (different seeds per rank); the
+    # candidate split shares one request across the ranks
     pool_n = max(2, args.pool)
-    pool = [P.generate_requests(n_req, n_cand, ll_tokens=L, seed=1000 * rank + i) for i in range(pool_n)]
-    packed = [[(r.user, r.candidates, r.ctx) for r in reqs] for reqs in pool]
+    pool = [P.generate_requests(n_req, n_total, ll_tokens=L, seed=(0 if split else 1000 * rank) + i)
+            for i in range(pool_n)]
+    if split:
+        packed = [[(r.user, r.candidates[c_lo:c_hi], r.ctx) for r in reqs] for reqs in pool]
+    else:
+        packed = [[(r.user, r.candidates, r.ctx) for r in reqs] for reqs in pool]
     mode = args.mode
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     logits = torch.empty((n_req * n_cand, 4), dtype=torch.float32, device=dev)
+    gather = split and world > 1
+    if gather:  # padded slices -> one all_gather_into_tensor (parallel.rank_split)
+        send = torch.zeros((width, 4), dtype=torch.float32, device=dev)
+        recv = torch.empty((world * width, 4), dtype=torch.float32, device=dev)
+
+    def step():
+        if gather:
+            eng.run_staged(mode, send[:n_cand])
+            dist.all_gather_into_tensor(recv, send)
+        else:
+            eng.run_staged(mode, logits)
 
     def barrier():
         if world > 1:
@@ -235,7 +262,7 @@ def run_gpu(args, rank, world, local_rank):
     # ---- device-resident throughput (value) ----
     eng.stage(packed[0])
     for _ in range(args.warmup):
-        eng.run_staged(mode, logits)
+        step()
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -245,7 +272,7 @@ def run_gpu(args, rank, world, local_rank):
         for i in range(args.steps):
             flush.fill_(float(i))  # evict the previous step's working set from L2 (untimed)
             starts[i].record()
-            eng.run_staged(mode, logits)
+            step()
             ends[i].record()
         torch.cuda.synchronize()
     barrier()
@@ -269,7 +296,8 @@ def run_gpu(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
     cand_step = n_req * n_cand
-    value = world * cand_step * args.steps / (max_ms / 1e3)
+    job_cand = n_req * n_total if split else world * cand_step  # candidates all ranks score per step
+    value = job_cand * args.steps / (max_ms / 1e3)
 
     # ---- end-to-end through the public API (host buffers, H2D + D2H inside) ----
     # (a) the serving loop Engine.rank_pipelined: every step's host packing,
@@ -286,7 +314,7 @@ def run_gpu(args, rank, world, local_rank):
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * cand_step * args.steps / float(te.item())
+    e2e_value = job_cand * args.steps / float(te.item())
     for i in range(min(args.warmup, 5)):
         eng.rank_requests(packed[i % pool_n], mode=mode)
     torch.cuda.synchronize()
@@ -348,14 +376,16 @@ def run_gpu(args, rank, world, local_rank):
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if split else "weak", "vs_baseline": None,
         "dtype": ("bf16x3 split GEMMs on tcgen05 (f32 accumulate); NN: fp16 tcgen05 scan + f64 exact "
                   "re-scoring" if mode == "bf16" else "fp32 SIMT transformer; NN: fp16 scan + f64 re-scoring"),
         "mode": mode, "data": "synthetic (generate_requests, seqrank.dataset distribution), random-init weights seed 0",
         "config": {"workload": f"{args.config}: {n_req} request(s) x {n_cand} candidates, L={L}, "
                                f"RT=256, IMP=256, NNConfig{nn_t} -> S={nn.seq_len}, 2 layers d=64",
                    "requests_per_step_per_gpu": n_req, "candidates_per_step_per_gpu": cand_step,
-                   "parallelism": f"request-sharded x{world} (no collective)",
+                   "parallelism": (f"candidate-split x{world} + NCCL all_gather of the logits per step"
+                                   " (e2e: slices without the gather)" if split
+                                   else f"request-sharded x{world} (no collective)"),
                    "l2": "flushed between timed steps (256 MB write, untimed)"},
         "p50_request_ms": round(nearest_rank(step_ms, 50), 4),
         "p99_request_ms": round(nearest_rank(step_ms, 99), 4),
