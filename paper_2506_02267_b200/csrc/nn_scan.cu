@@ -364,8 +364,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_scan_kernel(Staged st, NNCfg
 // Gate bound of a (candidate, source): T <= the k-th largest group maximum,
 // by bisection on the value range with warp-wide counts (values held in
 // registers, kBoundPer per lane; no shared-memory histograms).  The
-// invariant count(g >= lo) >= k keeps lo a valid bound; 24 halvings of
-// [min, max] leave it within ~1e-7 of the exact k-th value.  Also resets the
+// invariant count(g >= lo) >= k keeps lo a valid bound; ~14 halvings of
+// [min, max] leave it within 1e-4 of the exact k-th value.  Also resets the
 // pass-2 survivor counter.
 constexpr int kBoundWarps = 4;
 constexpr int kBoundPer = 72;  // values per lane: ng <= 8k + 2 <= 2304
@@ -401,12 +401,21 @@ __device__ __forceinline__ float bisect_kth(const float* g, int ng, int k, int l
     return (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
   };
   if (count_ge(mx) >= k) return mx;
+  // T only has to stay <= the k-th largest maximum: stop once the bracket is
+  // 1e-4 wide (a tenth of the gate margin: a handful of extra survivors at
+  // most) or a midpoint counts exactly k
   float lo = mn, hi = mx;  // count(>= lo) >= k > count(>= hi)
 #pragma unroll 1
-  for (int it = 0; it < 24; ++it) {
+  while (hi - lo > 1e-4f) {
     const float mid = 0.5f * (lo + hi);
     if (!(mid > lo && mid < hi)) break;  // adjacent floats
-    if (count_ge(mid) >= k) lo = mid; else hi = mid;
+    const int c = count_ge(mid);
+    if (c >= k) {
+      lo = mid;
+      if (c == k) break;
+    } else {
+      hi = mid;
+    }
   }
   return lo;
 }
