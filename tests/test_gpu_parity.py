@@ -290,3 +290,51 @@ def test_softmax_shift_guard_falls_back_to_running_max():
     assert "skut_simt" in kt and "skut_tc3" not in kt and "skut_tc" not in kt, kt
     ref = orc.rank_request(from_user(r.user), r.candidates, r.ctx, Pd, (32, 96, 32, 32))
     assert np.abs(logits - ref).max() <= TOL["bf16"]
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_direct_select_ties_and_near_ties(mode):
+    """The small-source path (RT tail, IMP: <= 256 selectable tokens, no scan)
+    on degenerate inputs: identical tokens (every score ties exactly -> the k
+    lowest indices), a zero candidate, a candidate equal to a planted token,
+    and near ties (perturbed copies whose scores differ by ~1e-4, inside the
+    f32 histogram's ambiguous band)."""
+    nn = P.NNConfig()
+    r = P.generate_requests(1, 6, ll_tokens=2048, seed=9)[0]
+    ud = from_user(r.user)
+    for src in ("rt", "imp"):
+        ud[f"{src}_emb"] = ud[f"{src}_emb"].copy()
+    v = ud["rt_emb"][40].copy()
+    ud["rt_emb"][40:200] = v                      # 160 identical RT-tail tokens
+    w = ud["imp_emb"][10].copy()
+    for i in range(10, 120):                      # near ties in IMP: +-1 on one coordinate
+        ud["imp_emb"][i] = w
+        ud["imp_emb"][i, i % 32] = np.clip(int(w[i % 32]) + (1 if i % 2 else -1), -127, 127)
+    cands = r.candidates.copy()
+    cands[0] = 0.0
+    cands[1] = v.astype(np.float32)
+    cands[2] = w.astype(np.float32)
+    cands[3] = -w.astype(np.float32)
+    eng = _engine_for(nn, cap=Capacity(1, 8, 4096))
+    logits, idx = eng.rank_requests([(to_user(ud), cands, r.ctx)], mode=mode, return_indices=True)
+    Pd = orc.model_init(0, seq_len=nn.seq_len)
+    lg, det = orc.rank_request(ud, cands, r.ctx, Pd, (32, 96, 32, 32), return_detail=True)
+    m = len(cands)
+    ref_idx = np.full((m, nn.seq_len), -1, np.int32)
+    kth = np.zeros((m, 4))
+    for j in range(m):
+        for st, sg in zip(nn.segment_starts(), det["segs"][j]):
+            ref_idx[j, st:st + len(sg)] = sg
+        for g, name in ((0, "nn_lifelong"), (2, "nn_realtime_tail"), (3, "nn_impression")):
+            kth[j, g] = det["scores"][j][name][-1]
+
+    def fn(i, g, ii):
+        src = {0: "ll", 2: "rt", 3: "imp"}[g]
+        return orc.similarity_scores(ud[f"{src}_emb"], cands[i])[ii]
+
+    check_nn_contract(idx, ref_idx, fn, kth, nn.segment_starts(), nn.segment_lengths())
+    for g in (2, 3):  # exact ties (zero candidate, planted copies): identical sets
+        a, b = nn.segment_starts()[g], nn.segment_starts()[g] + nn.segment_lengths()[g]
+        assert np.array_equal(idx[0, a:b], ref_idx[0, a:b])
+        assert np.array_equal(idx[1, a:b], ref_idx[1, a:b])
+    assert np.abs(logits - lg).max() <= TOL[mode]
