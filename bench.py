@@ -349,6 +349,11 @@ def run_gpu(args, rank, world, local_rank):
     t0 = time.perf_counter()
     eng.rank_pipelined([sp[i % pool_n] for i in range(args.steps)], mode=mode, latencies=lat_st)
     st_value = cand_step * args.steps / (time.perf_counter() - t0)
+    lat_st_sync = []  # one request at a time through the store (serving latency)
+    for i in range(min(args.steps, 100)):
+        ts = time.perf_counter()
+        eng.rank_requests(sp[i % pool_n], mode=mode)
+        lat_st_sync.append(time.perf_counter() - ts)
     h2d_store = h2d - sum(u.total_tokens() for u, _, _ in packed[0]) * (32 + 2 + 1)
     eng.store_reserve(0)
 
@@ -399,7 +404,9 @@ def run_gpu(args, rank, world, local_rank):
                 "store": {"value": round(st_value, 1), "h2d_bytes_per_step": h2d_store,
                           "api": "Engine.rank_pipelined over serving.DeviceFeatureStore users (HBM-resident tokens)",
                           "p50_request_ms": round(1e3 * nearest_rank(lat_st, 50), 4),
-                          "p99_request_ms": round(1e3 * nearest_rank(lat_st, 99), 4)}},
+                          "p99_request_ms": round(1e3 * nearest_rank(lat_st, 99), 4),
+                          "sync_p50_request_ms": round(1e3 * nearest_rank(lat_st_sync, 50), 4),
+                          "sync_p99_request_ms": round(1e3 * nearest_rank(lat_st_sync, 99), 4)}},
         "gpu_launches": launches_per_step * args.steps,
         "kernels": {k: {"ms_per_launch": round(v[0] / max(v[1], 1), 4), "launches": v[1]} for k, v in kt.items()},
         "roofline": roof,
