@@ -252,6 +252,23 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   // the gather's index chain (idx -> token) of the next candidate is resolved
   // during the last layer of the current one
   int tok_pf = (in_seq && (int)blockIdx.x < n) ? slot_token(st, nn, idx, blockIdx.x, r) : -1;
+  // Tile 1's rows' position embeddings stay in TMEM for the kernel's
+  // lifetime: tile 0's columns [128, 192) are never used by tile 0 (its
+  // scores span <= 96 keys, its widest output 128 columns), and tile 1's
+  // warp q shares tile 0's warp q lane quadrant.  Saves tile 1 -- the
+  // critical tile -- 16 of its 40 row-per-thread global loads per item.
+  const uint32_t pos_t = ((uint32_t)(32 * q) << 16) + 128u;
+  if (t == 1) {
+    float pp[kDModel];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float4 b = in_seq ? __ldg(pos4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      pp[4 * j] = b.x; pp[4 * j + 1] = b.y; pp[4 * j + 2] = b.z; pp[4 * j + 3] = b.w;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_st16(pos_t + 16 * c, reinterpret_cast<const uint32_t*>(pp + 16 * c));
+    tmem_st_wait();
+  }
   for (int item = blockIdx.x; item < n; item += gridDim.x) {
     if (kDebug && dbg) {
       dbg[31] += 1;
@@ -259,6 +276,11 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     }
     // ---- K3: gather + encode: x = tok_feat[tok] + pos[r] + [0 | unit(c)] ----
     float x[kDModel];
+    if (t == 1) {  // position rows from TMEM (warp-collective: before any divergence)
+      tmem_ld32(pos_t, reinterpret_cast<uint32_t*>(x));
+      tmem_ld32(pos_t + 32, reinterpret_cast<uint32_t*>(x + 32));
+      tmem_ld_wait();
+    }
     bool ok = false;
     if (in_seq) {
       const int tok = tok_pf;
@@ -268,7 +290,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         const float4* cu = reinterpret_cast<const float4*>(st.cand_unit + (size_t)item * kEmbed);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const float4 a = tf[j], b = __ldg(pos4 + j);
+          const float4 a = tf[j];
+          const float4 b = t == 1 ? make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]) : __ldg(pos4 + j);
           const float4 c = j >= 8 ? cu[j - 8] : make_float4(0.f, 0.f, 0.f, 0.f);
           x[4 * j] = (a.x + c.x) + b.x;
           x[4 * j + 1] = (a.y + c.y) + b.y;
