@@ -285,18 +285,28 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     if (in_seq) {
       const int tok = tok_pf;
       ok = tok >= 0;
-      if (ok) {
-        const float4* tf = reinterpret_cast<const float4*>(st.tok_feat + (size_t)tok * kDModel);
-        const float4* cu = reinterpret_cast<const float4*>(st.cand_unit + (size_t)item * kEmbed);
+      if (ok) {  // 32-byte loads: the token row is 8 sectors, one per load
+        const float* tf = st.tok_feat + (size_t)tok * kDModel;
+        const float* cu = st.cand_unit + (size_t)item * kEmbed;
+        const float* pr = p.position_table + (size_t)r * kDModel;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float4 a = tf[j];
-          const float4 b = t == 1 ? make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]) : __ldg(pos4 + j);
-          const float4 c = j >= 8 ? cu[j - 8] : make_float4(0.f, 0.f, 0.f, 0.f);
-          x[4 * j] = (a.x + c.x) + b.x;
-          x[4 * j + 1] = (a.y + c.y) + b.y;
-          x[4 * j + 2] = (a.z + c.z) + b.z;
-          x[4 * j + 3] = (a.w + c.w) + b.w;
+        for (int j = 0; j < 8; ++j) {
+          float a[8], b[8], c[8];
+          ldg256(tf + 8 * j, a);
+          if (t == 1) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) b[e] = x[8 * j + e];
+          } else {
+            ldg256(pr + 8 * j, b);
+          }
+          if (j >= 4) {
+            ldg256(cu + 8 * (j - 4), c);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) c[e] = 0.0f;
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[8 * j + e] = (a[e] + c[e]) + b[e];
         }
       }
     }

@@ -73,6 +73,13 @@ __device__ __forceinline__ void split_pair_t(float a, float b, uint32_t& hi, uin
   const float2 r = __ffma2_rn(h, make_float2(-1.0f, -1.0f), make_float2(a, b));  // exact residuals
   lo = __byte_perm(__float_as_uint(r.x), __float_as_uint(r.y), 0x7632);
 }
+// 32-byte global load (LDG.256, sm_100): one full sector per lane, half the
+// L1 requests of two 16-byte loads for row-per-thread gathers
+__device__ __forceinline__ void ldg256(const float* p, float* r) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+               : "l"(p));
+}
 // three-input max (one FMNMX3 on sm_100)
 __device__ __forceinline__ float fmax3f(float a, float b, float c) {
   float r;
