@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include "tav2_common.cuh"
+#include "tc_common.cuh"
 
 namespace tav2 {
 
@@ -58,6 +59,32 @@ __device__ __forceinline__ void encode_row(const Staged& st, const Params& p, in
     f[4 * j + 2] = (f[4 * j + 2] + asum[4 * j + 2]) + s4.z;
     f[4 * j + 3] = (f[4 * j + 3] + asum[4 * j + 3]) + s4.w;
     f[4 * j] += p4.x; f[4 * j + 1] += p4.y; f[4 * j + 2] += p4.z; f[4 * j + 3] += p4.w;
+  }
+}
+
+// The same row from prep's precomputed token part (tok_feat = [unit(q) | 0]
+// + bits @ action_table + surface_table[min(s,3)]): x = (tok_feat + [0 |
+// unit(c)]) + position_table[r], with 32-byte loads (LDG.256: one sector
+// per lane).  f32 sums in another order than encode_row (<= 1 ulp apart);
+// the bf16 tensor-core kernels use it, the fp32 parity path keeps encode_row.
+__device__ __forceinline__ void encode_feat(const Staged& st, const Params& p, int item, int tok, int r,
+                                            float* f) {
+  const float* tf = st.tok_feat + (size_t)tok * kDModel;
+  const float* cu = st.cand_unit + (size_t)item * kEmbed;
+  const float* pr = p.position_table + (size_t)r * kDModel;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float a[8], b[8], c[8];
+    tc::ldg256(tf + 8 * j, a);
+    tc::ldg256(pr + 8 * j, b);
+    if (j >= 4) {
+      tc::ldg256(cu + 8 * (j - 4), c);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) c[e] = 0.0f;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[8 * j + e] = (a[e] + c[e]) + b[e];
   }
 }
 

@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc_kernel(
       if (use_staged) {
         const int tok = slot_token(st, nn, idx, item, r);
         ok = tok >= 0;
-        if (ok) encode_row(st, p, item, tok, r, x);
+        if (ok) encode_feat(st, p, item, tok, r, x);
       } else {
         ok = fmask[(size_t)item * S + r] != 0;
         if (ok) {
@@ -856,7 +856,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) skut_tc2_kernel(
       if (use_staged) {
         const int tok = slot_token(st, nn, idx, item, r);
         ok = tok >= 0;
-        if (ok) encode_row(st, p, item, tok, r, x);
+        if (ok) encode_feat(st, p, item, tok, r, x);
       } else {
         ok = fmask[(size_t)item * S + r] != 0;
         if (ok) {
