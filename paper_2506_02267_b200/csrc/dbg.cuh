@@ -49,12 +49,6 @@ __device__ __forceinline__ void sel_record_phase(int slot, int phase, long long 
   long long* d = g_dbg_cta;
   if (d != nullptr && slot < kDbgCtas) d[(phase == 0 ? 6 * 3 + 2 : 7 * 3 + 0) * kDbgCtas + slot] = dur;
 }
-// raw stamp array (record 7, slots 1-2 of the cta buffer: 8192 entries)
-__device__ __forceinline__ void raw_stamp(int i, long long v) {
-  if constexpr (!kDebug) return;
-  long long* d = g_dbg_cta;
-  if (d != nullptr && i < 2 * kDbgCtas) d[(7 * 3 + 1) * kDbgCtas + i] = v;
-}
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
