@@ -459,7 +459,7 @@ cudaError_t launch_nn_scan(const Staged& st, const NNCfg& nn, const NNScan& sc, 
                            cudaStream_t s) {
   if (st.n_work == 0) return cudaSuccess;
   const size_t smem = kATile + (size_t)kStages * kBTile;
-  cudaError_t e = cudaFuncSetAttribute(nn_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_max_dyn_smem((const void*)nn_scan_kernel, (int)smem);
   if (e != cudaSuccess) return e;
   return launch_pdl(nn_scan_kernel, dim3(st.n_work), dim3(kTcThreads), smem, s, st, nn, sc, pass);
 }

@@ -298,8 +298,7 @@ cudaError_t launch_skut_simt(const Params& p, const NNCfg& nn, const Staged* st,
   if (n == 0) return cudaSuccess;
   const int S = nn.seq_len;
   size_t smem = (size_t)(2 * S * kDModel + 4 * kDModel + 112 + kHidden) * 4 + kMaxSeq * 4;
-  cudaError_t e = cudaFuncSetAttribute(skut_simt_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_max_dyn_smem((const void*)skut_simt_kernel, (int)smem);
   if (e != cudaSuccess) return e;
   Staged dummy{};
   skut_simt_kernel<<<skut_simt_grid(n), kSkutThreads, smem, s>>>(

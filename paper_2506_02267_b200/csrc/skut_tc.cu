@@ -1185,11 +1185,9 @@ cudaError_t launch_skut_tc(const Params& p, const SkutImages& img, const NNCfg& 
   const size_t smem = (size_t)kImgWA + kImgWB + 4 * (size_t)S_pad * 128;
   // S <= 192: tile-decoupled kernel; 192 < S <= 256: the coupled 2-tile kernel
   auto kern = S_pad <= 192 ? skut_tc2_kernel : skut_tc_kernel;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_max_dyn_smem((const void*)kern, (int)smem);
   if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sms();
   Staged dummy{};
   e = launch_pdl(kern, dim3(n < sms ? n : sms), dim3(kSkThreads), smem, s, p, img, nn, st ? *st : dummy,
                  (int)(st != nullptr), idx, F, fmask, n, U, logits, pooled);

@@ -662,11 +662,9 @@ cudaError_t launch_skut_tc3(const Params& p, const SkutImages3& img, const NNCfg
   if (n == 0) return cudaSuccess;
   const int S_pad = (nn.seq_len + 15) & ~15;
   const size_t smem = (size_t)p.num_layers * kW3Layer + kImg3WO + 4 * (size_t)S_pad * 128;
-  cudaError_t e = cudaFuncSetAttribute(skut_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_max_dyn_smem((const void*)skut_tc3_kernel, (int)smem);
   if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sms();
   return launch_pdl(skut_tc3_kernel, dim3(n < sms ? n : sms), dim3(kT3Threads), smem, s, p, img, nn, st, idx, n,
                     logits, pooled);
 }

@@ -11,6 +11,8 @@
 #include <string.h>
 
 #include <string>
+#include <map>
+#include <mutex>
 #include <unordered_map>
 #include <vector>
 
@@ -50,6 +52,34 @@ inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 
 }  // namespace
+
+cudaError_t tav2::set_max_dyn_smem(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  int& v = done[{kern, dev}];
+  if (v >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) v = bytes;
+  return e;
+}
+
+int tav2::device_sms() {
+  static std::mutex mu;
+  static std::map<int, int> sms;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = sms.find(dev);
+  if (it != sms.end()) return it->second;
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  sms[dev] = n;
+  return n;
+}
 
 bool tav2::pdl_enabled() {
   static const bool on = [] {

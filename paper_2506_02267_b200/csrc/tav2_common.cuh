@@ -206,6 +206,11 @@ namespace tav2 {
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) and the SM count cost a
+// host round trip each; every launcher calls these instead (cached per
+// kernel and device, defined in tav2_api.cu)
+cudaError_t set_max_dyn_smem(const void* kern, int bytes);
+int device_sms();
 bool pdl_enabled();  // TAV2_NO_PDL=1 disables programmatic dependent launch (A/B timing)
 
 template <typename... KArgs, typename... Args>
