@@ -152,3 +152,30 @@ def test_gpu_store_load_truncates_like_reference(tmp_path):
     uid, raw = users[0]
     store.put(uid, raw)
     assert store.get(uid).equals(trunc[uid])
+
+
+@pytest.mark.gpu
+def test_gpu_store_abi_errors():
+    """tav2_store_* argument checks surface as ValidationError (the Python
+    mirror truncates first; the C ABI itself rejects over-cap columns)."""
+    eng = _engine()
+    eng.store_reserve(2)
+    r = P.generate_requests(1, 8, ll_tokens=300, seed=2)[0]
+    blk = r.user.realtime
+    over = UserSequences(r.user.lifelong, TokenBlock(np.concatenate([blk.timestamps] * 2),
+                                                     np.concatenate([blk.actions] * 2),
+                                                     np.concatenate([blk.surfaces] * 2),
+                                                     np.concatenate([blk.embeddings] * 2)),
+                         r.user.impression)
+    with pytest.raises(P.ValidationError, match="outside"):
+        eng.store_put(1, over)  # 512 real-time tokens > REALTIME_CAP
+    with pytest.raises(P.ValidationError, match="not in the HBM store"):
+        eng.store_remove(12345)
+    eng.store_put(1, r.user)
+    assert eng.store_count() == 1
+    eng.store_reserve(0)  # drops every user
+    assert eng.store_count() == 0
+    from paper_2506_02267_b200.runtime import StoreUser
+
+    with pytest.raises(P.ValidationError, match="not in the HBM store"):
+        eng.rank_requests([(StoreUser(1), r.candidates, r.ctx)])
