@@ -1,0 +1,76 @@
+"""Randomised parity sweep (the spirit of SPEC.md acceptance #2 "fused NN
+path == naive path over randomized instances" and #4 "fused transformer ==
+reference over random trials"): random source lengths (empty, shorter than
+k, around the 256-token direct-selection limit, scanned), random candidate
+counts, five NN configurations (every SKUT kernel), co-batched requests -- every instance
+checked against the CPU oracle with the north-star contract (index sets
+equal except ties within 1e-6 of the k-th score; logits within 1e-5 fp32 /
+2e-3 bf16)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2506_02267_b200 as P  # noqa: E402
+from paper_2506_02267_b200.runtime import Capacity, Engine  # noqa: E402
+from helpers import check_nn_contract, from_user  # noqa: E402
+from oracle import seqrank_oracle as orc  # noqa: E402
+
+TOL = {"fp32": 1e-5, "bf16": 2e-3}
+# S = 192 (tc3), 160, 96, 224 (unfolded tc kernel), 352 (SIMT in both modes)
+CONFIGS = [(32, 96, 32, 32), (16, 64, 48, 16), (32, 32, 0, 32), (32, 128, 32, 32), (32, 256, 32, 32)]
+N_TRIALS = 30  # per config and mode (each trial: 1-3 co-batched requests)
+
+
+def _rand_lengths(rng):
+    """LL length from a mix of regimes: empty, < k, <= 256 (direct), scanned."""
+    regime = rng.integers(0, 4)
+    ll = [0, int(rng.integers(1, 64)), int(rng.integers(64, 257)), int(rng.integers(257, 5000))][regime]
+    rt = int(rng.choice([0, int(rng.integers(1, 40)), int(rng.integers(40, 257))]))
+    imp = int(rng.choice([0, int(rng.integers(1, 40)), int(rng.integers(40, 257))]))
+    return ll, rt, imp
+
+
+@pytest.mark.parametrize("mode", ["fp32", "bf16"])
+@pytest.mark.parametrize("cfg", CONFIGS, ids=lambda c: "nn" + "_".join(map(str, c)))
+def test_random_instances_vs_oracle(cfg, mode):
+    nn = P.NNConfig(*cfg)
+    model = P.RankingModel.init(P.ModelConfig.for_nn(nn), seed=3)
+    Pd = orc.model_init(3, seq_len=nn.seq_len)
+    eng = Engine(model, capacity=Capacity(3, 3 * 48, 3 * (5000 + 512)))
+    rng = np.random.default_rng(hash(cfg) % 2**32 + (mode == "bf16"))
+    for trial in range(N_TRIALS if nn.seq_len <= 256 else 8):
+        n_req = int(rng.integers(1, 4))
+        reqs = []
+        for q in range(n_req):
+            ll, rt, imp = _rand_lengths(rng)
+            r = P.generate_requests(1, int(rng.integers(1, 48)), ll_tokens=ll, rt_tokens=rt, imp_tokens=imp,
+                                    seed=int(rng.integers(1 << 30)))[0]
+            reqs.append(r)
+        logits, idx = eng.rank_requests([(r.user, r.candidates, r.ctx) for r in reqs], mode=mode,
+                                        return_indices=True)
+        row = 0
+        for r in reqs:
+            ud = from_user(r.user)
+            lg, det = orc.rank_request(ud, r.candidates, r.ctx, Pd, cfg, return_detail=True)
+            m = len(r.candidates)
+            ref_idx = np.full((m, nn.seq_len), -1, np.int32)
+            kth = np.zeros((m, 4))
+            for j in range(m):
+                for st, sg in zip(nn.segment_starts(), det["segs"][j]):
+                    ref_idx[j, st:st + len(sg)] = sg
+                for g, name in ((0, "nn_lifelong"), (2, "nn_realtime_tail"), (3, "nn_impression")):
+                    sc = det["scores"][j].get(name)
+                    kth[j, g] = sc[-1] if sc is not None and len(sc) else 0.0
+
+            def fn(i, g, ii, _u=ud, _c=r.candidates):
+                src = {0: "ll", 2: "rt", 3: "imp"}[g]
+                return orc.similarity_scores(_u[f"{src}_emb"], _c[i])[ii]
+
+            check_nn_contract(idx[row:row + m], ref_idx, fn, kth, nn.segment_starts(), nn.segment_lengths())
+            a, b = nn.segment_starts()[1], nn.segment_starts()[1] + nn.recent
+            assert np.array_equal(idx[row:row + m, a:b], ref_idx[:, a:b])  # RT[:r] verbatim
+            err = np.abs(logits[row:row + m] - lg).max()
+            assert err <= TOL[mode], f"trial {trial}: max |dlogit| {err:.3g}"
+            row += m
