@@ -14,7 +14,8 @@
 
 namespace tav2 {
 
-constexpr int kSkutThreads = 128;
+constexpr int kSkutThreads = 256;  // one row per thread up to S = 256
+constexpr int kSkutWarps = kSkutThreads / 32;
 constexpr float kLnEps = 1e-5f;  // encoder.py:19
 
 // out[j] = sum_i a[i] * W[i, j]   (W row-major [IN, OUT] f32 in global)
@@ -111,8 +112,8 @@ __global__ void __launch_bounds__(kSkutThreads, 1) skut_simt_kernel(
   const int S = nn.seq_len;
   float* Ks = sm;                    // [S][64]
   float* Vs = sm + S * kDModel;      // [S][64]
-  float* red = Vs + S * kDModel;     // [4][64] pool partials
-  float* zs = red + 4 * kDModel;     // [104] head input
+  float* red = Vs + S * kDModel;     // [warps][64] pool partials
+  float* zs = red + kSkutWarps * kDModel;  // [104] head input
   float* hs = zs + 112;              // [64]  head hidden
   int* valid_s = reinterpret_cast<int*>(hs + kHidden);  // [kMaxSeq] mask
   float* X = scratch + (size_t)blockIdx.x * 2 * S * kDModel;
@@ -255,7 +256,9 @@ __global__ void __launch_bounds__(kSkutThreads, 1) skut_simt_kernel(
       }
       __syncthreads();
       if (tid < kDModel) {
-        float v = fmaxf(fmaxf(red[tid], red[kDModel + tid]), fmaxf(red[2 * kDModel + tid], red[3 * kDModel + tid]));
+        float v = red[tid];
+#pragma unroll
+        for (int w = 1; w < kSkutWarps; ++w) v = fmaxf(v, red[w * kDModel + tid]);
         v = any ? v : 0.0f;  // empty user -> pooled = 0 (trainer.py:358-359)
         zs[tid] = v;
         if (pooled_out) pooled_out[(size_t)item * kDModel + tid] = v;
@@ -297,7 +300,7 @@ cudaError_t launch_skut_simt(const Params& p, const NNCfg& nn, const Staged* st,
                              cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const int S = nn.seq_len;
-  size_t smem = (size_t)(2 * S * kDModel + 4 * kDModel + 112 + kHidden) * 4 + kMaxSeq * 4;
+  size_t smem = (size_t)(2 * S * kDModel + kSkutWarps * kDModel + 112 + kHidden) * 4 + kMaxSeq * 4;
   cudaError_t e = set_max_dyn_smem((const void*)skut_simt_kernel, (int)smem);
   if (e != cudaSuccess) return e;
   Staged dummy{};
