@@ -107,7 +107,8 @@ cudaError_t launch_encode(const Staged& st, const NNCfg& nn, const Params& p, co
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kSkutThreads, 1) skut_simt_kernel(
     Params p, NNCfg nn, Staged st, int use_staged, const int32_t* idx, const float* Fin,
-    const uint8_t* fmask, int n, float* scratch, float* U, float* logits, float* pooled_out) {
+    const uint8_t* fmask, int n, float* scratch, float* U, float* logits, float* pooled_out, int cs_shift) {
+  __shared__ unsigned kmax_s;  // max_j ||k_j||^2 of the layer (single-pass shift)
   extern __shared__ __align__(16) float sm[];
   const int S = nn.seq_len;
   float* Ks = sm;                    // [S][64]
@@ -139,6 +140,8 @@ __global__ void __launch_bounds__(kSkutThreads, 1) skut_simt_kernel(
     __syncthreads();
 
     for (int L = 0; L < p.num_layers; ++L) {
+      if (tid == 0) kmax_s = 0u;
+      __syncthreads();
       // ---- LN1 + Q/K/V projections (encoder.py:386-392, :398, :412-413) ----
       for (int r = tid; r < S; r += kSkutThreads) {
         if (!valid_s[r]) continue;
@@ -149,6 +152,12 @@ __global__ void __launch_bounds__(kSkutThreads, 1) skut_simt_kernel(
         store64(Q + r * kDModel, o);
         matvec<kDModel, kDModel>(a, p.wk[L], o);
         store64(Ks + r * kDModel, o);
+        if (cs_shift) {
+          float kn2 = 0.0f;
+#pragma unroll
+          for (int j = 0; j < kDModel; ++j) kn2 = fmaf(o[j], o[j], kn2);
+          atomicMax(&kmax_s, __float_as_uint(kn2));
+        }
         matvec<kDModel, kDModel>(a, p.wv[L], o);
         store64(Vs + r * kDModel, o);
       }
@@ -166,34 +175,71 @@ __global__ void __launch_bounds__(kSkutThreads, 1) skut_simt_kernel(
         if (mine) load64(Q + r * kDModel, q);
 #pragma unroll
         for (int j = 0; j < kDModel; ++j) acc[j] = 0.0f;
-        float m = -INFINITY, l = 0.0f;
-        for (int j = 0; j <= rmax; ++j) {
-          if (!valid_s[j]) continue;  // warp-uniform
-          const float4* kr = reinterpret_cast<const float4*>(Ks + j * kDModel);
-          float sdot = 0.0f;
+        float l = 0.0f;
+        if (cs_shift) {
+          // single pass: p_j = exp(s_j - m') with the Cauchy-Schwarz bound
+          // m' = ||q_r|| max_j ||k_j|| / 8 >= s_j (shift invariance keeps 1/l
+          // the exact normaliser; the host enables it only when m' provably
+          // keeps every exponent in the normal range) -- no running max, no
+          // per-key rescale of the accumulator
+          float qn2 = 0.0f;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            float4 kv = kr[e];
-            sdot = fmaf(q[4 * e], kv.x, sdot);
-            sdot = fmaf(q[4 * e + 1], kv.y, sdot);
-            sdot = fmaf(q[4 * e + 2], kv.z, sdot);
-            sdot = fmaf(q[4 * e + 3], kv.w, sdot);
+          for (int e = 0; e < kDModel; ++e) qn2 = fmaf(q[e], q[e], qn2);
+          const float mb = sqrtf(qn2 * __uint_as_float(kmax_s)) * 0.125f;
+          for (int j = 0; j <= rmax; ++j) {
+            if (!valid_s[j]) continue;  // warp-uniform
+            const float4* kr = reinterpret_cast<const float4*>(Ks + j * kDModel);
+            float sdot = 0.0f;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              float4 kv = kr[e];
+              sdot = fmaf(q[4 * e], kv.x, sdot);
+              sdot = fmaf(q[4 * e + 1], kv.y, sdot);
+              sdot = fmaf(q[4 * e + 2], kv.z, sdot);
+              sdot = fmaf(q[4 * e + 3], kv.w, sdot);
+            }
+            const float pj = (mine && j <= r) ? expf(sdot * 0.125f - mb) : 0.0f;
+            l += pj;
+            const float4* vr = reinterpret_cast<const float4*>(Vs + j * kDModel);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              float4 vv = vr[e];
+              acc[4 * e] = fmaf(pj, vv.x, acc[4 * e]);
+              acc[4 * e + 1] = fmaf(pj, vv.y, acc[4 * e + 1]);
+              acc[4 * e + 2] = fmaf(pj, vv.z, acc[4 * e + 2]);
+              acc[4 * e + 3] = fmaf(pj, vv.w, acc[4 * e + 3]);
+            }
           }
-          const bool use = mine && j <= r;
-          const float sc = sdot * 0.125f;  // 1/sqrt(64)
-          const float mn = use ? fmaxf(m, sc) : m;
-          const float alpha = use ? expf(m - mn) : 1.0f;
-          const float pj = use ? expf(sc - mn) : 0.0f;
-          m = mn;
-          l = l * alpha + pj;
-          const float4* vr = reinterpret_cast<const float4*>(Vs + j * kDModel);
+        } else {
+          float m = -INFINITY;
+          for (int j = 0; j <= rmax; ++j) {
+            if (!valid_s[j]) continue;  // warp-uniform
+            const float4* kr = reinterpret_cast<const float4*>(Ks + j * kDModel);
+            float sdot = 0.0f;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            float4 vv = vr[e];
-            acc[4 * e] = fmaf(pj, vv.x, acc[4 * e] * alpha);
-            acc[4 * e + 1] = fmaf(pj, vv.y, acc[4 * e + 1] * alpha);
-            acc[4 * e + 2] = fmaf(pj, vv.z, acc[4 * e + 2] * alpha);
-            acc[4 * e + 3] = fmaf(pj, vv.w, acc[4 * e + 3] * alpha);
+            for (int e = 0; e < 16; ++e) {
+              float4 kv = kr[e];
+              sdot = fmaf(q[4 * e], kv.x, sdot);
+              sdot = fmaf(q[4 * e + 1], kv.y, sdot);
+              sdot = fmaf(q[4 * e + 2], kv.z, sdot);
+              sdot = fmaf(q[4 * e + 3], kv.w, sdot);
+            }
+            const bool use = mine && j <= r;
+            const float sc = sdot * 0.125f;  // 1/sqrt(64)
+            const float mn = use ? fmaxf(m, sc) : m;
+            const float alpha = use ? expf(m - mn) : 1.0f;
+            const float pj = use ? expf(sc - mn) : 0.0f;
+            m = mn;
+            l = l * alpha + pj;
+            const float4* vr = reinterpret_cast<const float4*>(Vs + j * kDModel);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              float4 vv = vr[e];
+              acc[4 * e] = fmaf(pj, vv.x, acc[4 * e] * alpha);
+              acc[4 * e + 1] = fmaf(pj, vv.y, acc[4 * e + 1] * alpha);
+              acc[4 * e + 2] = fmaf(pj, vv.z, acc[4 * e + 2] * alpha);
+              acc[4 * e + 3] = fmaf(pj, vv.w, acc[4 * e + 3] * alpha);
+            }
           }
         }
         if (!mine) continue;
@@ -296,7 +342,7 @@ size_t skut_simt_scratch_floats(int seq_len) { return (size_t)2 * seq_len * kDMo
 
 cudaError_t launch_skut_simt(const Params& p, const NNCfg& nn, const Staged* st,
                              const int32_t* idx, const float* F, const uint8_t* fmask, int n,
-                             float* scratch, float* U, float* logits, float* pooled,
+                             float* scratch, float* U, float* logits, float* pooled, int cs_shift,
                              cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const int S = nn.seq_len;
@@ -305,7 +351,7 @@ cudaError_t launch_skut_simt(const Params& p, const NNCfg& nn, const Staged* st,
   if (e != cudaSuccess) return e;
   Staged dummy{};
   skut_simt_kernel<<<skut_simt_grid(n), kSkutThreads, smem, s>>>(
-      p, nn, st ? *st : dummy, st != nullptr, idx, F, fmask, n, scratch, U, logits, pooled);
+      p, nn, st ? *st : dummy, st != nullptr, idx, F, fmask, n, scratch, U, logits, pooled, cs_shift);
   return cudaGetLastError();
 }
 

@@ -972,7 +972,7 @@ int run_score(tav2_ctx* c, int mode, const int32_t* idx, float* logits, float* p
   }
   CU(timed(c, "skut_simt", s, [&] {
     return launch_skut_simt(c->params, c->nn, &st, idx, nullptr, nullptr, st.n_items,
-                            c->skut_scratch, nullptr, logits, pooled, s);
+                            c->skut_scratch, nullptr, logits, pooled, (int)tc_ok, s);
   }));
   return TAV2_OK;
 }
@@ -1020,7 +1020,8 @@ int tav2_forward(tav2_ctx* c, int mode, const float* features_dev, const uint8_t
     return TAV2_OK;
   }
   CU(launch_skut_simt(c->params, c->nn, nullptr, nullptr, features_dev, mask_dev, n,
-                      c->skut_scratch, u_dev, nullptr, nullptr, (cudaStream_t)stream));
+                      c->skut_scratch, u_dev, nullptr, nullptr, (int)(c->cs_bound <= 60.0),
+                      (cudaStream_t)stream));
   return TAV2_OK;
 }
 
