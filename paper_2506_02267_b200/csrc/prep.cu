@@ -49,7 +49,8 @@ __device__ __forceinline__ float quad_sumsq(const float* v, unsigned qm) {
 // elements 8g..8g+7 of the 32-vector and features 16g..16g+15 of the 64-d
 // Eq. 4 token part.
 __device__ __forceinline__ void prep_body(const Staged& st, int with_feat, const float* tab_s, int action_rows,
-                                          int2 raw, unsigned act, int surf_raw, float4 c0, float4 c1);
+                                          int2 raw, unsigned act, int surf_raw, float4 c0, float4 c1,
+                                          const float* deq_s);
 
 __global__ void __launch_bounds__(256) prep_kernel(Staged st, Params p, int with_feat) {
   cta_stamp(kDbgPrep, 0);
@@ -87,9 +88,14 @@ __global__ void __launch_bounds__(256) prep_kernel(Staged st, Params p, int with
       reinterpret_cast<float4*>(tab_s)[r < p.action_rows ? i : 16 * kDModel / 4 + (i - p.action_rows * kDModel / 4)] =
           __ldg(srcp);
     }
-    __syncthreads();
   }
-  prep_body(st, with_feat, tab_s, p.action_rows, raw, act, surf, c0, c1);
+  // dequantize (core.py:54-57) as a 256-entry table: one IEEE division per
+  // thread per CTA instead of eight per row (bit-identical: the same two
+  // correctly rounded operations per int8 value)
+  __shared__ float deq_s[256];
+  deq_s[threadIdx.x] = __fmul_rn(__fdiv_rn((float)((int)threadIdx.x - 128), 127.0f), 0.65f);
+  __syncthreads();
+  prep_body(st, with_feat, tab_s, p.action_rows, raw, act, surf, c0, c1, deq_s);
   if (kDebug) {
     __syncthreads();
     cta_stamp(kDbgPrep, 1);
@@ -97,7 +103,8 @@ __global__ void __launch_bounds__(256) prep_kernel(Staged st, Params p, int with
 }
 
 __device__ __forceinline__ void prep_body(const Staged& st, int with_feat, const float* tab_s, int action_rows,
-                                          int2 raw, unsigned act, int surf_raw, float4 v0, float4 v1) {
+                                          int2 raw, unsigned act, int surf_raw, float4 v0, float4 v1,
+                                          const float* deq_s) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   int i = gt >> 2;
   const int g = gt & 3;
@@ -106,7 +113,7 @@ __device__ __forceinline__ void prep_body(const Staged& st, int with_feat, const
     const int8_t* q = reinterpret_cast<const int8_t*>(&raw);
     float d[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) d[j] = __fmul_rn(__fdiv_rn((float)q[j], 127.0f), 0.65f);  // core.py:54-57
+    for (int j = 0; j < 8; ++j) d[j] = deq_s[(int)q[j] + 128];  // core.py:54-57
     float nrm = __fsqrt_rn(quad_sumsq(d, qm));
     if (nrm == 0.0f) nrm = 1.0f;  // zero rows stay zero (core.py:69-74)
     float u[8];
