@@ -269,45 +269,47 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     for (int c = 0; c < 4; ++c) tmem_st16(pos_t + 16 * c, reinterpret_cast<const uint32_t*>(pp + 16 * c));
     tmem_st_wait();
   }
+  // this row's token features of the item about to be encoded: loaded for the
+  // first item here, for the next one during the current item's pooling
+  // (its 32-byte loads then overlap the pool and head phases)
+  float tfv[kDModel];
+  {
+    const size_t tr = (in_seq && tok_pf >= 0) ? (size_t)tok_pf : 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ldg256(st.tok_feat + tr * kDModel + 8 * j, tfv + 8 * j);
+  }
   for (int item = blockIdx.x; item < n; item += gridDim.x) {
     if (kDebug && dbg) {
       dbg[31] += 1;
       t_last = clock64();
     }
     // ---- K3: gather + encode: x = tok_feat[tok] + pos[r] + [0 | unit(c)] ----
+    // (the token row tfv was loaded during the previous item's head; x is
+    // built 16 columns at a time so x and tfv do not both stay live)
     float x[kDModel];
-    if (t == 1) {  // position rows from TMEM (warp-collective: before any divergence)
-      tmem_ld32(pos_t, reinterpret_cast<uint32_t*>(x));
-      tmem_ld32(pos_t + 32, reinterpret_cast<uint32_t*>(x + 32));
-      tmem_ld_wait();
-    }
-    bool ok = false;
-    if (in_seq) {
-      const int tok = tok_pf;
-      ok = tok >= 0;
-      if (ok) {  // 32-byte loads: the token row is 8 sectors, one per load
-        const float* tf = st.tok_feat + (size_t)tok * kDModel;
-        const float* cu = st.cand_unit + (size_t)item * kEmbed;
-        const float* pr = p.position_table + (size_t)r * kDModel;
+    const bool ok = in_seq && tok_pf >= 0;
+    {
+      const float* cu = st.cand_unit + (size_t)item * kEmbed;
+      const float* pr = p.position_table + (size_t)(in_seq ? r : 0) * kDModel;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float a[8], b[8], c[8];
-          ldg256(tf + 8 * j, a);
-          if (t == 1) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) b[e] = x[8 * j + e];
-          } else {
-            ldg256(pr + 8 * j, b);
-          }
-          if (j >= 4) {
-            ldg256(cu + 8 * (j - 4), c);
-          } else {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) c[e] = 0.0f;
-          }
-#pragma unroll
-          for (int e = 0; e < 8; ++e) x[8 * j + e] = (a[e] + c[e]) + b[e];
+      for (int c16 = 0; c16 < 4; ++c16) {
+        float pp[16], cc[16];
+        if (t == 1) {  // position rows from TMEM (warp-uniform branch)
+          tmem_ld16(pos_t + 16 * c16, reinterpret_cast<uint32_t*>(pp));
+          tmem_ld_wait();
+        } else {
+          ldg256(pr + 16 * c16, pp);
+          ldg256(pr + 16 * c16 + 8, pp + 8);
         }
+        if (c16 >= 2) {
+          ldg256(cu + 16 * (c16 - 2), cc);
+          ldg256(cu + 16 * (c16 - 2) + 8, cc + 8);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) cc[e] = 0.0f;
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e) x[16 * c16 + e] = (tfv[16 * c16 + e] + cc[e]) + pp[e];
       }
     }
     if (!ok) {
@@ -601,6 +603,13 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         const float v = warp_max_f32(ok ? y[j] : -INFINITY);
         if (lane == 0) red_s[warp][j] = v;
       }
+    }
+    {  // the next item's token row (tok_pf resolved in the last layer), under
+       // the head; always overwritten (row 0 for padding slots) so tfv is dead
+       // through the layers
+      const size_t tr = (in_seq && tok_pf >= 0) ? (size_t)tok_pf : 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ldg256(st.tok_feat + tr * kDModel + 8 * j, tfv + 8 * j);
     }
     named_bar_sync(1, kT3Threads);
     stamp(22);
