@@ -347,12 +347,25 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         }
 #pragma unroll
         for (int j = 0; j < kDModel; ++j) an2 = fmaf(a[j], a[j], an2);
-        t3_st_split<64>(cA, a);  // warp-collective: never under a divergent branch
-        if (mapped) {
+        // one bf16 hi/lo split of a, stored twice: the M1 A operand (TMEM,
+        // warp-collective: never under a divergent branch) and this row's K
+        // (K-major smem slabs: chunk c of row r at c*(S_pad*16) + r*16)
+        {
+          uint32_t hi[32], lo[32];
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {  // K-major slabs: chunk c of row r at c*(S_pad*16) + r*16
-            const int off = c * (S_pad * 16) + r * 16;
-            t3_split8_store(Khi + off, Klo + off, a + 8 * c);
+          for (int i = 0; i < 32; ++i) split_pair(a[2 * i], a[2 * i + 1], hi[i], lo[i]);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            tmem_st8(cA + 8 * c, hi + 8 * c);
+            tmem_st8(cA + 32 + 8 * c, lo + 8 * c);
+          }
+          if (mapped) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const int off = c * (S_pad * 16) + r * 16;
+              *reinterpret_cast<uint4*>(Khi + off) = make_uint4(hi[4 * c], hi[4 * c + 1], hi[4 * c + 2], hi[4 * c + 3]);
+              *reinterpret_cast<uint4*>(Klo + off) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+            }
           }
         }
 #pragma unroll
