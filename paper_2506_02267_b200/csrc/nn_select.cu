@@ -499,9 +499,24 @@ __device__ __forceinline__ void select_direct(const KeySrc& ks, const float* ucf
 __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn, const NNScan& sc,
                                                int32_t* idx, float* scores);
 
+// CTA -> (candidate pair, source): source-major, so with the C2 shapes the
+// first candidate of every SKUT CTA (items < 148, SelFlags) is selected in
+// the first wave (a candidate-major order measured 1% slower)
+__device__ __forceinline__ int sel_item(int warp) { return blockIdx.x * kSelWarps + warp; }
+__device__ __forceinline__ int sel_source() { return blockIdx.y; }
+
 __global__ void __launch_bounds__(32 * kSelWarps) nn_select_kernel(Staged st, NNCfg nn, NNScan sc,
-                                                                   int32_t* idx, float* scores) {
+                                                                   int32_t* idx, float* scores, SelFlags sel) {
   nn_select_body(st, nn, sc, idx, scores);
+  if (sel.done) {  // this (candidate, source)'s idx / scores rows are written (release)
+    const int item = sel_item(threadIdx.x >> 5);
+    if (item < st.n_items && item < sel.n_first) {
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) {
+        st_release_gpu(sel.done + 3 * item + sel_source(), sel.epoch);
+      }
+    }
+  }
   __syncthreads();
   cta_stamp(kDbgSelect, 1);
 }
@@ -516,10 +531,13 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
   uint64_t (&keys_s)[kSelWarps][kSelCap] = buf;
   cta_stamp(kDbgSelect, 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int item = blockIdx.x * kSelWarps + warp;
-  const int s = blockIdx.y;
-  griddep_launch();
+  const int item = sel_item(warp);
+  const int s = sel_source();
   griddep_wait();  // scan pass 2 complete
+  // dependents launch only now: with SelFlags the SKUT kernel skips its
+  // up-front griddep_wait, so it must not start before prep .. scan2 are
+  // complete (measured: no cost against triggering at CTA start)
+  griddep_launch();
   cta_stamp(kDbgSelect, 2);
   if (item >= st.n_items) return;  // warp-uniform
   const ReqInfo& rq = st.req[st.item_req[item]];
@@ -601,10 +619,10 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
 cudaError_t set_dbg_cta_select(long long* dev) { return set_dbg_cta_tu(dev); }
 
 cudaError_t launch_nn_select(const Staged& st, const NNCfg& nn, const NNScan& sc, int32_t* idx,
-                             float* scores, cudaStream_t s) {
+                             float* scores, SelFlags sel, cudaStream_t s) {
   if (st.n_items == 0) return cudaSuccess;
-  dim3 grid((st.n_items + kSelWarps - 1) / kSelWarps, 3);
-  return launch_pdl(nn_select_kernel, grid, dim3(32 * kSelWarps), 0, s, st, nn, sc, idx, scores);
+  const dim3 grid((st.n_items + kSelWarps - 1) / kSelWarps, 3);
+  return launch_pdl(nn_select_kernel, grid, dim3(32 * kSelWarps), 0, s, st, nn, sc, idx, scores, sel);
 }
 
 }  // namespace tav2

@@ -127,6 +127,8 @@ struct tav2_ctx {
 
   int32_t* idx = nullptr;
   float* logits = nullptr;
+  uint32_t* sel_done = nullptr;  // per-(candidate, source) select flags (SelFlags)
+  uint32_t sel_epoch = 0;
   float* skut_scratch = nullptr;
   // params
   float* d_params = nullptr;
@@ -256,6 +258,7 @@ int free_all(tav2_ctx* c) {
   cudaFree(c->scan.count);
   cudaFree(c->scan.surv);
   cudaFree(c->idx);
+  cudaFree(c->sel_done);
   cudaFree(c->logits);
   cudaFree(c->skut_scratch);
   cudaFree(c->d_params);
@@ -397,6 +400,8 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
   if ((e = cudaMalloc(&c->scan.surv, (size_t)N * c->scan.surv_stride * 2)) != cudaSuccess)
     return bad(e, "scan survivors");
   if ((e = cudaMalloc(&c->idx, (size_t)N * S * 4)) != cudaSuccess) return bad(e, "idx");
+  if ((e = cudaMalloc(&c->sel_done, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "select flags");
+  if ((e = cudaMemset(c->sel_done, 0, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "select flags");
   if ((e = cudaMalloc(&c->logits, (size_t)N * kHeads * 4)) != cudaSuccess) return bad(e, "logits");
   {
     int sms = 148;
@@ -935,20 +940,30 @@ int check_ready(tav2_ctx* c, int mode) {
   return TAV2_OK;
 }
 
+// Fused select -> SKUT runs hand over per candidate (SelFlags): a fresh
+// epoch per run, so flags left by any earlier run never match.
+SelFlags next_sel(tav2_ctx* c) {
+#ifdef TAV2_NO_SELFLAGS
+  return SelFlags{nullptr, 0, 0};
+#endif
+  if (++c->sel_epoch == 0) c->sel_epoch = 1;
+  return SelFlags{c->sel_done, c->sel_epoch, device_sms()};
+}
+
 // NN selection (both precision modes: the scan's survivors are re-scored with
 // the reference's f64 formula, so the index sets are the reference's).
-int run_nn(tav2_ctx* c, int32_t* idx, float* scores, cudaStream_t s) {
+int run_nn(tav2_ctx* c, int32_t* idx, float* scores, cudaStream_t s, SelFlags sel = {nullptr, 0, 0}) {
   Staged st = staged_view(c);
   CU(timed(c, "prep", s, [&] { return launch_prep(st, c->params_ok ? &c->params : nullptr, s); }));
   CU(timed(c, "nn_scan1", s, [&] { return launch_nn_scan(st, c->nn, c->scan, 1, s); }));
   CU(timed(c, "nn_bound", s, [&] { return launch_nn_bound(st, c->nn, c->scan, s); }));
   CU(timed(c, "nn_scan2", s, [&] { return launch_nn_scan(st, c->nn, c->scan, 2, s); }));
-  CU(timed(c, "nn_select", s, [&] { return launch_nn_select(st, c->nn, c->scan, idx, scores, s); }));
+  CU(timed(c, "nn_select", s, [&] { return launch_nn_select(st, c->nn, c->scan, idx, scores, sel, s); }));
   return TAV2_OK;
 }
 
 int run_score(tav2_ctx* c, int mode, const int32_t* idx, float* logits, float* pooled,
-              cudaStream_t s) {
+              cudaStream_t s, SelFlags sel = {nullptr, 0, 0}) {
   if (!c->params_ok) return fail(TAV2_ESTATE, "parameters not loaded");
   Staged st = staged_view(c);
   // The 2-row-tile tensor-core SKUT holds K/V of <= 256 keys in shared
@@ -959,7 +974,7 @@ int run_score(tav2_ctx* c, int mode, const int32_t* idx, float* logits, float* p
   const bool tc3_ok = c->cs_bound3 <= 60.0, tc_ok = c->cs_bound <= 60.0;
   if (mode == TAV2_MODE_BF16 && tc3_ok && skut_tc3_supported(c->nn, c->params)) {
     CU(timed(c, "skut_tc3", s, [&] {
-      return launch_skut_tc3(c->params, c->images3, c->nn, st, idx, st.n_items, logits, pooled, s);
+      return launch_skut_tc3(c->params, c->images3, c->nn, st, idx, st.n_items, logits, pooled, sel, s);
     }));
     return TAV2_OK;
   }
@@ -1044,8 +1059,9 @@ int tav2_run_staged(tav2_ctx* c, int mode, float* logits_dev, void* stream) {
   CU(cudaSetDevice(c->device));
   cudaStream_t s = (cudaStream_t)stream;
   c->launches = 0;
-  if ((rc = run_nn(c, c->idx, nullptr, s))) return rc;
-  if ((rc = run_score(c, mode, c->idx, logits_dev ? logits_dev : c->logits, nullptr, s))) return rc;
+  const SelFlags sel = next_sel(c);
+  if ((rc = run_nn(c, c->idx, nullptr, s, sel))) return rc;
+  if ((rc = run_score(c, mode, c->idx, logits_dev ? logits_dev : c->logits, nullptr, s, sel))) return rc;
   return mark_used(c, s);
 }
 
@@ -1059,8 +1075,9 @@ int tav2_rank_submit(tav2_ctx* c, const tav2_request* reqs, int n_req, int mode,
   int rc = tav2_stage(c, reqs, n_req, stream, &n);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  if ((rc = run_nn(c, c->idx, nullptr, s))) return rc;
-  if ((rc = run_score(c, mode, c->idx, c->logits, nullptr, s))) return rc;
+  const SelFlags sel = next_sel(c);
+  if ((rc = run_nn(c, c->idx, nullptr, s, sel))) return rc;
+  if ((rc = run_score(c, mode, c->idx, c->logits, nullptr, s, sel))) return rc;
   CU(cudaMemcpyAsync(c->h_out[slot], c->logits, (size_t)n * kHeads * 4, cudaMemcpyDeviceToHost, s));
   if (want_idx)
     CU(cudaMemcpyAsync(c->h_idx[slot], c->idx, (size_t)n * c->nn.seq_len * 4, cudaMemcpyDeviceToHost, s));

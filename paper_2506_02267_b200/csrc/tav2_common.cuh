@@ -206,6 +206,30 @@ namespace tav2 {
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Per-(candidate, source) completion flags of nn_select for the first
+// candidate of every SKUT CTA (items < n_first = the SKUT grid size): a SKUT
+// CTA starts its first candidate as soon as that candidate's three
+// selections are written instead of waiting for the whole select grid, so
+// the select kernel's tail overlaps the transformer; before its second
+// candidate's idx reads it executes griddep_wait (by then select is
+// normally long complete).  done[3 item + s] = epoch (a per-context counter,
+// never 0, bumped per fused run) is stored with release semantics after the
+// warp's idx writes; the reader spins with ld.acquire.  done == null:
+// griddep_wait up front as for every other kernel.
+struct SelFlags {
+  uint32_t* done;
+  uint32_t epoch;
+  int n_first;
+};
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) and the SM count cost a
 // host round trip each; every launcher calls these instead (cached per
 // kernel and device, defined in tav2_api.cu)
@@ -235,7 +259,8 @@ namespace tav2 {
 cudaError_t launch_prep(const Staged& st, const Params* p, cudaStream_t s);
 bool skut_tc3_supported(const NNCfg& nn, const Params& p);
 cudaError_t launch_skut_tc3(const Params& p, const SkutImages3& img, const NNCfg& nn, const Staged& st,
-                            const int32_t* idx, int n, float* logits, float* pooled, cudaStream_t s);
+                            const int32_t* idx, int n, float* logits, float* pooled, SelFlags sel,
+                            cudaStream_t s);
 cudaError_t launch_nn_scan(const Staged& st, const NNCfg& nn, const NNScan& sc, int pass,
                            cudaStream_t s);
 cudaError_t launch_nn_bound(const Staged& st, const NNCfg& nn, const NNScan& sc, cudaStream_t s);
@@ -243,7 +268,7 @@ cudaError_t launch_store_gather(const StoreCopy* d, int n, int max_tok, const in
                                 const uint16_t* sact, const uint8_t* ssurf, int8_t* demb, uint16_t* dact,
                                 uint8_t* dsurf, cudaStream_t s);
 cudaError_t launch_nn_select(const Staged& st, const NNCfg& nn, const NNScan& sc, int32_t* idx,
-                             float* scores, cudaStream_t s);
+                             float* scores, SelFlags sel, cudaStream_t s);
 cudaError_t set_debug_timeline(long long* dev, int block);
 cudaError_t set_debug_skut(long long* dev);
 cudaError_t set_debug_skut3(long long* dev);
