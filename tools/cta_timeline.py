@@ -70,3 +70,17 @@ if sel.any():
                   f"med {np.median(st_t[m]) / 1e3:.2f} us, threshold found med {np.median(bi_t[m]) / 1e3:.2f} us, "
                   f"n med {np.median(rec_n[m]):.0f}")
 
+
+if "--detail" in sys.argv:  # the slowest CTAs of every kernel
+    for k, name in enumerate(KERNELS):
+        n = int((t[k, 0] > 0).sum())
+        if not n:
+            continue
+        st, en, rd = t[k, 0, :n], t[k, 1, :n], t[k, 2, :n]
+        if not ((rd > 0).all() and (en > 0).all()):
+            continue
+        d = (en - rd) / 1e3
+        top = np.argsort(-d)[:6]
+        print(f"{name}: run > 2 us: {(d > 2).sum()} CTAs; slowest (cta, launch, ready, end, run):",
+              [(int(i), round((st[i] - t0) / 1e3, 2), round((rd[i] - t0) / 1e3, 2), round((en[i] - t0) / 1e3, 2),
+                round(float(d[i]), 2)) for i in top])
