@@ -160,7 +160,7 @@ def cpu_baseline(cfg_name, steps=3, warmup=1, budget_s=60.0, procs=None, n_per_p
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     try:
         with ctx.Pool(procs, initializer=_cpu_init, initargs=(0, n, L, nn)) as pool:
-            for _ in range(max(1, min(warmup, 2))):
+            for _ in range(max(1, min(warmup, 5))):
                 pool.map(_cpu_step, range(procs))
             done, lats, wall, k = 0, [], 0.0, 0
             while k < max(1, steps) and (k == 0 or wall < budget_s):
@@ -455,7 +455,7 @@ def main():
         value = cb["value"]
         print(json.dumps({
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "impl": "reference",
-            "n_gpus": 0, "steps": cb["steps_timed"], "warmup": min(args.warmup, 2),
+            "n_gpus": 0, "steps": cb["steps_timed"], "warmup": max(1, min(args.warmup, 5)),
             "ms_per_step": round(1e3 * n_cand / value, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64 (numpy)",
             "data": "synthetic (generate_requests), random-init weights seed 0",
