@@ -56,3 +56,19 @@ def test_unfused_between_fused_runs():
     assert np.array_equal(lg2, fused2)
     again, _ = eng.rank_requests(b1, mode="bf16", return_indices=True)
     assert np.array_equal(first, again)
+
+
+def test_multi_request_batch_fused_equals_unfused():
+    """Several requests co-batched (600 items > 148 flagged first candidates):
+    the items past the first SKUT wave go through griddepcontrol.wait."""
+    nn = P.NNConfig()
+    model = P.RankingModel.init(P.ModelConfig.for_nn(nn), seed=2)
+    eng = Engine(model, capacity=Capacity(6, 600, 6 * 16896))
+    ref = Engine(model, capacity=Capacity(6, 600, 6 * 16896))
+    reqs = P.generate_requests(6, 100, ll_tokens=8192, seed=11)
+    batch = [(r.user, r.candidates, r.ctx) for r in reqs]
+    for _ in range(2):
+        lg, idx = eng.rank_requests(batch, mode="bf16", return_indices=True)
+        rl, ri = _unfused(ref, batch, nn)
+        assert np.array_equal(idx, ri)
+        assert np.array_equal(lg, rl)
