@@ -24,7 +24,7 @@
 // sub-partition holds one early and one late block, and tile 0 only needs
 // the keys < S_pad/2 (half the score / P.V MMA work).  Two independent
 // tiles (warps 4t..4t+3), each with its own TMEM half (256 columns), its own
-// simt/mma barriers and issuer (thread 128t); they couple only through the
+// simt/mma barriers and issuing warp (warp 4t); they couple only through the
 // K/V operands (kvready / kvfree).  All weight images stay resident in
 // shared memory for the CTA's lifetime (loaded once); the token features of
 // the gather come precomputed from prep_kernel (tok_feat).
@@ -132,15 +132,18 @@ __device__ __forceinline__ void t3_layer_norm(const float* x, const float* g, co
   }
 }
 
-// D += A(TMEM hi/lo) x B(smem hi/lo, K-major slabs), 3 terms per k-step
+// D += A(TMEM hi/lo) x B(smem hi/lo, K-major slabs), 3 terms per k-step;
+// warp-collective (one elected lane issues), fully unrolled
+template <int KSTEPS>
 __device__ __forceinline__ void t3_mma3(uint32_t d, uint32_t a_col, uint32_t a_lo_off, uint32_t b_hi,
-                                        uint32_t b_lo, uint32_t lbo, int ksteps, uint32_t idesc) {
-  for (int j = 0; j < ksteps; ++j) {
+                                        uint32_t b_lo, uint32_t lbo, uint32_t idesc) {
+#pragma unroll
+  for (int j = 0; j < KSTEPS; ++j) {
     const uint64_t bh = sdesc(b_hi + 2 * j * lbo, lbo, 128);
     const uint64_t bl = sdesc(b_lo + 2 * j * lbo, lbo, 128);
-    mma_bf16_ts(d, a_col + 8 * j, bh, idesc, j > 0);
-    mma_bf16_ts(d, a_col + 8 * j, bl, idesc, 1);
-    mma_bf16_ts(d, a_col + a_lo_off + 8 * j, bh, idesc, 1);
+    mma_bf16_ts_w(d, a_col + 8 * j, bh, idesc, j > 0);
+    mma_bf16_ts_w(d, a_col + 8 * j, bl, idesc, 1);
+    mma_bf16_ts_w(d, a_col + a_lo_off + 8 * j, bh, idesc, 1);
   }
 }
 
@@ -208,7 +211,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     bulk_g2s(Wsm + NL * kW3Layer, img.wout, kImg3WO, &t3.wfull);
   }
 
-  const bool issuer = (tid & 127) == 0;
+  const bool issuer = (tid & 127) == 0;  // debug stamps only
+  const bool issue_warp = q == 0;         // warp 4t issues tile t's MMAs (warp-collective)
   long long* dbg = (kDebug && blockIdx.x == 0 && issuer && g_dbg_skut3) ? g_dbg_skut3 + 32 * (tid >> 7) : nullptr;
   long long t_last = 0;
   auto stamp = [&](int id) {
@@ -254,7 +258,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   if (sel.done) __syncthreads();
   bool sel_all = !sel.done;  // the whole select grid is complete and visible
   cta_stamp(kDbgSkut, 2);
-  if (issuer) {
+  if (issue_warp) {
     mbar_wait(&t3.wfull, 0);
     fence_after();
   }
@@ -390,11 +394,11 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         done();
       }
       stamp(3);
-      if (issuer) {  // M1: [Q' | V'] = A [Wqk | Wvo]   (N = 128, K = 64)
+      if (issue_warp) {  // M1: [Q' | V'] = A [Wqk | Wvo]   (N = 128, K = 64)
         issuer_wait_simt();
         stamp(28);
-        t3_mma3(R + kCD, R + kCA, 32, wa(L), wa(L) + kImg3WA / 2, 128 * 16, 4, idesc_bf16(128, 128));
-        commit(&t3.mma[t]);
+        t3_mma3<4>(R + kCD, R + kCA, 32, wa(L), wa(L) + kImg3WA / 2, 128 * 16, idesc_bf16(128, 128));
+        commit_w(&t3.mma[t]);
       }
       stamp(4);
       // ---- P2: Q' -> A, V' -> smem (MN-major) ----
@@ -444,11 +448,11 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         mbar_arrive(&t3.kvready);  // this row's K, V' and Q' are in place
       }
       stamp(6);
-      if (issuer) {  // M2: S = Q' K^T   (N = keys of this tile, K = 64)
+      if (issue_warp) {  // M2: S = Q' K^T   (N = keys of this tile, K = 64)
         mbar_wait(&t3.kvready, n_kv & 1);
         fence_after();
-        t3_mma3(R + kCD, R + kCA, 32, khi, klo, S_pad * 16, 4, idesc_bf16(128, NK));
-        commit(&t3.mma[t]);
+        t3_mma3<4>(R + kCD, R + kCA, 32, khi, klo, S_pad * 16, idesc_bf16(128, NK));
+        commit_w(&t3.mma[t]);
       }
       stamp(7);
       // ---- P3: causal key-masked softmax -> P (bf16 hi/lo, in place over S) ----
@@ -530,19 +534,23 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         done();
       }
       stamp(9);
-      if (issuer) {  // M3: O' = P V'   (N = 64, K = keys; V' MN-major)
+      if (issue_warp) {  // M3: O' = P V'   (N = 64, K = keys; V' MN-major)
         issuer_wait_simt();
         stamp(29);
         const uint32_t id = idesc_bf16(128, 64, 0, 1);
-        for (int j = 0; j < NK / 16; ++j) {
-          const uint64_t bh = sdesc(vhi + 2 * j * 1024, 1024, 128);
-          const uint64_t bl = sdesc(vlo + 2 * j * 1024, 1024, 128);
-          mma_bf16_ts(R + kCA, R + kCD + 16 * j, bh, id, j > 0);
-          mma_bf16_ts(R + kCA, R + kCD + 16 * j, bl, id, 1);
-          mma_bf16_ts(R + kCA, R + kCD + 16 * j + 8, bh, id, 1);
+        const int nk16 = NK / 16;  // <= 12 (S_pad <= 192); unrolled, warp-uniform bound
+#pragma unroll
+        for (int j = 0; j < 12; ++j) {
+          if (j < nk16) {
+            const uint64_t bh = sdesc(vhi + 2 * j * 1024, 1024, 128);
+            const uint64_t bl = sdesc(vlo + 2 * j * 1024, 1024, 128);
+            mma_bf16_ts_w(R + kCA, R + kCD + 16 * j, bh, id, j > 0);
+            mma_bf16_ts_w(R + kCA, R + kCD + 16 * j, bl, id, 1);
+            mma_bf16_ts_w(R + kCA, R + kCD + 16 * j + 8, bh, id, 1);
+          }
         }
-        commit(&t3.mma[t]);
-        commit(&t3.kvfree);  // this tile no longer reads K / V' of this layer
+        commit_w(&t3.mma[t]);
+        commit_w(&t3.kvfree);  // this tile no longer reads K / V' of this layer
       }
       stamp(10);
       ++n_kv;
@@ -570,11 +578,11 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         done();
       }
       stamp(12);
-      if (issuer) {  // M4: H = A W1   (N = 32, K = 64)
+      if (issue_warp) {  // M4: H = A W1   (N = 32, K = 64)
         issuer_wait_simt();
         stamp(30);
-        t3_mma3(R + kCD, R + kCA, 32, wb(L), wb(L) + 4096, 32 * 16, 4, idesc_bf16(128, 32));
-        commit(&t3.mma[t]);
+        t3_mma3<4>(R + kCD, R + kCA, 32, wb(L), wb(L) + 4096, 32 * 16, idesc_bf16(128, 32));
+        commit_w(&t3.mma[t]);
       }
       stamp(13);
       // ---- P5: ReLU(H) -> A2 ----
@@ -591,10 +599,10 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         done();
       }
       stamp(15);
-      if (issuer) {  // M5: D2 = ReLU(H) W2   (N = 64, K = 32)
+      if (issue_warp) {  // M5: D2 = ReLU(H) W2   (N = 64, K = 32)
         issuer_wait_simt();
-        t3_mma3(R + kCW2, R + kCA2, 16, wb(L) + 8192, wb(L) + 8192 + 4096, 64 * 16, 2, idesc_bf16(128, 64));
-        commit(&t3.mma[t]);
+        t3_mma3<2>(R + kCW2, R + kCA2, 16, wb(L) + 8192, wb(L) + 8192 + 4096, 64 * 16, idesc_bf16(128, 64));
+        commit_w(&t3.mma[t]);
       }
       stamp(16);
       // ---- P6: x += D2 ----
@@ -620,11 +628,11 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     tmem_st_wait();
     done();
     stamp(19);
-    if (issuer) {
+    if (issue_warp) {
       issuer_wait_simt();
-      t3_mma3(R + kCD, R + kCA, 32, wsm + NL * kW3Layer, wsm + NL * kW3Layer + 8192, 64 * 16, 4,
-              idesc_bf16(128, 64));
-      commit(&t3.mma[t]);
+      t3_mma3<4>(R + kCD, R + kCA, 32, wsm + NL * kW3Layer, wsm + NL * kW3Layer + 8192, 64 * 16,
+                 idesc_bf16(128, 64));
+      commit_w(&t3.mma[t]);
     }
     stamp(20);
     wait_mma();

@@ -130,6 +130,36 @@ __device__ __forceinline__ void mma_i8_ss(uint32_t d_tmem, uint64_t a, uint64_t 
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;}\n" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accum));
 }
+// Warp-collective issue: the whole (converged) warp executes these and
+// elect.sync picks one lane (always the lowest active lane, so the same
+// thread issues the MMAs and the commit that tracks them).  Versus issuing
+// from one thread under a divergent `if`, the operands stay warp-uniform and
+// the compiler emits no ELECT / R2UR.BROADCAST waterfall loop per MMA:
+// back-to-back MMAs then issue at the tensor-pipe floor (N/2 cycles at
+// M = 128, tools/mma_bench4.cu: 17 cycles at N = 32 vs 45-260 before).
+__device__ __forceinline__ void mma_bf16_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
+                                              uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{.reg .pred p, e; setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_bf16_ss_w(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                              uint32_t accum) {
+  asm volatile(
+      "{.reg .pred p, e; setp.ne.b32 p, %4, 0;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void commit_w(uint64_t* bar) {
+  asm volatile(
+      "{.reg .pred e; elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
 // Arrive on an mbarrier when all prior tcgen05 async ops of this thread finish.
 __device__ __forceinline__ void commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
