@@ -6,9 +6,13 @@ candidates scored/sec at 16k lifelong seq; p50/p99 request ms).
 
 One step = one request of BASELINE configs[1] (1 user, 1,000 candidates,
 L=16,384, NNConfig(32, 96, 32, 32) -> S=192) through stage -> NN select ->
-SKUT -> head.  N>1 (torchrun, one rank per GPU): every rank scores its own
-independent requests (weak scaling, no data-path collective); ``value`` is
-the aggregate over ranks / the max-over-ranks device time.
+SKUT -> head.  N>1: ``--gpus N`` re-launches itself under
+torch.distributed.run (one rank per GPU, NCCL; or the driver's own torchrun
+launch is used as is); every rank scores its own independent requests (weak
+scaling, no data-path collective; ``--config c3``: 32 x 500 per rank); with
+``--config c4`` the ranks split one 8,192-candidate request and all-gather
+its logits every step (strong scaling).  ``value`` is the aggregate over
+ranks / the max-over-ranks device time.
 
 ``value``: device-resident inputs (staged once per pool request), CUDA events
 around each step on the launch stream, L2 flushed between timed steps.
@@ -432,6 +436,59 @@ def _staged_bytes(reqs):
     return tok * (32 + 2 + 1) + n * (32 * 4 + 4) + len(reqs) * (8 * 4 + 40)
 
 
+def _free_port():
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(nproc: int, argv: list[str]) -> int:
+    """``--gpus N`` (N > 1) outside a torchrun environment: re-launch this
+    script under ``torch.distributed.run``, one process per GPU on this node
+    (127.0.0.1 rendezvous; RANK / LOCAL_RANK / WORLD_SIZE come from the
+    launcher).  NCCL_DEBUG=INFO so the communicator set-up lines show in the
+    log; rank 0 prints the one JSON line last.  Returns the exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.abspath(__file__), *argv]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args, rank, world):
+    """CPU stand-in for one rank (``--dry-run``, gloo): the launcher, the
+    barrier + max-over-ranks timing and the rank-0 JSON line without a GPU
+    (tests/test_multiproc.py)."""
+    import torch
+    import torch.distributed as dist
+
+    n_req, n_cand, L, nn_t = CONFIGS[args.config]
+    x = np.random.default_rng(rank).normal(size=(64, 64)).astype(np.float32)
+    for _ in range(args.warmup):
+        x = np.tanh(x @ x.T / 64)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        x = np.tanh(x @ x.T / 64)
+    t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sec = float(t.item())
+    job = world * n_req * n_cand if args.config != "c4" else n_req * n_cand
+    return {"metric": METRIC, "value": round(job * args.steps / sec, 1), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sec / args.steps, 4),
+            "higher_is_better": True, "scaling": "strong" if args.config == "c4" else "weak",
+            "vs_baseline": None, "dry_run": True,
+            "config": {"workload": f"{args.config} (dry run: CPU stand-in step, no GPU)",
+                       "parallelism": f"x{world} ranks (gloo)"}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -442,10 +499,16 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--pool", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="CPU stand-in ranks over gloo (launcher test)")
     args = ap.parse_args()
+    launched = "WORLD_SIZE" in os.environ
+    if args.gpus > 1 and not launched and args.impl == "ours":
+        sys.exit(launch_ranks(args.gpus, sys.argv[1:]))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if launched and world != args.gpus and rank == 0:
+        print(f"bench: WORLD_SIZE={world} differs from --gpus {args.gpus}; using {world}", file=sys.stderr)
 
     if args.impl == "reference":
         if rank != 0:
@@ -470,19 +533,27 @@ def main():
         }))
         return
 
+    import torch.distributed as dist
+
     if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", init_method="env://")
-    out = run_gpu(args, rank, world, local_rank)
-    if rank == 0:
-        if world == 1 and not args.no_cpu_baseline:
+        dist.init_process_group("gloo" if args.dry_run else "nccl", init_method="env://")
+    if args.dry_run:
+        out = run_dry(args, rank, world)
+    else:
+        import torch
+
+        if torch.cuda.device_count() < world:
+            raise SystemExit(f"bench: {world} ranks but only {torch.cuda.device_count()} visible GPU(s)")
+        out = run_gpu(args, rank, world, local_rank)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
             cb = cpu_baseline(args.config, steps=3, warmup=1, budget_s=20.0)
             out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
                                                        "per_process_cand_s", "p50_sample_ms", "p99_sample_ms")}
-        print(json.dumps(out))
     if world > 1:
-        import torch.distributed as dist
+        dist.barrier()
         dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__":
