@@ -33,7 +33,7 @@ extern "C" {
 /* Precision modes of the scoring path (north_star: fp32 parity mode and the
  * bf16 headline mode). */
 #define TAV2_MODE_FP32 0  /* SIMT fp32 transformer, f64 NN scores (ref-faithful) */
-#define TAV2_MODE_BF16 1  /* tcgen05: i8-limb NN GEMM + bf16x3 SKUT              */
+#define TAV2_MODE_BF16 1  /* tcgen05: fp16 NN scan + f64 re-scoring, bf16x3 SKUT */
 
 /* ModelConfig (trainer.py:42-70) + NNConfig (nnsearch.py:25-46) as ints. */
 typedef struct {
@@ -98,8 +98,22 @@ int tav2_stage(tav2_ctx* ctx, const tav2_request* reqs, int n_req, void* stream,
  * NN segment the top-k token indices (stable ties -> lower index), laid out
  * in Eq. 2 order (nnsearch.py:153-180).  idx_dev: [n_items, seq_len] int32,
  * source-relative indices (RT-tail offset by `recent`), -1 on padding.
- * scores_dev (nullable): [n_items, seq_len] f32 score of each NN slot. */
-int tav2_nn_select(tav2_ctx* ctx, int mode, int32_t* idx_dev, float* scores_dev, void* stream);
+ * scores_dev (nullable): [n_items, seq_len] f64 score of each NN slot -- the
+ * reference's float64 dot of the f32 unit vectors (nnsearch.py:344-347,
+ * returned by fused_assemble(return_scores=True) at :362-363); 0 elsewhere. */
+int tav2_nn_select(tav2_ctx* ctx, int mode, int32_t* idx_dev, double* scores_dev, void* stream);
+
+/* similarity_scores (nnsearch.py:83-90) on the staged batch: the f64 score
+ * of every token of `source` (0 = LL, 1 = RT, 2 = IMP; all tokens, RT from
+ * index 0) of item `item`'s request against that item's candidate.
+ * scores_dev: [len(source)] f64. */
+int tav2_similarity(tav2_ctx* ctx, int32_t item, int32_t source, double* scores_dev, void* stream);
+
+/* pool (encoder.py:265-273) over caller encoder outputs: u_dev [n, seq_len,
+ * 64] f32, mask_dev [n, seq_len] u8 -> pooled_dev [n, 64] f32 (max over the
+ * valid rows of U out_linear; zeros for an item with no valid row). */
+int tav2_pool(tav2_ctx* ctx, const float* u_dev, const uint8_t* mask_dev, int32_t n, float* pooled_dev,
+              void* stream);
 
 /* encode_batch (encoder.py:161-188) from staged tokens + idx_dev:
  * features_dev [n_items, seq_len, 64] f32, mask_dev [n_items, seq_len] u8. */

@@ -9,11 +9,18 @@ from .core import (  # noqa: F401
     EMBED_DIM, LIFELONG_CAP, REALTIME_CAP, IMPRESSION_CAP, TokenBlock, UserSequences,
     ValidationError, dequantize, l2_normalize_rows, quantize, unit_embeddings,
 )
-from .dataset import HEAD_NAMES, NUM_HEADS, context_features, generate_requests  # noqa: F401
-from .encoder import EncoderConfig, EncoderParams, LayerParams  # noqa: F401
+from .dataset import (  # noqa: F401
+    HEAD_NAMES, NUM_HEADS, SyntheticConfig, context_features, generate_requests, generate_synthetic,
+    synthetic_requests,
+)
+from .encoder import (  # noqa: F401
+    EncodedSequence, EncoderConfig, EncoderParams, LayerParams, encode, encode_batch, forward_fused,
+    forward_reference, pool,
+)
 from .model import HeadConfig, HeadParams, ModelConfig, RankingModel  # noqa: F401
 from .nnsearch import (  # noqa: F401
-    AssembledSequence, DedupBatch, NNConfig, Segment, build_dedup_batch, fused_assemble,
+    AssembledSequence, DedupBatch, NNConfig, Segment, assemble, build_dedup_batch, fused_assemble,
+    similarity_scores, top_k_nn,
 )
 
 __version__ = "0.1.0"
@@ -28,4 +35,8 @@ def __getattr__(name):  # lazy: torch + the native library load on first use
         from . import serving
 
         return getattr(serving, name)
+    if name in ("model_forward", "ForwardState", "TrainBatch"):
+        from . import trainer
+
+        return getattr(trainer, name)
     raise AttributeError(name)

@@ -132,7 +132,7 @@ __device__ __forceinline__ void bm_clear(uint32_t* bm, int words, int lane) {
 // segment order, nnsearch.py:364): lane l scans its words high first; a warp
 // prefix sum of the per-lane counts places its bits.
 __device__ __forceinline__ void emit_bitmap(const uint32_t* bm, int words, int k, int lane, int32_t* orow,
-                                            float* srow, const KeySrc& ks) {
+                                            double* srow, const KeySrc& ks) {
   const int per = (words + 31) / 32;
   const int w_hi = words - per * lane;  // this lane's logical words: [w_hi - per, w_hi)
   int cnt = 0;
@@ -157,7 +157,7 @@ __device__ __forceinline__ void emit_bitmap(const uint32_t* bm, int words, int k
           float4 r[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q) r[q] = __ldg(reinterpret_cast<const float4*>(ks.tok + (size_t)t * kEmbed) + q);
-          srow[pos] = (float)dot_exact(r, ks.uc);
+          srow[pos] = dot_exact(r, ks.uc);
         }
       }
       ++pos;
@@ -166,7 +166,7 @@ __device__ __forceinline__ void emit_bitmap(const uint32_t* bm, int words, int k
   const int total = __shfl_sync(0xffffffffu, incl, 31);
   for (int j = total + lane; j < k; j += 32) {
     orow[j] = -1;
-    if (srow) srow[j] = 0.0f;
+    if (srow) srow[j] = 0.0;
   }
 }
 
@@ -303,7 +303,7 @@ __device__ __forceinline__ void warp_bitonic_desc_smem(uint64_t* a, int n, int l
 // warp-aggregated histogram) isolates the top k, then a shared bitonic sort
 // orders the winners by index.
 __device__ __forceinline__ void select_radix(const KeySrc& ks, int n, int k, int lane, uint64_t* a,
-                                             unsigned* hist, int32_t* orow, float* srow) {
+                                             unsigned* hist, int32_t* orow, double* srow) {
   const bool cached = n <= kSelCap;
   if (cached) {
     for (int i = lane; i < n; i += 32) a[i] = ks.key(i);
@@ -381,7 +381,17 @@ __device__ __forceinline__ void select_radix(const KeySrc& ks, int n, int k, int
   for (int j = lane; j < k; j += 32) {
     const uint64_t e = j < v ? a[j] : 0ull;
     orow[j] = e ? (int32_t)(e >> 32) - 1 : -1;
-    if (srow) srow[j] = e ? __uint_as_float((uint32_t)e) : 0.0f;
+    if (srow) {  // the exact f64 key of the winner (its f32 image only sorts)
+      double v = 0.0;
+      if (e) {
+        float4 r[8];
+        const int t = (int)(e >> 32) - 1;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) r[q] = __ldg(reinterpret_cast<const float4*>(ks.tok + (size_t)t * kEmbed) + q);
+        v = dot_exact(r, ks.uc);
+      }
+      srow[j] = v;
+    }
   }
 }
 
@@ -497,7 +507,7 @@ __device__ __forceinline__ void select_direct(const KeySrc& ks, const float* ucf
 }
 
 __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn, const NNScan& sc,
-                                               int32_t* idx, float* scores);
+                                               int32_t* idx, double* scores);
 
 // CTA -> (candidate pair, source): source-major, so with the C2 shapes the
 // first candidate of every SKUT CTA (items < 148, SelFlags) is selected in
@@ -506,7 +516,7 @@ __device__ __forceinline__ int sel_item(int warp) { return blockIdx.x * kSelWarp
 __device__ __forceinline__ int sel_source() { return blockIdx.y; }
 
 __global__ void __launch_bounds__(32 * kSelWarps) nn_select_kernel(Staged st, NNCfg nn, NNScan sc,
-                                                                   int32_t* idx, float* scores, SelFlags sel) {
+                                                                   int32_t* idx, double* scores, SelFlags sel) {
   nn_select_body(st, nn, sc, idx, scores);
   if (sel.done) {  // this (candidate, source)'s idx / scores rows are written (release)
     const int item = sel_item(threadIdx.x >> 5);
@@ -522,7 +532,7 @@ __global__ void __launch_bounds__(32 * kSelWarps) nn_select_kernel(Staged st, NN
 }
 
 __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn, const NNScan& sc,
-                                               int32_t* idx, float* scores) {
+                                               int32_t* idx, double* scores) {
   __shared__ uint64_t buf[kSelWarps][kSelCap];  // radix path key cache; also the sort array
   __shared__ unsigned hist_s[kSelWarps][256];
   __shared__ float4 rows_s[kSelWarps][kRowBatch * 8];  // staged token rows (8 KB per warp)
@@ -548,13 +558,13 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
     const int n_recent = min(nn.recent, rq.len[1]);
     for (int j = lane; j < nn.recent; j += 32) {
       idx[(size_t)item * S + nn.seg_start[1] + j] = j < n_recent ? n_recent - 1 - j : -1;
-      if (scores) scores[(size_t)item * S + nn.seg_start[1] + j] = 0.0f;
+      if (scores) scores[(size_t)item * S + nn.seg_start[1] + j] = 0.0;
     }
   }
   if (k == 0) return;
   const int seg = s == 0 ? 0 : (s == 1 ? 2 : 3);
   int32_t* orow = idx + (size_t)item * S + nn.seg_start[seg];
-  float* srow = scores ? scores + (size_t)item * S + nn.seg_start[seg] : nullptr;
+  double* srow = scores ? scores + (size_t)item * S + nn.seg_start[seg] : nullptr;
   const int lo = s == 1 ? min(nn.recent, rq.len[1]) : 0, hi = rq.len[s];
 
   if (hi - lo <= k) {  // 1. everything selected, descending storage index
@@ -565,9 +575,13 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
       orow[j] = t >= lo ? t : -1;
       if (srow) {  // reference score: f64 dot of the f32 unit vectors (nnsearch.py:344-347)
         double a = 0.0;
-        if (t >= lo)
-          for (int q = 0; q < kEmbed; ++q) a = fma((double)tok[(size_t)t * kEmbed + q], (double)cu[q], a);
-        srow[j] = (float)a;
+        if (t >= lo) {
+          float4 r[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) r[q] = __ldg(reinterpret_cast<const float4*>(tok + (size_t)t * kEmbed) + q);
+          a = dot_exact(r, cu);
+        }
+        srow[j] = a;
       }
     }
     return;
@@ -618,8 +632,34 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
 
 cudaError_t set_dbg_cta_select(long long* dev) { return set_dbg_cta_tu(dev); }
 
+// similarity_scores (nnsearch.py:83-90): the f64 dot of every token of one
+// source of a staged request with one staged candidate -- the f32 unit rows
+// prep_kernel derived (core.py:54-79 op order), widened to f64 exactly as
+// the reference's unit64 @ cand64 (nnsearch.py:344-347).  Thread per token.
+__global__ void __launch_bounds__(256) similarity_kernel(Staged st, int item, int source, double* out) {
+  griddep_wait();
+  const ReqInfo& rq = st.req[st.item_req[item]];
+  const int n = rq.len[source];
+  const float* tok = st.tok_unit + (size_t)rq.tok_off[source] * kEmbed;
+  float uc[kEmbed];
+#pragma unroll
+  for (int q = 0; q < kEmbed; ++q) uc[q] = st.cand_unit[(size_t)item * kEmbed + q];
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    float4 r[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r[q] = __ldg(reinterpret_cast<const float4*>(tok + (size_t)t * kEmbed) + q);
+    out[t] = dot_exact(r, uc);
+  }
+}
+
+cudaError_t launch_similarity(const Staged& st, int item, int source, int n, double* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (n + 255) / 256;
+  return launch_pdl(similarity_kernel, dim3(blocks < 148 ? blocks : 148), dim3(256), 0, s, st, item, source, out);
+}
+
 cudaError_t launch_nn_select(const Staged& st, const NNCfg& nn, const NNScan& sc, int32_t* idx,
-                             float* scores, SelFlags sel, cudaStream_t s) {
+                             double* scores, SelFlags sel, cudaStream_t s) {
   if (st.n_items == 0) return cudaSuccess;
   const dim3 grid((st.n_items + kSelWarps - 1) / kSelWarps, 3);
   return launch_pdl(nn_select_kernel, grid, dim3(32 * kSelWarps), 0, s, st, nn, sc, idx, scores, sel);

@@ -952,7 +952,7 @@ SelFlags next_sel(tav2_ctx* c) {
 
 // NN selection (both precision modes: the scan's survivors are re-scored with
 // the reference's f64 formula, so the index sets are the reference's).
-int run_nn(tav2_ctx* c, int32_t* idx, float* scores, cudaStream_t s, SelFlags sel = {nullptr, 0, 0}) {
+int run_nn(tav2_ctx* c, int32_t* idx, double* scores, cudaStream_t s, SelFlags sel = {nullptr, 0, 0}) {
   Staged st = staged_view(c);
   CU(timed(c, "prep", s, [&] { return launch_prep(st, c->params_ok ? &c->params : nullptr, s); }));
   CU(timed(c, "nn_scan1", s, [&] { return launch_nn_scan(st, c->nn, c->scan, 1, s); }));
@@ -996,7 +996,7 @@ int run_score(tav2_ctx* c, int mode, const int32_t* idx, float* logits, float* p
 
 extern "C" {
 
-int tav2_nn_select(tav2_ctx* c, int mode, int32_t* idx_dev, float* scores_dev, void* stream) {
+int tav2_nn_select(tav2_ctx* c, int mode, int32_t* idx_dev, double* scores_dev, void* stream) {
   int rc = check_ready(c, mode);
   if (rc) return rc;
   if (!idx_dev) return fail(TAV2_EINVAL, "idx_dev is null");
@@ -1004,6 +1004,35 @@ int tav2_nn_select(tav2_ctx* c, int mode, int32_t* idx_dev, float* scores_dev, v
   c->launches = 0;
   int rc2 = run_nn(c, idx_dev, scores_dev, (cudaStream_t)stream);
   return rc2 ? rc2 : mark_used(c, (cudaStream_t)stream);
+}
+
+int tav2_similarity(tav2_ctx* c, int32_t item, int32_t source, double* scores_dev, void* stream) {
+  int rc = check_ready(c, TAV2_MODE_FP32);
+  if (rc) return rc;
+  if (!scores_dev) return fail(TAV2_EINVAL, "scores_dev is null");
+  if (source < 0 || source > 2) return fail(TAV2_EINVAL, "source must be 0 (LL), 1 (RT) or 2 (IMP)");
+  const Plan& pl = c->plans[c->cur];
+  if (item < 0 || item >= pl.n_items) return fail(TAV2_EINVAL, "item %d out of range", item);
+  const ReqInfo* rq = reinterpret_cast<const ReqInfo*>(c->h_arena[c->cur] + pl.off_req);
+  const int32_t* item_req = reinterpret_cast<const int32_t*>(c->h_arena[c->cur] + pl.off_item_req);
+  const int n = rq[item_req[item]].len[source];
+  CU(cudaSetDevice(c->device));
+  Staged st = staged_view(c);
+  CU(launch_prep(st, nullptr, (cudaStream_t)stream));
+  CU(launch_similarity(st, item, source, n, scores_dev, (cudaStream_t)stream));
+  return mark_used(c, (cudaStream_t)stream);
+}
+
+int tav2_pool(tav2_ctx* c, const float* u_dev, const uint8_t* mask_dev, int32_t n, float* pooled_dev,
+              void* stream) {
+  if (!c) return fail(TAV2_EINVAL, "null context");
+  if (!c->params_ok) return fail(TAV2_ESTATE, "parameters not loaded");
+  if (n < 0) return fail(TAV2_EINVAL, "negative batch");
+  if (n == 0) return TAV2_OK;
+  if (!u_dev || !mask_dev || !pooled_dev) return fail(TAV2_EINVAL, "null device pointer");
+  CU(cudaSetDevice(c->device));
+  CU(launch_pool(u_dev, mask_dev, c->params.out_linear, n, c->nn.seq_len, pooled_dev, (cudaStream_t)stream));
+  return TAV2_OK;
 }
 
 int tav2_encode(tav2_ctx* c, const int32_t* idx_dev, float* features_dev, uint8_t* mask_dev,

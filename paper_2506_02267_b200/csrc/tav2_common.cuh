@@ -268,7 +268,7 @@ cudaError_t launch_store_gather(const StoreCopy* d, int n, int max_tok, const in
                                 const uint16_t* sact, const uint8_t* ssurf, int8_t* demb, uint16_t* dact,
                                 uint8_t* dsurf, cudaStream_t s);
 cudaError_t launch_nn_select(const Staged& st, const NNCfg& nn, const NNScan& sc, int32_t* idx,
-                             float* scores, SelFlags sel, cudaStream_t s);
+                             double* scores, SelFlags sel, cudaStream_t s);
 cudaError_t set_debug_timeline(long long* dev, int block);
 cudaError_t set_debug_skut(long long* dev);
 cudaError_t set_debug_skut3(long long* dev);
@@ -287,6 +287,9 @@ cudaError_t launch_skut_tc(const Params& p, const SkutImages& img, const NNCfg& 
                            const Staged* st, const int32_t* idx, const float* F,
                            const uint8_t* fmask, int n, float* U, float* logits, float* pooled,
                            cudaStream_t s);
+cudaError_t launch_similarity(const Staged& st, int item, int source, int n, double* out, cudaStream_t s);
+cudaError_t launch_pool(const float* U, const uint8_t* mask, const float* out_linear, int n, int S, float* pooled,
+                        cudaStream_t s);
 int skut_simt_grid(int n);
 size_t skut_simt_scratch_floats(int seq_len);
 }  // namespace tav2

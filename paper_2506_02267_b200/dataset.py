@@ -13,7 +13,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .core import CLICK, CLOSEUP, EMBED_DIM, HIDE, IMPRESSION, REPIN, TokenBlock, UserSequences, quantize
+from .core import (CLICK, CLOSEUP, EMBED_DIM, HIDE, IMPRESSION, REPIN, TokenBlock, UserSequences,
+                   ValidationError, quantize)
 
 HEAD_NAMES = ("repin", "click", "closeup", "hide")
 NUM_HEADS = len(HEAD_NAMES)
@@ -90,6 +91,153 @@ def generate_requests(num_requests: int, n_candidates: int, ll_tokens: int = 163
         is_near = rng.random(n_candidates) < 0.5
         cands = np.where(is_near[:, None], near(n_candidates), far(n_candidates)).astype(np.float32)
         out.append(SyntheticRequest(uid, user, np.ascontiguousarray(cands), context_features(uid)))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# The reference generator itself (dataset.py:297-427), draw for draw: the
+# same Generator calls in the same order, so a seed gives bit-identical
+# users and candidates (pinned against the live reference by
+# oracle/gen_c2_golden.py -> tests/golden/c2_seed0.npz).  It is a per-token
+# Python loop like the reference (~1 s per 16k-token user); the benchmark and
+# the shape tests use it so their inputs are the reference's.
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class SyntheticConfig:
+    """dataset.py:296-321."""
+
+    num_users: int = 100
+    num_clusters: int = 8
+    ll_tokens: int = 128
+    rt_tokens: int = 48
+    imp_tokens: int = 48
+    positive_rate: float = 0.9
+    hide_rate: float = 0.9
+    chunks_per_user: int = 2
+    chunk_size: int = 8
+    seed: int = 0
+
+    def validate(self) -> None:
+        if min(self.num_users, self.num_clusters, self.ll_tokens, self.rt_tokens, self.imp_tokens,
+               self.chunks_per_user, self.chunk_size) < 1:
+            raise ValidationError("all synthetic counts must be >= 1")
+        if not (0.0 <= self.positive_rate <= 1.0 and 0.0 <= self.hide_rate <= 1.0):
+            raise ValidationError("rates must lie in [0, 1]")
+
+
+@dataclass
+class TrainingExample:
+    """One labelled (user, candidate) pair (dataset.py:179-203)."""
+
+    user_id: int
+    chunk_id: int
+    candidate: np.ndarray
+    labels: np.ndarray
+    nn_features: object = None
+
+
+@dataclass
+class SyntheticData:
+    users: list
+    examples: list
+    centroids: np.ndarray
+
+
+def _unit_vec(e: np.ndarray) -> np.ndarray:
+    """The reference's per-vector l2_normalize (core.py:60-66): f32 dot,
+    float sqrt, one f32 division (bit-for-bit, unlike the row-wise form)."""
+    e = np.asarray(e, dtype=np.float32)
+    nrm = float(np.sqrt(np.dot(e, e)))
+    return e.copy() if nrm == 0.0 else e / np.float32(nrm)
+
+
+def generate_synthetic(cfg: SyntheticConfig) -> SyntheticData:
+    """Users with 1-3 interest clusters, engagement / impression blocks and
+    labelled candidate chunks, drawn exactly as dataset.py:335-427 does."""
+    cfg.validate()
+    rng = np.random.default_rng(cfg.seed)
+    normal, random, choice, integers = rng.normal, rng.random, rng.choice, rng.integers
+    centroids = normal(0.0, 1.0, (cfg.num_clusters, EMBED_DIM)).astype(np.float32)
+    centroids = np.stack([_unit_vec(c) for c in centroids])
+    pos3 = (REPIN, CLICK, CLOSEUP)
+    pos2 = (REPIN, CLOSEUP)
+    users, examples, chunk_id = [], [], 0
+    for uid in range(1, cfg.num_users + 1):
+        k = int(integers(1, min(3, cfg.num_clusters) + 1))
+        interests = choice(cfg.num_clusters, k, replace=False)
+        foreign = np.setdiff1d(np.arange(cfg.num_clusters), interests)
+
+        def near(_i=interests):
+            c = centroids[int(choice(_i))]
+            return _unit_vec(c + normal(0.0, 0.08, EMBED_DIM).astype(np.float32))
+
+        def far(_f=foreign):
+            if len(_f) == 0:
+                return _unit_vec(normal(0.0, 1.0, EMBED_DIM).astype(np.float32))
+            c = centroids[int(choice(_f))]
+            return _unit_vec(c + normal(0.0, 0.08, EMBED_DIM).astype(np.float32))
+
+        def engagement(n, base_ts, step):
+            ts = base_ts - np.arange(n, dtype=np.int64) * step
+            act = np.zeros(n, np.uint16)
+            surf = integers(0, 4, n).astype(np.uint8)
+            emb = np.zeros((n, EMBED_DIM), np.int8)
+            for i in range(n):
+                if random() < 0.15:
+                    act[i] = HIDE
+                    emb[i] = quantize(far())
+                else:
+                    a = int(choice(pos3))
+                    if random() < 0.1:  # multi-hot pair
+                        a |= int(choice(pos2))
+                    act[i] = a
+                    emb[i] = quantize(near())
+            return TokenBlock(ts, act, surf, emb)
+
+        def impressions(n):
+            ts = _RT_BASE_TS + 30 - np.arange(n, dtype=np.int64) * 60
+            surf = integers(0, 4, n).astype(np.uint8)
+            emb = np.zeros((n, EMBED_DIM), np.int8)
+            for i in range(n):
+                emb[i] = quantize(far() if random() < 0.75 else near())
+            return TokenBlock(ts, np.full(n, IMPRESSION, np.uint16), surf, emb)
+
+        seqs = UserSequences(engagement(cfg.ll_tokens, _LL_BASE_TS, 3600),
+                             engagement(cfg.rt_tokens, _RT_BASE_TS, 60), impressions(cfg.imp_tokens))
+        seqs.validate()
+        users.append((uid, seqs))
+        for _ in range(cfg.chunks_per_user):
+            chunk_id += 1
+            for _ in range(cfg.chunk_size):
+                labels = np.zeros(NUM_HEADS, np.uint8)
+                if random() < 0.5:
+                    emb = near()
+                    labels[0] = random() < cfg.positive_rate
+                    labels[1] = random() < cfg.positive_rate * 0.7
+                    labels[2] = random() < cfg.positive_rate * 0.5
+                else:
+                    emb = far()
+                    labels[3] = random() < cfg.hide_rate
+                examples.append(TrainingExample(uid, chunk_id, emb, labels))
+    return SyntheticData(users, examples, centroids)
+
+
+def synthetic_requests(num_requests: int, n_candidates: int, ll_tokens: int = 16384,
+                       rt_tokens: int = 256, imp_tokens: int = 256, seed: int = 0) -> list[SyntheticRequest]:
+    """Serving requests from the reference generator: request
+    i is ``generate_synthetic(num_users=1, num_clusters=8, L, 256, 256,
+    chunks_per_user=1, chunk_size=N, seed=seed + i)``'s user and its N
+    candidate embeddings; ctx = context_features(user id)."""
+    out = []
+    for i in range(num_requests):
+        d = generate_synthetic(SyntheticConfig(num_users=1, num_clusters=8, ll_tokens=ll_tokens,
+                                               rt_tokens=rt_tokens, imp_tokens=imp_tokens, chunks_per_user=1,
+                                               chunk_size=n_candidates, seed=seed + i))
+        uid, user = d.users[0]
+        cands = np.ascontiguousarray(np.stack([e.candidate for e in d.examples]), np.float32)
+        out.append(SyntheticRequest(uid, user, cands, context_features(uid)))
     return out
 
 

@@ -9,6 +9,8 @@ compute runs in ``libtav2.so``; there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import functools
+import threading
 import time
 from dataclasses import dataclass
 
@@ -55,6 +57,18 @@ def _columns(user: UserSequences, r, keep) -> None:
         r.len[s] = len(blk)
 
 
+def _locked(fn):
+    """Serialise a method on the engine's lock: one native context is never
+    driven by two threads at once (arena.py:17), whoever calls it."""
+
+    @functools.wraps(fn)
+    def wrapper(self, *a, **kw):
+        with self._lock:
+            return fn(self, *a, **kw)
+
+    return wrapper
+
+
 class _Pack:
     """Keeps the numpy columns of a request list alive across a native call.
     A request's user is a UserSequences (host columns) or a StoreUser."""
@@ -77,7 +91,15 @@ class _Pack:
 
 
 class Engine:
-    """One native worker context (never share across threads, arena.py:17)."""
+    """One native worker context (arena.py:16-55): a pinned staging arena and
+    a device workspace sized once from ``capacity``.  Every native call runs
+    under the engine's lock, so a shared engine serialises its callers
+    (give each worker thread its own engine for parallelism).
+
+    Capacity overflow follows the reference arena (arena.py:40-44): a batch
+    that does not fit is split into fitting sub-batches, and a single request
+    larger than the whole capacity runs on a fallback context sized for it;
+    both count in ``overflow_count`` instead of failing the batch."""
 
     def __init__(self, model: RankingModel | None = None, config: ModelConfig | None = None,
                  capacity: Capacity = Capacity(), device: int = 0):
@@ -95,6 +117,11 @@ class Engine:
                                       device, ctypes.byref(self._ctx)))
         self.model = None
         self.n_items = 0
+        self.overflow_count = 0
+        self._perm = None          # staged item order -> batch item order (DedupBatch)
+        self._store_tokens = {}    # user id -> resident token count (capacity planning)
+        self._fallback = None      # context for requests larger than `capacity`
+        self._lock = threading.RLock()
         if model is not None:
             self.load_model(model)
 
@@ -109,6 +136,9 @@ class Engine:
         return self.config.nn
 
     def close(self) -> None:
+        if getattr(self, "_fallback", None) is not None:
+            self._fallback.close()
+            self._fallback = None
         if getattr(self, "_ctx", None) and self._ctx.value:
             self._lib.tav2_destroy(self._ctx)
             self._ctx = ctypes.c_void_p()
@@ -126,6 +156,7 @@ class Engine:
         self.close()
 
     # ------------------------------------------------------------------
+    @_locked
     def load_model(self, model: RankingModel) -> None:
         """RankingModel.load equivalent: upload the named tensors once."""
         if model.config != self.config:
@@ -143,22 +174,80 @@ class Engine:
     # ------------------------------------------------------------------
     # HBM-resident feature store (tav2_store_*; serving.DeviceFeatureStore
     # is the FeatureStore-shaped front end)
+    @_locked
     def store_reserve(self, max_users: int) -> None:
         """(Re)allocate the device pool for max_users users (drops all)."""
         N.check(self._lib.tav2_store_reserve(self._ctx, int(max_users)))
+        self._store_tokens.clear()
 
+    @_locked
     def store_put(self, user_id: int, user: UserSequences) -> None:
         """Insert or replace a user's sequences in HBM (lengths within the caps)."""
         r, keep = N.Request(), []
         _columns(user, r, keep)
         N.check(self._lib.tav2_store_put(self._ctx, int(user_id), ctypes.byref(r)))
+        self._store_tokens[int(user_id)] = user.total_tokens()
 
+    @_locked
     def store_remove(self, user_id: int) -> None:
         N.check(self._lib.tav2_store_remove(self._ctx, int(user_id)))
+        self._store_tokens.pop(int(user_id), None)
 
     def store_count(self) -> int:
         return int(self._lib.tav2_store_count(self._ctx))
 
+    # ------------------------------------------------------------------
+    # capacity planning (the arena contract, arena.py:32-47)
+    def _size(self, req) -> tuple[int, int]:
+        user, cands, _ = req
+        if isinstance(user, StoreUser):
+            toks = self._store_tokens.get(int(user.user_id), 0)
+        else:
+            toks = user.total_tokens()
+        return len(cands), toks
+
+    def _fits(self, n_req, items, toks) -> bool:
+        c = self.capacity
+        return n_req <= c.max_requests and items <= c.max_items and toks <= c.max_tokens
+
+    def _chunks(self, requests):
+        """Greedy split into sub-batches that fit the capacity, in order;
+        yields (chunk, oversized) with oversized=True for a single request
+        larger than the whole capacity."""
+        cur, items, toks = [], 0, 0
+        for req in requests:
+            i, t = self._size(req)
+            if not self._fits(1, i, t):
+                if cur:
+                    yield cur, False
+                    cur, items, toks = [], 0, 0
+                yield [req], True
+                continue
+            if cur and not self._fits(len(cur) + 1, items + i, toks + t):
+                yield cur, False
+                cur, items, toks = [], 0, 0
+            cur.append(req)
+            items += i
+            toks += t
+        if cur:
+            yield cur, False
+
+    def _fallback_engine(self, req) -> "Engine":
+        """The counted fallback allocation (arena.py:40-44): a context sized
+        for one request that exceeds ``capacity``; kept for reuse."""
+        i, t = self._size(req)
+        if isinstance(req[0], StoreUser):
+            raise ValidationError("a stored user's request exceeds the engine capacity")
+        fb = self._fallback
+        if fb is None or not fb._fits(1, i, t):
+            if fb is not None:
+                fb.close()
+            cap = Capacity(1, max(i, self.capacity.max_items), max(t, self.capacity.max_tokens, 1))
+            fb = Engine(self.model, config=self.config, capacity=cap, device=self.device)
+            self._fallback = fb
+        return fb
+
+    @_locked
     def stage(self, requests) -> int:
         """requests: list of (UserSequences | StoreUser, candidates[M,32], ctx[8] | None)."""
         pack = _Pack(requests)
@@ -166,15 +255,30 @@ class Engine:
         N.check(self._lib.tav2_stage(self._ctx, pack.arr, len(requests), self.stream(),
                                      ctypes.byref(n)))
         self.n_items = n.value
+        self._perm = None
         return n.value
 
+    @_locked
     def stage_batch(self, batch: DedupBatch, contexts=None) -> int:
+        """Stage a DedupBatch (items grouped by request on the device; see
+        ``DedupBatch.grouped_order``)."""
         batch.validate()
+        perm = batch.grouped_order()
+        cands = batch.candidates[perm]
         reqs = []
         for r, sl in enumerate(batch.request_slices()):
             ctx = None if contexts is None else contexts[r]
-            reqs.append((batch.users[r], batch.candidates[sl], ctx))
-        return self.stage(reqs)
+            reqs.append((batch.users[r], cands[sl], ctx))
+        n = self.stage(reqs)
+        self._perm = None if np.array_equal(perm, np.arange(len(perm))) else perm
+        return n
+
+    def _unpermute(self, a: np.ndarray) -> np.ndarray:
+        if self._perm is None:
+            return a
+        out = np.empty_like(a)
+        out[self._perm] = a
+        return out
 
     def _mode(self, mode: str) -> int:
         try:
@@ -183,21 +287,39 @@ class Engine:
             raise ValidationError(f"unknown precision mode {mode!r} (fp32 | bf16)") from None
 
     # ------------------------------------------------------------------
+    @_locked
     def nn_select(self, batch: DedupBatch, mode: str = "bf16", return_scores: bool = False):
-        """Device NN selection over a DedupBatch -> idx [N, S] int32 (-1 pad)."""
+        """Device NN selection over a DedupBatch -> idx [N, S] int32 (-1 pad)
+        in batch item order (and the f64 score of every NN slot)."""
+        toks = sum(u.total_tokens() for u in batch.users)
+        if not self._fits(len(batch.users), len(batch), toks):
+            raise ValidationError("batch exceeds the engine capacity (use fused_assemble without an "
+                                  "engine, or a larger Capacity)")
         n = self.stage_batch(batch)
         S = self.config.nn.seq_len
         idx = torch.empty((n, S), dtype=torch.int32, device=self.torch_device)
-        sc = torch.empty((n, S), dtype=torch.float32, device=self.torch_device) if return_scores else None
+        sc = torch.empty((n, S), dtype=torch.float64, device=self.torch_device) if return_scores else None
         N.check(self._lib.tav2_nn_select(self._ctx, self._mode(mode), N.ptr(idx), N.ptr(sc),
                                          self.stream()))
-        idx_h = idx.cpu().numpy()
+        idx_h = self._unpermute(idx.cpu().numpy())
         if return_scores:
-            return idx_h, sc.cpu().numpy()
+            return idx_h, self._unpermute(sc.cpu().numpy())
         return idx_h
 
-    def encode(self, seqs: list[AssembledSequence], candidates: np.ndarray):
-        """encode_batch (encoder.py:161-188) on the GPU -> (F [B,S,64], mask [B,S])."""
+    @_locked
+    def similarity(self, user: UserSequences, candidates: np.ndarray, source: int = 0, item: int = 0):
+        """similarity_scores of every token of one source (0 LL, 1 RT, 2 IMP)
+        against candidate `item` (tav2_similarity) -> f64 [len(source)]."""
+        n = len(user.blocks()[source])
+        self.stage([(user, candidates, None)])
+        out = torch.empty((max(n, 1),), dtype=torch.float64, device=self.torch_device)
+        N.check(self._lib.tav2_similarity(self._ctx, int(item), int(source), N.ptr(out), self.stream()))
+        return out.cpu().numpy()[:n]
+
+    def _stage_assembled(self, seqs: list[AssembledSequence], candidates: np.ndarray, contexts=None):
+        """Stage already-assembled sequences: each becomes a one-item request
+        whose sources hold exactly its valid tokens, with the index layout
+        that gathers them back in place -> device idx [B, S]."""
         if self.model is None:
             raise ValidationError("no model loaded")
         cfg = self.config.nn
@@ -206,8 +328,6 @@ class Engine:
             raise ValidationError("assembled length must match the positional table")
         starts, lens = cfg.segment_starts(), cfg.segment_lengths()
         reqs, idx = [], np.full((len(seqs), S), -1, np.int32)
-        from .core import TokenBlock
-
         for i, s in enumerate(seqs):
             parts = []
             for g in range(4):
@@ -219,14 +339,48 @@ class Engine:
             idx[i, parts[2]] = len(parts[1]) + np.arange(len(parts[2]))
             idx[i, parts[3]] = np.arange(len(imp))
             user = UserSequences(s.block.take(ll), s.block.take(rt), s.block.take(imp))
-            reqs.append((user, np.asarray(candidates[i:i + 1], np.float32), None))
-        n = self.stage(reqs)
-        idx_d = torch.from_numpy(idx).to(self.torch_device)
+            ctx = None if contexts is None else contexts[i]
+            reqs.append((user, np.asarray(candidates[i:i + 1], np.float32), ctx))
+        if not self._fits(len(reqs), len(reqs), sum(u.total_tokens() for u, _, _ in reqs)):
+            raise ValidationError("batch exceeds the engine capacity")
+        self.stage(reqs)
+        return torch.from_numpy(idx).to(self.torch_device)
+
+    @_locked
+    def encode(self, seqs: list[AssembledSequence], candidates: np.ndarray):
+        """encode_batch (encoder.py:161-188) on the GPU -> (F [B,S,64], mask [B,S])."""
+        idx_d = self._stage_assembled(seqs, candidates)
+        n, S = idx_d.shape
         F = torch.empty((n, S, 2 * EMBED_DIM), dtype=torch.float32, device=self.torch_device)
         m = torch.empty((n, S), dtype=torch.uint8, device=self.torch_device)
         N.check(self._lib.tav2_encode(self._ctx, N.ptr(idx_d), N.ptr(F), N.ptr(m), self.stream()))
         return F.cpu().numpy(), m.cpu().numpy().astype(bool)
 
+    @_locked
+    def score_assembled(self, seqs: list[AssembledSequence], candidates: np.ndarray, contexts,
+                        mode: str = "fp32"):
+        """The fused gather + encode + SKUT + pool + head (tav2_score) over
+        assembled sequences -> (logits [B, 4], pooled [B, 64])."""
+        idx_d = self._stage_assembled(seqs, candidates, contexts)
+        logits, pooled = self.score_staged(idx_d, mode=mode, pooled=True)
+        return logits.cpu().numpy(), pooled.cpu().numpy()
+
+    @_locked
+    def pool(self, u: np.ndarray, mask: np.ndarray) -> np.ndarray:
+        """pool (encoder.py:265-273) over encoder outputs U [B, S, 64] -> [B, 64]."""
+        if self.model is None:
+            raise ValidationError("no model loaded")
+        u = np.asarray(u, np.float32)
+        B, S, d = u.shape
+        if S != self.config.nn.seq_len or d != 2 * EMBED_DIM:
+            raise ValidationError("encoder output shape does not match the model")
+        U = torch.from_numpy(np.ascontiguousarray(u)).to(self.torch_device)
+        m = torch.from_numpy(np.ascontiguousarray(mask, np.uint8)).to(self.torch_device)
+        out = torch.empty((B, d), dtype=torch.float32, device=self.torch_device)
+        N.check(self._lib.tav2_pool(self._ctx, N.ptr(U), N.ptr(m), B, N.ptr(out), self.stream()))
+        return out.cpu().numpy()
+
+    @_locked
     def forward(self, features: np.ndarray, mask: np.ndarray, mode: str = "fp32") -> np.ndarray:
         """forward_fused over caller features (B, S, 64) -> U (valid rows)."""
         if self.model is None:
@@ -241,10 +395,27 @@ class Engine:
                                        self.stream()))
         return U.cpu().numpy()
 
+    @_locked
     def rank_requests(self, requests, mode: str = "bf16", return_indices: bool = False):
-        """Host-to-host rank over (user, candidates, ctx) requests -> logits [N, 4]."""
+        """Host-to-host rank over (user, candidates, ctx) requests -> logits [N, 4]
+        (request order kept).  A batch beyond the capacity is split / run on
+        the fallback context and counted in ``overflow_count``."""
         if self.model is None:
             raise ValidationError("no model loaded")
+        requests = list(requests)
+        chunks = list(self._chunks(requests))
+        if len(chunks) > 1 or (chunks and chunks[0][1]):
+            self.overflow_count += 1
+            outs = []
+            for chunk, big in chunks:
+                eng = self._fallback_engine(chunk[0]) if big else self
+                outs.append(eng._rank_native(chunk, mode, return_indices))
+            if return_indices:
+                return (np.concatenate([o[0] for o in outs]), np.concatenate([o[1] for o in outs]))
+            return np.concatenate(outs)
+        return self._rank_native(requests, mode, return_indices)
+
+    def _rank_native(self, requests, mode, return_indices):
         pack = _Pack(requests)
         n = sum(len(c) for _, c, _ in requests)
         logits = np.empty((n, 4), np.float32)
@@ -253,6 +424,7 @@ class Engine:
                                     logits.ctypes.data, N.ptr(idx), self.stream()))
         return (logits, idx) if return_indices else logits
 
+    @_locked
     def rank_pipelined(self, batches, mode: str = "bf16", return_indices: bool = False,
                        latencies: list | None = None):
         """Serving loop (tav2_rank_submit / tav2_rank_collect): every batch of
@@ -279,6 +451,16 @@ class Engine:
 
         for reqs in batches:
             t0 = time.perf_counter()
+            reqs = list(reqs)
+            ch = list(self._chunks(reqs))
+            if len(ch) > 1 or (ch and ch[0][1]):  # overflow: drain, then the counted slow path
+                if pending is not None:
+                    collect(pending)
+                    pending = None
+                out.append(self.rank_requests(reqs, mode=mode, return_indices=return_indices))
+                if latencies is not None:
+                    latencies.append(time.perf_counter() - t0)
+                continue
             pack = _Pack(reqs)
             n = sum(len(c) for _, c, _ in reqs)
             slot = ctypes.c_int32()
@@ -291,10 +473,12 @@ class Engine:
             collect(pending)
         return out
 
+    @_locked
     def run_staged(self, mode: str, logits: torch.Tensor | None = None) -> None:
         """Device-resident path (bench ``value``): NN + score on the staged batch."""
         N.check(self._lib.tav2_run_staged(self._ctx, self._mode(mode), N.ptr(logits), self.stream()))
 
+    @_locked
     def score_staged(self, idx: torch.Tensor, mode: str = "bf16", pooled: bool = False):
         logits = torch.empty((self.n_items, 4), dtype=torch.float32, device=self.torch_device)
         pl = torch.empty((self.n_items, 64), dtype=torch.float32, device=self.torch_device) if pooled else None
@@ -316,3 +500,35 @@ class Engine:
         cnt = (ctypes.c_int32 * n)()
         k = self._lib.tav2_kernel_times(self._ctx, names, ms, cnt, n)
         return {names[i].decode(): (ms[i], cnt[i]) for i in range(min(k, n))}
+
+
+# ---------------------------------------------------------------------------
+# Implicit per-thread engines for the module-level functions the reference
+# calls without an engine (fused_assemble(arena=None), similarity_scores,
+# top_k_nn, assemble, encode_batch / forward_fused / pool(params)).  One
+# engine per (thread, NNConfig, parameter object), created on first use and
+# grown when a call needs more capacity -- never per call.
+# ---------------------------------------------------------------------------
+
+_TLS = threading.local()
+
+
+def implicit_engine(nn: NNConfig, requests: int = 1, items: int = 1, tokens: int = 1,
+                    model: RankingModel | None = None) -> Engine:
+    cache = getattr(_TLS, "engines", None)
+    if cache is None:
+        cache = _TLS.engines = {}
+    key = (nn, id(model) if model is not None else None)
+    eng, ref = cache.get(key, (None, None))
+    if eng is not None and model is not None and ref is not model:
+        eng = None  # the id was recycled by another object
+    if eng is None or not eng._fits(requests, items, tokens):
+        old = eng.capacity if eng is not None else Capacity(1, 1, 1)
+        cap = Capacity(max(requests, old.max_requests), max(items, old.max_items, 64),
+                       max(tokens, old.max_tokens, 16896))
+        if eng is not None:
+            eng.close()
+        cfg = model.config if model is not None else ModelConfig.for_nn(nn)
+        eng = Engine(model, config=cfg, capacity=cap, device=torch.cuda.current_device())
+        cache[key] = (eng, model)
+    return eng

@@ -38,3 +38,36 @@ def check_nn_contract(idx_gpu, idx_ref, ref_scores_fn, kth, seg_starts, seg_lens
                     f"item {i} seg {g}: set differs beyond ties: {diff} {s} kth={kth[i, g]}")
                 swaps += len(diff) // 2
     return swaps
+
+
+def oracle_layout(user, cands, cfg):
+    """The oracle's selection of one request in the device index layout:
+    idx [m, S] (source-relative, RT tail offset by r, -1 padding) and the
+    k-th best score of every NN segment kth [m, 4] (NaN where empty)."""
+    from oracle import seqrank_oracle as orc
+
+    segs, scores = orc.nn_select_request(user["ll_emb"], user["rt_emb"], user["imp_emb"], cands, cfg,
+                                         return_scores=True)
+    r, k_ll, k_rt, k_imp = cfg
+    lens = (k_ll, r, k_rt, k_imp)
+    starts = np.cumsum((0,) + lens[:-1])
+    idx = np.full((len(cands), sum(lens)), -1, np.int32)
+    kth = np.full((len(cands), 4), np.nan)
+    names = ("nn_lifelong", "recent_realtime", "nn_realtime_tail", "nn_impression")
+    for i, (sg, sc) in enumerate(zip(segs, scores)):
+        for g in range(4):
+            idx[i, starts[g]:starts[g] + len(sg[g])] = sg[g]
+            if names[g] in sc and len(sc[names[g]]):
+                kth[i, g] = sc[names[g]][-1]
+    return idx, kth
+
+
+def ref_scores_fn(user_of_item, cands):
+    """Reference f64 scores of given source-relative tokens (tie windows)."""
+    from oracle import seqrank_oracle as orc
+
+    def fn(i, g, idx):
+        u = user_of_item(i)
+        src = {0: "ll", 2: "rt", 3: "imp"}[g]
+        return orc.similarity_scores(u[f"{src}_emb"], cands[i])[idx]
+    return fn
