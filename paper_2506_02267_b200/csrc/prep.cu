@@ -25,24 +25,34 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
 // candidate  l2_normalize_rows (nnsearch.py:313-320).
 // ---------------------------------------------------------------------------
 // Sum of squares of a 32-vector held by a quad of threads (thread g holds
-// elements 8g..8g+7): 8 interleaved accumulators a[l] = ((v_l^2 + v_{l+8}^2)
-// + v_{l+16}^2) + v_{l+24}^2, adjacent-pair combine -- a fixed order (the
-// reference's einsum order is BLAS-internal; differences are <= 1 ulp).
-// Every thread of the quad returns the same value.
+// elements 8g..8g+7) in numpy's exact einsum("ij,ij->i", dtype=f32) order
+// (core.py:72, nnsearch.py:282 / :317), probed bit for bit on this image's
+// numpy (tools/einsum_order.py): four 4-lane accumulators, lane l summing
+// x[l + 4m]^2 in the unrolled-by-4 reverse order m = 3,2,1,0 then 7,6,5,4
+// (separately rounded products and additions), then (l0 + l1) + (l2 + l3).
+// Every thread of the quad gathers all 32 squares and returns the same value.
 __device__ __forceinline__ float quad_sumsq(const float* v, unsigned qm) {
-  float a[8];
+  float s[32];
 #pragma unroll
-  for (int l = 0; l < 8; ++l) {
-    const float sq = __fmul_rn(v[l], v[l]);
-    const float s0 = __shfl_sync(qm, sq, 0, 4);
-    const float s1 = __shfl_sync(qm, sq, 1, 4);
-    const float s2 = __shfl_sync(qm, sq, 2, 4);
-    const float s3 = __shfl_sync(qm, sq, 3, 4);
-    a[l] = __fadd_rn(__fadd_rn(__fadd_rn(s0, s1), s2), s3);
+  for (int i = 0; i < 8; ++i) {
+    const float sq = __fmul_rn(v[i], v[i]);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) s[8 * t + i] = __shfl_sync(qm, sq, t, 4);
   }
-  const float b0 = __fadd_rn(a[0], a[1]), b1 = __fadd_rn(a[2], a[3]);
-  const float b2 = __fadd_rn(a[4], a[5]), b3 = __fadd_rn(a[6], a[7]);
-  return __fadd_rn(__fadd_rn(b0, b1), __fadd_rn(b2, b3));
+  float lane[4];
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    float a = s[12 + l];
+    a = __fadd_rn(s[8 + l], a);
+    a = __fadd_rn(s[4 + l], a);
+    a = __fadd_rn(s[l], a);
+    a = __fadd_rn(s[28 + l], a);
+    a = __fadd_rn(s[24 + l], a);
+    a = __fadd_rn(s[20 + l], a);
+    a = __fadd_rn(s[16 + l], a);
+    lane[l] = a;
+  }
+  return __fadd_rn(__fadd_rn(lane[0], lane[1]), __fadd_rn(lane[2], lane[3]));
 }
 
 // One quad of threads per token row (then per candidate row); thread g owns

@@ -8,7 +8,7 @@ import pytest
 
 import paper_2506_02267_b200 as P
 from paper_2506_02267_b200 import checkpoint, nnsearch, serving
-from conftest import golden_cases, load_case
+from conftest import REPO, golden_cases, load_case
 from helpers import to_user
 from oracle import seqrank_oracle as orc
 
@@ -98,3 +98,18 @@ def test_synthetic_requests_are_valid():
         assert r.candidates.shape == (50, 32)
         np.testing.assert_allclose(np.linalg.norm(r.candidates, axis=1), 1, atol=1e-5)
         np.testing.assert_array_equal(r.ctx, P.context_features(r.user_id))
+
+
+def test_einsum_row_norm_order_restated():
+    """prep_kernel's quad_sumsq reproduces numpy's f32 einsum row norm order
+    bit for bit (the reference's unit vectors, core.py:72, nnsearch.py:282)."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("einsum_order", os.path.join(REPO, "tools", "einsum_order.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    q = np.random.default_rng(5).integers(-127, 128, (20000, 32)).astype(np.int8)
+    x = (q.astype(np.float32) / np.float32(127)) * np.float32(0.65)
+    assert np.array_equal(mod.restated(x), np.einsum("ij,ij->i", x, x, dtype=np.float32))
+    c = np.random.default_rng(6).normal(size=(20000, 32)).astype(np.float32)
+    assert np.array_equal(mod.restated(c), np.einsum("ij,ij->i", c, c, dtype=np.float32))
