@@ -18,8 +18,10 @@ ranks / the max-over-ranks device time.
 around each step on the launch stream, L2 flushed between timed steps.
 ``e2e``: the public API ``Engine.rank_requests`` from host numpy buffers,
 host->device and device->host copies inside the timed region.
-``--impl reference`` times the CPU oracle port of the reference path on all
-host cores (rank 0 only) and prints the same metric.
+``--impl reference`` times the reference's own numpy path (seqrank 0.1.0
+installed in baseline/_ref; the oracle port when absent) on all host cores,
+every process scoring whole 1,000-candidate requests (rank 0 only), and
+prints the same metric with per-request p50/p99.
 """
 
 from __future__ import annotations
@@ -124,47 +126,92 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
-# CPU reference arm (oracle port of the reference path), one process per core
+# CPU reference arm: the reference's own numpy path (seqrank 0.1.0 installed
+# in baseline/_ref, kind "reference") or the oracle port (kind "port"), one
+# process per host core, each scoring WHOLE requests of the workload
 # ---------------------------------------------------------------------------
 
+REF_DIR = os.path.join(REPO, "baseline", "_ref")
 _CPU_STATE = {}
 
 
-def _cpu_init(seed, n_cand, L, nn):
+def reference_available() -> bool:
+    return os.path.isdir(os.path.join(REF_DIR, "seqrank"))
+
+
+def _cpu_init(kind, seed, n_cand, L, nn):
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    import paper_2506_02267_b200 as P
-    from oracle import seqrank_oracle as orc
-    r = P.generate_requests(1, n_cand, ll_tokens=L, seed=seed)[0]
-    user = {f"{s}_{c}": getattr(b, a) for s, b in zip(("ll", "rt", "imp"), r.user.blocks())
-            for c, a in (("emb", "embeddings"), ("action", "actions"), ("surface", "surfaces"),
-                         ("ts", "timestamps"))}
-    _CPU_STATE.update(orc=orc, user=user, cands=r.candidates, ctx=r.ctx, nn=nn,
-                      P=orc.model_init(0, seq_len=sum(nn)))
+    if kind == "reference":
+        sys.path.insert(0, REF_DIR)
+        from seqrank import core as rcore
+        from seqrank import dataset as rdata
+        from seqrank import encoder as renc
+        from seqrank import nnsearch as rnn
+        from seqrank import trainer as rtr
+
+        d = rdata.generate_synthetic(rdata.SyntheticConfig(
+            num_users=1, num_clusters=8, ll_tokens=L, rt_tokens=256, imp_tokens=256, chunks_per_user=1,
+            chunk_size=n_cand, seed=seed))
+        uid, user = d.users[0]
+        cands = np.stack([e.candidate for e in d.examples]).astype(np.float32)
+        cfg = rnn.NNConfig(*nn)
+        model = rtr.RankingModel.init(rtr.ModelConfig(encoder=renc.EncoderConfig(seq_len=cfg.seq_len), nn=cfg),
+                                      seed=0)
+        ctx = np.repeat(rdata.context_features(uid)[None], n_cand, 0)
+
+        def run():
+            """The reference serving composition: build_dedup_batch
+            -> fused_assemble -> encode_batch -> forward_fused -> pool + head
+            (trainer.py:354-366), all through the reference's public API."""
+            batch = rnn.build_dedup_batch([(user, cands, None)])
+            seqs = rnn.fused_assemble(batch, cfg)
+            F, mask = renc.encode_batch(seqs, batch.candidates, model.encoder)
+            U = renc.forward_fused(F, mask, model.encoder)
+            y = U @ model.encoder.out_linear
+            ym = np.where(mask[:, :, None], y, np.array(-np.inf, y.dtype))
+            pooled = ym.max(1)
+            pooled[~mask.any(1)] = 0
+            z = np.concatenate([pooled, rcore.l2_normalize_rows(batch.candidates), ctx], axis=1)
+            h = np.maximum(z @ model.head.w1 + model.head.b1, 0)
+            return h @ model.head.w2 + model.head.b2
+    else:
+        import paper_2506_02267_b200 as P
+        from oracle import seqrank_oracle as orc
+
+        r = P.synthetic_requests(1, n_cand, L, 256, 256, seed=seed)[0]
+        user = {f"{s}_{c}": getattr(b, a) for s, b in zip(("ll", "rt", "imp"), r.user.blocks())
+                for c, a in (("emb", "embeddings"), ("action", "actions"), ("surface", "surfaces"),
+                             ("ts", "timestamps"))}
+        Pd = orc.model_init(0, seq_len=sum(nn))
+
+        def run():
+            return orc.rank_request(user, r.candidates, r.ctx, Pd, nn)
+    _CPU_STATE.update(run=run, n=n_cand)
 
 
 def _cpu_step(_):
-    """One bounded sample: the oracle port of the reference path over this
-    process's candidate slice of a full-length request."""
-    st = _CPU_STATE
+    """One whole request of the workload through the CPU reference path."""
     t = time.perf_counter()
-    st["orc"].rank_request(st["user"], st["cands"], st["ctx"], st["P"], st["nn"])
-    return len(st["cands"]), time.perf_counter() - t
+    _CPU_STATE["run"]()
+    return _CPU_STATE["n"], time.perf_counter() - t
 
 
-def cpu_baseline(cfg_name, steps=3, warmup=1, budget_s=60.0, procs=None, n_per_proc=250):
-    """Reference CPU path (oracle port; the Python reference cannot travel to
-    the GPU box) in one process per host core, OPENBLAS_NUM_THREADS=1.  A step
-    = every process scores `n_per_proc` candidates of a full-length request
-    once; timed steps stop early when `budget_s` is spent (reported)."""
+def cpu_baseline(cfg_name, steps=3, warmup=1, budget_s=60.0, procs=None, kind=None):
+    """The reference's CPU path in one process per host core
+    (OPENBLAS_NUM_THREADS=1); a step = every process scores one whole
+    request of the workload (C2: 1 user x 1,000 candidates, L = 16,384, the
+    reference generator's inputs); timed steps stop early once `budget_s` is
+    spent.  kind: "reference" (the installed reference package) when
+    available, else "port" (oracle/seqrank_oracle.py)."""
     _, n_cand, L, nn = CONFIGS[cfg_name]
+    kind = kind or ("reference" if reference_available() else "port")
     procs = procs or os.cpu_count() or 1
-    n = min(n_cand, n_per_proc)
     ctx = mp.get_context("spawn")
     old = os.environ.get("OPENBLAS_NUM_THREADS")
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     try:
-        with ctx.Pool(procs, initializer=_cpu_init, initargs=(0, n, L, nn)) as pool:
-            for _ in range(max(1, min(warmup, 5))):
+        with ctx.Pool(procs, initializer=_cpu_init, initargs=(kind, 0, n_cand, L, nn)) as pool:
+            for _ in range(max(1, min(warmup, 2))):
                 pool.map(_cpu_step, range(procs))
             done, lats, wall, k = 0, [], 0.0, 0
             while k < max(1, steps) and (k == 0 or wall < budget_s):
@@ -179,14 +226,17 @@ def cpu_baseline(cfg_name, steps=3, warmup=1, budget_s=60.0, procs=None, n_per_p
             os.environ.pop("OPENBLAS_NUM_THREADS", None)
         else:
             os.environ["OPENBLAS_NUM_THREADS"] = old
+    what = ("the reference package seqrank 0.1.0 (baseline/_ref): build_dedup_batch->fused_assemble->"
+            "encode_batch->forward_fused->pool->head" if kind == "reference" else
+            "oracle port of build_dedup_batch->fused_assemble->encode_batch->forward_fused->pool->head")
     return {
-        "value": done / wall, "unit": UNIT, "cores": procs, "kind": "port", "steps_timed": k,
-        "sample": (f"{procs} processes x {k} steps x {n} candidates of one L={L} request "
-                   f"(oracle port of build_dedup_batch->fused_assemble->encode_batch->forward_fused"
-                   f"->pool->head, OPENBLAS_NUM_THREADS=1); {wall:.1f}s timed wall"),
-        "per_process_cand_s": round(n / statistics.median(lats), 1),
-        "p50_sample_ms": round(1e3 * _nearest_rank(lats, 50), 2),
-        "p99_sample_ms": round(1e3 * _nearest_rank(lats, 99), 2),
+        "value": done / wall, "unit": UNIT, "cores": procs, "kind": kind, "steps_timed": k,
+        "sample": (f"{procs} processes x {k} steps x one whole request ({n_cand} candidates, L={L}, "
+                   f"reference generator seed 0) through {what}, OPENBLAS_NUM_THREADS=1; "
+                   f"{wall:.1f}s timed wall"),
+        "per_process_cand_s": round(n_cand / statistics.median(lats), 1),
+        "p50_request_ms": round(1e3 * _nearest_rank(lats, 50), 2),
+        "p99_request_ms": round(1e3 * _nearest_rank(lats, 99), 2),
         "cpu_model": _cpu_model(),
     }
 
@@ -210,6 +260,27 @@ def _cpu_model():
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+
+def _gen_one(args):
+    seed, n_cand, L = args
+    import paper_2506_02267_b200 as P
+
+    return P.synthetic_requests(1, n_cand, L, 256, 256, seed=seed)[0]
+
+
+def _gen_requests(seeds, n_cand, L):
+    """Requests from the reference generator, generated in parallel over the
+    host cores when there are many (the generator is a per-token loop)."""
+    import paper_2506_02267_b200 as P
+
+    uniq = sorted(set(seeds))
+    if len(uniq) <= 2:
+        got = {s: P.synthetic_requests(1, n_cand, L, 256, 256, seed=s)[0] for s in uniq}
+    else:
+        with mp.get_context("spawn").Pool(min(len(uniq), os.cpu_count() or 1)) as pool:
+            got = dict(zip(uniq, pool.map(_gen_one, [(s, n_cand, L) for s in uniq])))
+    return [got[s] for s in seeds]
+
 
 def run_gpu(args, rank, world, local_rank):
     import torch
@@ -237,8 +308,13 @@ def run_gpu(args, rank, world, local_rank):
     # a pool of distinct requests per rank (different seeds per rank); the
     # candidate split shares one request across the ranks
     pool_n = max(2, args.pool)
-    pool = [P.generate_requests(n_req, n_total, ll_tokens=L, seed=(0 if split else 1000 * rank) + i)
-            for i in range(pool_n)]
+    # the reference generator's requests (dataset.synthetic_requests, the
+    # draw-for-draw port of generate_synthetic; rank 0's C2 pool = seeds 0..3,
+    # pinned by tests/golden/shapes/c2_generator.json)
+    base = 0 if split else 1000 * rank
+    flat = _gen_requests([base + (0 if split else i * n_req + j) for i in range(pool_n) for j in range(n_req)],
+                         n_total, L)
+    pool = [flat[i * n_req:(i + 1) * n_req] for i in range(pool_n)]
     if split:
         packed = [[(r.user, r.candidates[c_lo:c_hi], r.ctx) for r in reqs] for reqs in pool]
     else:
@@ -388,7 +464,7 @@ def run_gpu(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "strong" if split else "weak", "vs_baseline": None,
         "dtype": ("bf16x3 split GEMMs on tcgen05 (f32 accumulate); NN: fp16 tcgen05 scan + f64 exact "
                   "re-scoring" if mode == "bf16" else "fp32 SIMT transformer; NN: fp16 scan + f64 re-scoring"),
-        "mode": mode, "data": "synthetic (generate_requests, seqrank.dataset distribution), random-init weights seed 0",
+        "mode": mode, "data": "synthetic (the reference's generate_synthetic: dataset.synthetic_requests), random-init weights seed 0",
         "config": {"workload": f"{args.config}: {n_req} request(s) x {n_cand} candidates, L={L}, "
                                f"RT=256, IMP=256, NNConfig{nn_t} -> S={nn.seq_len}, 2 layers d=64",
                    "requests_per_step_per_gpu": n_req, "candidates_per_step_per_gpu": cand_step,
@@ -516,21 +592,25 @@ def main():
         n_req, n_cand, L, nn_t = CONFIGS[args.config]
         cb = cpu_baseline(args.config, steps=args.steps, warmup=args.warmup, budget_s=90.0)
         value = cb["value"]
-        print(json.dumps({
+        line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "impl": "reference",
-            "n_gpus": 0, "steps": cb["steps_timed"], "warmup": max(1, min(args.warmup, 5)),
-            "ms_per_step": round(1e3 * n_cand / value, 3), "higher_is_better": True,
+            "n_gpus": 0, "steps": cb["steps_timed"], "warmup": max(1, min(args.warmup, 2)),
+            "ms_per_step": cb["p50_request_ms"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64 (numpy)",
-            "data": "synthetic (generate_requests), random-init weights seed 0",
+            "data": "synthetic (the reference's generate_synthetic), random-init weights seed 0",
             "config": {"workload": f"{args.config}: {n_req} request(s) x {n_cand} candidates, L={L}, "
-                                   f"NNConfig{nn_t} (CPU: bounded candidate sample per process)"},
-            "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cb["cores"],
-                             "kind": "port", "sample": cb["sample"], "cpu_model": cb["cpu_model"],
-                             "per_process_cand_s": cb["per_process_cand_s"],
-                             "p50_sample_ms": cb["p50_sample_ms"], "p99_sample_ms": cb["p99_sample_ms"]},
+                                   f"NNConfig{nn_t} (every process scores whole requests)"},
+            "p50_request_ms": cb["p50_request_ms"], "p99_request_ms": cb["p99_request_ms"],
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
+                                                 "per_process_cand_s", "p50_request_ms", "p99_request_ms")},
             "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
-        }))
+        }
+        if cb["kind"] == "reference":  # the oracle port on the same cores, for comparison
+            port = cpu_baseline(args.config, steps=2, warmup=1, budget_s=20.0, kind="port")
+            line["port"] = {k: port[k] for k in ("value", "cores", "kind", "per_process_cand_s",
+                                                  "p50_request_ms", "p99_request_ms")}
+        print(json.dumps(line), flush=True)
         return
 
     import torch.distributed as dist
@@ -546,9 +626,9 @@ def main():
             raise SystemExit(f"bench: {world} ranks but only {torch.cuda.device_count()} visible GPU(s)")
         out = run_gpu(args, rank, world, local_rank)
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            cb = cpu_baseline(args.config, steps=3, warmup=1, budget_s=20.0)
+            cb = cpu_baseline(args.config, steps=2, warmup=1, budget_s=15.0)
             out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
-                                                       "per_process_cand_s", "p50_sample_ms", "p99_sample_ms")}
+                                                       "per_process_cand_s", "p50_request_ms", "p99_request_ms")}
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
