@@ -148,6 +148,12 @@ int tav2_rank(tav2_ctx* ctx, const tav2_request* reqs, int n_req, int mode, floa
 int tav2_rank_submit(tav2_ctx* ctx, const tav2_request* reqs, int n_req, int mode, int want_idx,
                      void* stream, int32_t* slot_out);
 
+/* Block until a submitted rank's kernels and result copies finished, without
+ * touching the context's staging state: a completion thread may wait here
+ * while another thread submits into the other slot (the caller guarantees
+ * the slot is not resubmitted before it is collected). */
+int tav2_rank_wait(tav2_ctx* ctx, int slot);
+
 /* Wait for a submitted rank and copy its results out: logits_host
  * [n_items, 4] f32, idx_host (nullable, requires want_idx) [n_items, seq_len]. */
 int tav2_rank_collect(tav2_ctx* ctx, int slot, float* logits_host, int32_t* idx_host);

@@ -1117,6 +1117,12 @@ int tav2_rank_submit(tav2_ctx* c, const tav2_request* reqs, int n_req, int mode,
   return TAV2_OK;
 }
 
+int tav2_rank_wait(tav2_ctx* c, int slot) {
+  if (!c || slot < 0 || slot >= tav2_ctx::kStageSlots) return fail(TAV2_EINVAL, "bad slot");
+  CU(cudaEventSynchronize(c->ev_done[slot]));
+  return TAV2_OK;
+}
+
 int tav2_rank_collect(tav2_ctx* c, int slot, float* logits_host, int32_t* idx_host) {
   if (!c || slot < 0 || slot >= tav2_ctx::kStageSlots) return fail(TAV2_EINVAL, "bad slot");
   if (!logits_host) return fail(TAV2_EINVAL, "logits_host is null");

@@ -473,6 +473,37 @@ class Engine:
             collect(pending)
         return out
 
+    # ---- the serving loop's primitives (serving.PipelinedHandler) ----
+    def fits(self, requests) -> bool:
+        """True when the request list stages as one batch (no overflow path)."""
+        ch = list(self._chunks(list(requests)))
+        return len(ch) == 1 and not ch[0][1]
+
+    @_locked
+    def submit(self, requests, mode: str = "bf16", want_idx: bool = False) -> tuple[int, int, object]:
+        """tav2_rank_submit: stage into the next free slot and enqueue the
+        whole rank; returns (slot, items, keep-alive).  At most two submits
+        may be outstanding: ``wait`` + ``collect`` a slot before it is reused."""
+        if self.model is None:
+            raise ValidationError("no model loaded")
+        pack = _Pack(requests)
+        slot = ctypes.c_int32()
+        N.check(self._lib.tav2_rank_submit(self._ctx, pack.arr, len(requests), self._mode(mode), int(want_idx),
+                                           self.stream(), ctypes.byref(slot)))
+        return slot.value, sum(len(c) for _, c, _ in requests), pack
+
+    def wait(self, slot: int) -> None:
+        """tav2_rank_wait: block until a submitted rank finished.  Deliberately
+        not under the engine lock, so another thread can submit meanwhile."""
+        N.check(self._lib.tav2_rank_wait(self._ctx, int(slot)))
+
+    @_locked
+    def collect(self, slot: int, n: int, want_idx: bool = False):
+        logits = np.empty((n, 4), np.float32)
+        idx = np.empty((n, self.config.nn.seq_len), np.int32) if want_idx else None
+        N.check(self._lib.tav2_rank_collect(self._ctx, int(slot), logits.ctypes.data, N.ptr(idx)))
+        return (logits, idx) if want_idx else logits
+
     @_locked
     def run_staged(self, mode: str, logits: torch.Tensor | None = None) -> None:
         """Device-resident path (bench ``value``): NN + score on the staged batch."""

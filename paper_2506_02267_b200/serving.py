@@ -3,21 +3,34 @@ specifies but never ships, composed as the reference's serving-optimised
 path build_dedup_batch -> fused_assemble -> encode_batch -> forward_fused ->
 pool -> head (trainer.py:354-366), executed on the B200.
 
-Also the nearest-rank percentile of ``serving/stats.py:36-45`` used for the
-p50/p99 request latencies, and a ``DynamicBatcher`` handler adapter
-(batcher.py:87, :140) so the GPU rank plugs into the reference batcher.
+The serving loop around it:
+
+* ``LatencyStats`` -- sliding-window per-stage latencies with nearest-rank
+  percentiles (serving/stats.py:13-55; stages queueing, batch_prep,
+  staging, forward, e2e);
+* ``DynamicBatcher`` / ``BatcherConfig`` / ``BatchPolicy`` / ``Pending`` --
+  the reference's flush policy and worker pool (serving/batcher.py:14-143),
+  same API, so either batcher drives the handlers below;
+* ``batcher_handler`` -- synchronous handler, one engine per batcher worker
+  (``handler(batch, worker_index)``, batcher.py:140);
+* ``PipelinedHandler`` -- the handler returns as soon as a batch's rank is
+  submitted (pinned staging slot, H2D, kernels and result copies enqueued);
+  a completion thread collects results in order, so the host side of the
+  next batch overlaps the GPU work of the current one (two slots in flight).
 """
 
 from __future__ import annotations
 
 import math
+import queue
+import threading
+import time
+from collections import deque
 from dataclasses import dataclass, field
 
 import numpy as np
 
-import threading
-
-from .core import IMPRESSION_CAP, LIFELONG_CAP, REALTIME_CAP, TokenBlock, UserSequences
+from .core import IMPRESSION_CAP, LIFELONG_CAP, REALTIME_CAP, TokenBlock, UserSequences, ValidationError
 from .dataset import HEAD_NAMES, context_features, read_store
 from .model import HeadConfig
 from .runtime import Engine, StoreUser
@@ -153,22 +166,324 @@ class DeviceFeatureStore:
         return store
 
 
-def batcher_handler(engine: Engine, store, mode: str = "bf16"):
-    """Adapter for ``DynamicBatcher(cfg, handler)``: each Pending payload is
-    ``(user_id, candidates)``; users come from ``store.get`` (store.py:54) --
-    or, for a DeviceFeatureStore, straight from HBM."""
+# ---------------------------------------------------------------------------
+# Per-stage latency statistics (serving/stats.py:13-55)
+# ---------------------------------------------------------------------------
 
-    def user_of(uid):
-        if isinstance(store, DeviceFeatureStore):
-            return store.ref(uid)
-        return store.get(uid)
+STAGES = ("queueing", "batch_prep", "staging", "forward", "e2e")
+WINDOW_SECONDS = 60.0
 
-    def handler(batch, worker_index):  # noqa: ARG001 - batcher contract
-        reqs = [(uid, user_of(uid), cands) for uid, cands in (p.payload for p in batch)]
-        for p, r in zip(batch, rank_many(engine, reqs, mode=mode)):
+
+class LatencyStats:
+    """(timestamp, duration) samples per stage; nearest-rank percentiles over
+    the trailing window (stats.py:13-55)."""
+
+    def __init__(self, window: float = WINDOW_SECONDS, clock=time.monotonic):
+        self.window = window
+        self.clock = clock
+        self._samples: dict[str, deque] = {stage: deque() for stage in STAGES}
+        self._lock = threading.Lock()
+
+    def record(self, stage: str, seconds: float, now: float | None = None) -> None:
+        if stage not in self._samples:
+            raise KeyError(f"unknown stage {stage!r}")
+        now = self.clock() if now is None else now
+        with self._lock:
+            self._samples[stage].append((now, seconds))
+
+    def _evict(self, stage: str, now: float) -> None:
+        cutoff = now - self.window
+        q = self._samples[stage]
+        while q and q[0][0] <= cutoff:
+            q.popleft()
+
+    def percentile(self, stage: str, p: float, now: float | None = None) -> float | None:
+        now = self.clock() if now is None else now
+        with self._lock:
+            self._evict(stage, now)
+            values = [v for _, v in self._samples[stage]]
+        return nearest_rank(values, p)
+
+    def summary(self, now: float | None = None) -> dict[str, dict[str, float | None]]:
+        return {stage: {"p50": self.percentile(stage, 50, now), "p90": self.percentile(stage, 90, now),
+                        "p99": self.percentile(stage, 99, now)} for stage in STAGES}
+
+
+# ---------------------------------------------------------------------------
+# Dynamic batching (serving/batcher.py:14-143): the flush policy and a worker
+# pool calling handler(batch, worker_index)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class BatcherConfig:
+    max_batch: int = 128      # items across the batch
+    max_wait: float = 0.005   # seconds the oldest request may wait
+    workers: int = 1
+
+    def validate(self) -> None:
+        if self.max_batch < 1 or self.workers < 1 or self.max_wait < 0:
+            raise ValidationError("invalid batcher configuration")
+
+
+@dataclass
+class Pending:
+    payload: object
+    items: int
+    enqueue_time: float
+    done: threading.Event = field(default_factory=threading.Event)
+    result: object = None
+    error: Exception | None = None
+
+    def set_result(self, result) -> None:
+        self.result = result
+        self.done.set()
+
+    def set_error(self, error: Exception) -> None:
+        self.error = error
+        self.done.set()
+
+
+class BatchPolicy:
+    """Flush when pending items reach max_batch or the oldest request has
+    waited max_wait; whole requests, oldest first; an oversized request
+    flushes alone (batcher.py:47-80)."""
+
+    def __init__(self, cfg: BatcherConfig):
+        cfg.validate()
+        self.cfg = cfg
+
+    def deadline(self, oldest_enqueue: float) -> float:
+        return oldest_enqueue + self.cfg.max_wait
+
+    def should_flush(self, pending_items: int, oldest_enqueue: float, now: float) -> bool:
+        return pending_items >= self.cfg.max_batch or now >= self.deadline(oldest_enqueue)
+
+    def plan(self, pending: list, now: float):
+        if not pending or not self.should_flush(sum(p.items for p in pending), pending[0].enqueue_time, now):
+            return None
+        batch, items = [], 0
+        for p in pending:
+            if batch and items + p.items > self.cfg.max_batch:
+                break
+            batch.append(p)
+            items += p.items
+        return batch
+
+
+class DynamicBatcher:
+    """Queue + worker threads; each worker drains batches per the policy and
+    calls handler(batch, worker_index) (batcher.py:83-143)."""
+
+    def __init__(self, cfg: BatcherConfig, handler, clock=time.monotonic):
+        self.cfg = cfg
+        self.policy = BatchPolicy(cfg)
+        self.handler = handler
+        self.clock = clock
+        self._queue: queue.Queue = queue.Queue()
+        self._threads: list[threading.Thread] = []
+        self._stop = threading.Event()
+
+    def start(self) -> None:
+        for i in range(self.cfg.workers):
+            t = threading.Thread(target=self._worker, args=(i,), daemon=True)
+            t.start()
+            self._threads.append(t)
+
+    def stop(self) -> None:
+        self._stop.set()
+        for t in self._threads:
+            t.join(timeout=5)
+        self._threads.clear()
+
+    def submit(self, payload, items: int) -> Pending:
+        p = Pending(payload, items, self.clock())
+        self._queue.put(p)
+        return p
+
+    def _worker(self, index: int) -> None:
+        carry = None
+        while not self._stop.is_set():
+            if carry is not None:
+                first, carry = carry, None
+            else:
+                try:
+                    first = self._queue.get(timeout=0.05)
+                except queue.Empty:
+                    continue
+            batch, items = [first], first.items
+            deadline = self.policy.deadline(first.enqueue_time)
+            while items < self.cfg.max_batch:
+                remaining = deadline - self.clock()
+                if remaining <= 0:
+                    break
+                try:
+                    nxt = self._queue.get(timeout=remaining)
+                except queue.Empty:
+                    break
+                if items + nxt.items > self.cfg.max_batch:
+                    carry = nxt
+                    break
+                batch.append(nxt)
+                items += nxt.items
+            try:
+                self.handler(batch, index)
+            except Exception as exc:  # noqa: BLE001 - propagate to the waiters
+                for p in batch:
+                    p.set_error(exc)
+
+
+# ---------------------------------------------------------------------------
+# Batcher handlers
+# ---------------------------------------------------------------------------
+
+def _engine_picker(engines):
+    """engines: one Engine (shared: its lock serialises the workers), a list
+    indexed by worker_index, or a factory worker_index -> Engine (called once
+    per worker)."""
+    if isinstance(engines, Engine):
+        return lambda w: engines
+    if callable(engines):
+        made, lock = {}, threading.Lock()
+
+        def pick(w):
+            with lock:
+                if w not in made:
+                    made[w] = engines(w)
+                return made[w]
+        return pick
+    lst = list(engines)
+    return lambda w: lst[w % len(lst)]
+
+
+def _user_of(store, uid):
+    if isinstance(store, DeviceFeatureStore):
+        return store.ref(uid)
+    return store.get(uid)
+
+
+def batcher_handler(engines, store, mode: str = "bf16", stats: LatencyStats | None = None):
+    """Synchronous handler for ``DynamicBatcher(cfg, handler)``: each Pending
+    payload is ``(user_id, candidates)``; users come from ``store.get``
+    (store.py:54) -- or, for a DeviceFeatureStore, straight from HBM (its
+    engine then serves every worker).  One engine per worker (``engines`` a
+    list or a factory) runs workers in parallel; a single engine is shared
+    under its lock.  ``stats`` records the five SPEC stages."""
+    pick = (lambda w: store.engine) if isinstance(store, DeviceFeatureStore) else _engine_picker(engines)
+
+    def handler(batch, worker_index):
+        t0 = time.monotonic()
+        eng = pick(worker_index)
+        reqs = []
+        for p in batch:
+            uid, cands = p.payload
+            if stats is not None:
+                stats.record("queueing", t0 - p.enqueue_time)
+            reqs.append((uid, _user_of(store, uid), cands))
+        t1 = time.monotonic()
+        if stats is not None:
+            stats.record("batch_prep", t1 - t0)
+        for p, r in zip(batch, rank_many(eng, reqs, mode=mode)):
             p.set_result(r)
+        now = time.monotonic()
+        if stats is not None:
+            stats.record("forward", now - t1)
+            for p in batch:
+                stats.record("e2e", now - p.enqueue_time)
 
     return handler
+
+
+class PipelinedHandler:
+    """Pipelined ``DynamicBatcher`` handler over one engine's two staging
+    slots (tav2_rank_submit / tav2_rank_wait / tav2_rank_collect).
+
+    ``handler(batch, worker_index)`` packs the batch and submits its whole
+    rank (staging copy, kernels, result copy) and returns at once; a
+    completion thread waits for each submitted rank in order, collects its
+    logits and completes the Pending results.  So while batch i runs on the
+    GPU, the batcher already forms, packs and stages batch i+1.  At most two
+    ranks are in flight (one per staging slot).  A batch beyond the engine
+    capacity takes the engine's counted overflow path synchronously.
+
+    Stages recorded in ``stats``: queueing (enqueue -> handler), batch_prep
+    (request assembly), staging (pack + submit), forward (submit -> results
+    collected), e2e (enqueue -> result set)."""
+
+    def __init__(self, engine: Engine, store, mode: str = "bf16", stats: LatencyStats | None = None):
+        self.engine = engine
+        self.store = store
+        self.mode = mode
+        self.stats = stats
+        self._slots = threading.Semaphore(2)
+        self._inflight: queue.Queue = queue.Queue()
+        self._submit_lock = threading.Lock()
+        self._thread = threading.Thread(target=self._complete, daemon=True)
+        self._closed = False
+        self._thread.start()
+
+    def __call__(self, batch, worker_index=0):  # noqa: ARG002 - batcher contract
+        t0 = time.monotonic()
+        reqs, meta = [], []
+        for p in batch:
+            uid, cands = p.payload
+            if self.stats is not None:
+                self.stats.record("queueing", t0 - p.enqueue_time)
+            user = _user_of(self.store, uid)
+            c = np.asarray(cands, np.float32)
+            reqs.append((UserSequences() if user is None else user, c,
+                         context_features(uid, self.engine.config.ctx_dim)))
+            meta.append((p, len(c), user is None))
+        t1 = time.monotonic()
+        if self.stats is not None:
+            self.stats.record("batch_prep", t1 - t0)
+        if not self.engine.fits(reqs):
+            logits = self.engine.rank_requests(reqs, mode=self.mode)
+            self._finish(meta, logits, t1)
+            return
+        self._slots.acquire()
+        try:
+            with self._submit_lock:  # submission order == completion order
+                slot, n, keep = self.engine.submit(reqs, mode=self.mode)
+                self._inflight.put((slot, n, keep, meta, t1))
+        except Exception:
+            self._slots.release()
+            raise
+        if self.stats is not None:
+            self.stats.record("staging", time.monotonic() - t1)
+
+    def _finish(self, meta, logits, t_submit):
+        now = time.monotonic()
+        if self.stats is not None:
+            self.stats.record("forward", now - t_submit)
+        o = 0
+        for p, n, cold in meta:
+            p.set_result(_response(np.arange(n, dtype=np.uint64), logits[o:o + n], self.engine.config.heads, cold))
+            o += n
+            if self.stats is not None:
+                self.stats.record("e2e", time.monotonic() - p.enqueue_time)
+
+    def _complete(self):
+        while True:
+            item = self._inflight.get()
+            if item is None:
+                return
+            slot, n, _keep, meta, t_submit = item
+            try:
+                self.engine.wait(slot)
+                logits = self.engine.collect(slot, n)
+            except Exception as exc:  # noqa: BLE001 - fail this batch's waiters
+                self._slots.release()
+                for p, _, _ in meta:
+                    p.set_error(exc)
+                continue
+            self._slots.release()
+            self._finish(meta, logits, t_submit)
+
+    def close(self) -> None:
+        if not self._closed:
+            self._closed = True
+            self._inflight.put(None)
+            self._thread.join(timeout=10)
 
 
 def nearest_rank(values, p: float) -> float | None:
