@@ -436,6 +436,11 @@ def run_gpu(args, rank, world, local_rank):
         lat_st_sync.append(time.perf_counter() - ts)
     h2d_store = h2d - sum(u.total_tokens() for u, _, _ in packed[0]) * (32 + 2 + 1)
     eng.store_reserve(0)
+    # (d) open loop: requests arrive at a fixed rate (half the pipelined e2e
+    #     request rate) into the DynamicBatcher + PipelinedHandler serving
+    #     loop; p50/p99 of the per-request end-to-end latency (queueing
+    #     included) and of each serving stage
+    open_loop = None if split else _open_loop(eng, pool, mode, rate=0.5 * e2e_value / cand_step)
 
     # ---- roofline of the dominant kernel ----
     fl = flops_per_candidate(L, nn_t)
@@ -487,12 +492,57 @@ def run_gpu(args, rank, world, local_rank):
                           "p99_request_ms": round(1e3 * nearest_rank(lat_st, 99), 4),
                           "sync_p50_request_ms": round(1e3 * nearest_rank(lat_st_sync, 50), 4),
                           "sync_p99_request_ms": round(1e3 * nearest_rank(lat_st_sync, 99), 4)}},
+        "open_loop": open_loop,
         "gpu_launches": launches_per_step * args.steps,
         "kernels": {k: {"ms_per_launch": round(v[0] / max(v[1], 1), 4), "launches": v[1]} for k, v in kt.items()},
         "roofline": roof,
         "clocks": clk.summary(),
     }
     return out
+
+
+def _open_loop(eng, pool, mode, rate, seconds=2.0):
+    """Fixed-rate arrivals of the pool's requests (payload (user id,
+    candidates)) through serving.DynamicBatcher + serving.PipelinedHandler."""
+    from paper_2506_02267_b200 import serving as S
+
+    users, payloads = {}, []
+    for reqs in pool:
+        for r in reqs:
+            uid = len(payloads) + 1  # distinct ids (every generated request's user is id 1)
+            users[uid] = r.user
+            payloads.append((uid, r.candidates))
+    n_item = len(payloads[0][1])
+    stats = S.LatencyStats(window=3600.0)
+    h = S.PipelinedHandler(eng, users, mode=mode, stats=stats)
+    b = S.DynamicBatcher(S.BatcherConfig(max_batch=n_item, max_wait=0.0005, workers=1), h)
+    b.start()
+    n = max(10, int(rate * seconds))
+    try:
+        for i in range(20):  # warm the loop
+            b.submit(payloads[i % len(payloads)], n_item).done.wait(10)
+        stats = S.LatencyStats(window=3600.0)
+        h.stats = stats
+        t0 = time.perf_counter()
+        ps = []
+        for i in range(n):
+            dt = t0 + i / rate - time.perf_counter()
+            if dt > 0:
+                time.sleep(dt)
+            ps.append(b.submit(payloads[i % len(payloads)], n_item))
+        for p in ps:
+            p.done.wait(30)
+        wall = time.perf_counter() - t0
+    finally:
+        b.stop()
+        h.close()
+    errors = sum(p.error is not None for p in ps)
+    summ = stats.summary()
+    return {"arrival_rate_req_s": round(rate, 1), "requests": n, "errors": errors,
+            "offered_cand_s": round(rate * n_item, 1), "achieved_cand_s": round(n * n_item / wall, 1),
+            "p50_request_ms": round(1e3 * summ["e2e"]["p50"], 4), "p99_request_ms": round(1e3 * summ["e2e"]["p99"], 4),
+            "stages_ms": {k: {q: round(1e3 * v, 4) for q, v in summ[k].items() if v is not None} for k in summ},
+            "api": "serving.DynamicBatcher(max_batch=1 request) + serving.PipelinedHandler"}
 
 
 def _traffic(kernel):
