@@ -5,6 +5,8 @@
 #ifndef TAV2_INTERNAL_H_
 #define TAV2_INTERNAL_H_
 
+#include <stdint.h>
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -29,6 +31,10 @@ int tav2_debug_timeline(long long* dev, int block);
  * (candidate, source) select time and survivor count.  NULL disables.  Not
  * thread-safe. */
 int tav2_debug_cta(long long* dev);
+
+/* CUDA-graph cache of the launch chain (run_chain): number of captured
+ * graphs held and whether capture was abandoned (direct launches only). */
+int tav2_graph_info(const void* ctx, int32_t* n_graphs, int32_t* broken);
 
 #ifdef __cplusplus
 }

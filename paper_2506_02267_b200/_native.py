@@ -32,7 +32,7 @@ EXPORTS = (
     "tav2_kernel_times", "tav2_tc_selftest", "tav2_debug_timeline", "tav2_debug_cta",
     "tav2_rank_submit", "tav2_rank_collect",
     "tav2_store_reserve", "tav2_store_put", "tav2_store_remove", "tav2_store_count",
-    "tav2_similarity", "tav2_pool", "tav2_rank_wait",
+    "tav2_similarity", "tav2_pool", "tav2_rank_wait", "tav2_graph_info",
 )
 
 
@@ -100,6 +100,7 @@ def lib() -> ctypes.CDLL:
                                            vp, ctypes.POINTER(i32)]
             L.tav2_rank_collect.argtypes = [vp, ctypes.c_int, vp, vp]
             L.tav2_rank_wait.argtypes = [vp, ctypes.c_int]
+            L.tav2_graph_info.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
             L.tav2_store_reserve.argtypes = [vp, i32]
             L.tav2_store_put.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(Request)]
             L.tav2_store_remove.argtypes = [vp, ctypes.c_uint64]

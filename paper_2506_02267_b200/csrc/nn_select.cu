@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(32 * kSelWarps) nn_select_kernel(Staged st, NN
     if (item < st.n_items && item < sel.n_first) {
       __syncwarp();
       if ((threadIdx.x & 31) == 0) {
-        st_release_gpu(sel.done + 3 * item + sel_source(), sel.epoch);
+        st_release_gpu(sel.done + 3 * item + sel_source(), ld_acquire_gpu(sel.epoch));
       }
     }
   }

@@ -62,10 +62,17 @@ __device__ __forceinline__ void prep_body(const Staged& st, int with_feat, const
                                           int2 raw, unsigned act, int surf_raw, float4 c0, float4 c1,
                                           const float* deq_s);
 
-__global__ void __launch_bounds__(256) prep_kernel(Staged st, Params p, int with_feat) {
+__global__ void __launch_bounds__(256) prep_kernel(Staged st, Params p, int with_feat, uint32_t* epoch_bump) {
   cta_stamp(kDbgPrep, 0);
   griddep_launch();
   griddep_wait();  // the previous step's kernels may still read tok_unit / cand_unit
+  // a fresh select-flag epoch for this run (SelFlags): the previous run's
+  // select / SKUT grids are complete here; the epoch is never 0 (the flags'
+  // reset value)
+  if (epoch_bump && blockIdx.x == 0 && threadIdx.x == 0) {
+    const uint32_t e = *epoch_bump + 1u;
+    *epoch_bump = e ? e : 1u;
+  }
   cta_stamp(kDbgPrep, 2);
   // this thread's global inputs, requested before the table staging so the
   // round trips overlap
@@ -189,11 +196,12 @@ __device__ __forceinline__ void prep_body(const Staged& st, int with_feat, const
 
 cudaError_t set_dbg_cta_prep(long long* dev) { return set_dbg_cta_tu(dev); }
 
-cudaError_t launch_prep(const Staged& st, const Params* p, cudaStream_t s) {
+cudaError_t launch_prep(const Staged& st, const Params* p, cudaStream_t s, uint32_t* epoch_bump) {
   int n = st.n_tok + st.n_items;
   if (n == 0) return cudaSuccess;
   const Params pz{};
-  return launch_pdl(prep_kernel, dim3((4 * n + 255) / 256), dim3(256), 0, s, st, p ? *p : pz, (int)(p != nullptr));
+  return launch_pdl(prep_kernel, dim3((4 * n + 255) / 256), dim3(256), 0, s, st, p ? *p : pz, (int)(p != nullptr),
+                    epoch_bump);
 }
 
 }  // namespace tav2

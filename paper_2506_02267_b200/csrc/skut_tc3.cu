@@ -253,7 +253,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   // three select flags (sel_ready, checked before the candidate's idx reads)
   if (!sel.done) griddep_wait();
   if (sel.done && (int)blockIdx.x < n && tid < 3) {  // the first candidate's three selections
-    while (ld_acquire_gpu(sel.done + 3 * blockIdx.x + tid) != sel.epoch) __nanosleep(100);
+    const uint32_t ep = ld_acquire_gpu(sel.epoch);  // this run's epoch (bumped by prep)
+    while (ld_acquire_gpu(sel.done + 3 * blockIdx.x + tid) != ep) __nanosleep(100);
   }
   if (sel.done) __syncthreads();
   bool sel_all = !sel.done;  // the whole select grid is complete and visible

@@ -128,7 +128,23 @@ struct tav2_ctx {
   int32_t* idx = nullptr;
   float* logits = nullptr;
   uint32_t* sel_done = nullptr;  // per-(candidate, source) select flags (SelFlags)
-  uint32_t sel_epoch = 0;
+  uint32_t* sel_epoch = nullptr; // device word: the current run's flag epoch (prep bumps it)
+  // CUDA graphs of the launch chain prep .. SKUT (run_chain): one per
+  // (staging slot, mode, output buffer, batch plan), captured the second
+  // time a shape is seen and replayed after; invalidated by tav2_load_params
+  struct GraphEntry {
+    int slot, mode;
+    const float* logits;
+    Plan plan;
+    cudaGraphExec_t exec;
+    int launches;
+    uint64_t last_use;
+  };
+  std::vector<GraphEntry> graphs;
+  std::vector<std::pair<int, Plan>> graph_seen;  // shapes run once (candidates for capture)
+  cudaStream_t cap_stream = nullptr;
+  uint64_t graph_tick = 0;
+  bool graph_broken = false;  // a capture failed: launch directly from then on
   float* skut_scratch = nullptr;
   // params
   float* d_params = nullptr;
@@ -259,6 +275,9 @@ int free_all(tav2_ctx* c) {
   cudaFree(c->scan.surv);
   cudaFree(c->idx);
   cudaFree(c->sel_done);
+  cudaFree(c->sel_epoch);
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   cudaFree(c->logits);
   cudaFree(c->skut_scratch);
   cudaFree(c->d_params);
@@ -402,6 +421,10 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
   if ((e = cudaMalloc(&c->idx, (size_t)N * S * 4)) != cudaSuccess) return bad(e, "idx");
   if ((e = cudaMalloc(&c->sel_done, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "select flags");
   if ((e = cudaMemset(c->sel_done, 0, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "select flags");
+  if ((e = cudaMalloc(&c->sel_epoch, 4)) != cudaSuccess) return bad(e, "select epoch");
+  if ((e = cudaMemset(c->sel_epoch, 0, 4)) != cudaSuccess) return bad(e, "select epoch");
+  if ((e = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return bad(e, "capture stream");
   if ((e = cudaMalloc(&c->logits, (size_t)N * kHeads * 4)) != cudaSuccess) return bad(e, "logits");
   {
     int sms = 148;
@@ -597,6 +620,9 @@ int tav2_load_params(tav2_ctx* c, int n, const char* const* names, const float* 
     for (int l = 0; l < L; ++l) c->images3.w[l] = c->d_images3 + (size_t)l * lay;
     c->images3.wout = c->d_images3 + (size_t)L * lay;
   }
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);  // captured with the old parameters
+  c->graphs.clear();
+  c->graph_seen.clear();
   c->params_ok = true;
   return TAV2_OK;
 }
@@ -944,9 +970,8 @@ int check_ready(tav2_ctx* c, int mode) {
 // epoch per run, so flags left by any earlier run never match.
 SelFlags next_sel(tav2_ctx* c) {
 #ifdef TAV2_NO_SELFLAGS
-  return SelFlags{nullptr, 0, 0};
+  return SelFlags{nullptr, nullptr, 0};
 #endif
-  if (++c->sel_epoch == 0) c->sel_epoch = 1;
   return SelFlags{c->sel_done, c->sel_epoch, device_sms()};
 }
 
@@ -954,7 +979,9 @@ SelFlags next_sel(tav2_ctx* c) {
 // the reference's f64 formula, so the index sets are the reference's).
 int run_nn(tav2_ctx* c, int32_t* idx, double* scores, cudaStream_t s, SelFlags sel = {nullptr, 0, 0}) {
   Staged st = staged_view(c);
-  CU(timed(c, "prep", s, [&] { return launch_prep(st, c->params_ok ? &c->params : nullptr, s); }));
+  CU(timed(c, "prep", s, [&] {
+    return launch_prep(st, c->params_ok ? &c->params : nullptr, s, sel.done ? c->sel_epoch : nullptr);
+  }));
   CU(timed(c, "nn_scan1", s, [&] { return launch_nn_scan(st, c->nn, c->scan, 1, s); }));
   CU(timed(c, "nn_bound", s, [&] { return launch_nn_bound(st, c->nn, c->scan, s); }));
   CU(timed(c, "nn_scan2", s, [&] { return launch_nn_scan(st, c->nn, c->scan, 2, s); }));
@@ -991,6 +1018,83 @@ int run_score(tav2_ctx* c, int mode, const int32_t* idx, float* logits, float* p
   }));
   return TAV2_OK;
 }
+
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TAV2_NO_GRAPH");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
+bool same_plan(const Plan& a, const Plan& b) {  // field by field (no padding bytes)
+  return a.n_req == b.n_req && a.n_items == b.n_items && a.n_tok == b.n_tok && a.n_tiles == b.n_tiles &&
+         a.n_work == b.n_work && a.tile_size == b.tile_size && a.n_scopy == b.n_scopy && a.off_req == b.off_req &&
+         a.off_tiles == b.off_tiles && a.off_work == b.off_work && a.off_item_req == b.off_item_req &&
+         a.off_ctx == b.off_ctx && a.off_cand == b.off_cand && a.off_scopy == b.off_scopy &&
+         a.off_action == b.off_action && a.off_surface == b.off_surface && a.off_emb == b.off_emb &&
+         a.bytes == b.bytes;
+}
+
+// The whole launch chain of a rank on the staged batch: prep -> scan1 ->
+// bound -> scan2 -> select -> SKUT (programmatic dependent launches, the
+// select -> SKUT per-candidate flag handover).  A batch shape seen before
+// runs as one CUDA graph (captured on the ctx's capture stream the second
+// time the shape occurs; every kernel argument is a function of the slot,
+// the plan, the mode and the output buffer -- the flag epoch lives in
+// device memory), so a repeated shape costs one cudaGraphLaunch instead of
+// six launches.  Profiling (per-kernel events) launches directly.
+int run_chain(tav2_ctx* c, int mode, float* logits, cudaStream_t s) {
+  const SelFlags sel = next_sel(c);
+  const Plan& pl = c->plans[c->cur];
+  if (!c->profiling && graphs_enabled() && !c->graph_broken) {
+    for (auto& g : c->graphs) {
+      if (g.slot == c->cur && g.mode == mode && g.logits == logits && same_plan(g.plan, pl)) {
+        g.last_use = ++c->graph_tick;
+        c->launches = g.launches;
+        CU(cudaGraphLaunch(g.exec, s));
+        return TAV2_OK;
+      }
+    }
+    bool seen = false;
+    for (auto& x : c->graph_seen) seen = seen || (x.first == c->cur && same_plan(x.second, pl));
+    if (seen) {  // second occurrence: capture
+      cudaGraph_t graph = nullptr;
+      cudaGraphExec_t exec = nullptr;
+      c->launches = 0;
+      int rc = TAV2_OK;
+      if (cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+        rc = run_nn(c, c->idx, nullptr, c->cap_stream, sel);
+        if (!rc) rc = run_score(c, mode, c->idx, logits, nullptr, c->cap_stream, sel);
+        const cudaError_t e = cudaStreamEndCapture(c->cap_stream, &graph);
+        if (!rc && e == cudaSuccess && graph && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+          if (c->graphs.size() >= 8) {  // evict the least recently used
+            auto lru = c->graphs.begin();
+            for (auto it = c->graphs.begin(); it != c->graphs.end(); ++it)
+              if (it->last_use < lru->last_use) lru = it;
+            cudaGraphExecDestroy(lru->exec);
+            c->graphs.erase(lru);
+          }
+          c->graphs.push_back({c->cur, mode, logits, pl, exec, c->launches, ++c->graph_tick});
+          if (graph) cudaGraphDestroy(graph);
+          CU(cudaGraphLaunch(exec, s));
+          return TAV2_OK;
+        }
+        if (graph) cudaGraphDestroy(graph);
+      }
+      cudaGetLastError();  // clear a capture error; launch directly from now on
+      c->graph_broken = true;
+    } else {
+      if (c->graph_seen.size() >= 32) c->graph_seen.erase(c->graph_seen.begin());
+      c->graph_seen.push_back({c->cur, pl});
+    }
+  }
+  c->launches = 0;
+  int rc = run_nn(c, c->idx, nullptr, s, sel);
+  if (!rc) rc = run_score(c, mode, c->idx, logits, nullptr, s, sel);
+  return rc;
+}
+
 
 }  // namespace
 
@@ -1087,10 +1191,7 @@ int tav2_run_staged(tav2_ctx* c, int mode, float* logits_dev, void* stream) {
   if (rc) return rc;
   CU(cudaSetDevice(c->device));
   cudaStream_t s = (cudaStream_t)stream;
-  c->launches = 0;
-  const SelFlags sel = next_sel(c);
-  if ((rc = run_nn(c, c->idx, nullptr, s, sel))) return rc;
-  if ((rc = run_score(c, mode, c->idx, logits_dev ? logits_dev : c->logits, nullptr, s, sel))) return rc;
+  if ((rc = run_chain(c, mode, logits_dev ? logits_dev : c->logits, s))) return rc;
   return mark_used(c, s);
 }
 
@@ -1104,9 +1205,7 @@ int tav2_rank_submit(tav2_ctx* c, const tav2_request* reqs, int n_req, int mode,
   int rc = tav2_stage(c, reqs, n_req, stream, &n);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  const SelFlags sel = next_sel(c);
-  if ((rc = run_nn(c, c->idx, nullptr, s, sel))) return rc;
-  if ((rc = run_score(c, mode, c->idx, c->logits, nullptr, s, sel))) return rc;
+  if ((rc = run_chain(c, mode, c->logits, s))) return rc;
   CU(cudaMemcpyAsync(c->h_out[slot], c->logits, (size_t)n * kHeads * 4, cudaMemcpyDeviceToHost, s));
   if (want_idx)
     CU(cudaMemcpyAsync(c->h_idx[slot], c->idx, (size_t)n * c->nn.seq_len * 4, cudaMemcpyDeviceToHost, s));
@@ -1151,6 +1250,14 @@ int tav2_rank(tav2_ctx* c, const tav2_request* reqs, int n_req, int mode, float*
 }
 
 int tav2_last_launch_count(const tav2_ctx* c) { return c ? c->launches : 0; }
+
+int tav2_graph_info(const void* ctx, int32_t* n_graphs, int32_t* broken) {
+  const tav2_ctx* c = static_cast<const tav2_ctx*>(ctx);
+  if (!c) return fail(TAV2_EINVAL, "null context");
+  if (n_graphs) *n_graphs = (int32_t)c->graphs.size();
+  if (broken) *broken = c->graph_broken ? 1 : 0;
+  return TAV2_OK;
+}
 
 int tav2_debug_timeline(long long* dev, int block) {
   return set_debug_timeline(dev, block) == cudaSuccess && set_debug_skut(dev ? dev + 320 : nullptr) == cudaSuccess &&

@@ -218,7 +218,7 @@ __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.
 // griddep_wait up front as for every other kernel.
 struct SelFlags {
   uint32_t* done;
-  uint32_t epoch;
+  const uint32_t* epoch;  // device word: the current run's epoch (prep_kernel bumps it)
   int n_first;
 };
 __device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
@@ -256,7 +256,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 
 // Host-side launchers (defined in the kernel translation units).
 namespace tav2 {
-cudaError_t launch_prep(const Staged& st, const Params* p, cudaStream_t s);
+cudaError_t launch_prep(const Staged& st, const Params* p, cudaStream_t s, uint32_t* epoch_bump = nullptr);
 bool skut_tc3_supported(const NNCfg& nn, const Params& p);
 cudaError_t launch_skut_tc3(const Params& p, const SkutImages3& img, const NNCfg& nn, const Staged& st,
                             const int32_t* idx, int n, float* logits, float* pooled, SelFlags sel,

@@ -517,6 +517,12 @@ class Engine:
                                      self.stream()))
         return (logits, pl) if pooled else logits
 
+    def graph_info(self) -> tuple[int, bool]:
+        """(captured launch-chain graphs held, capture abandoned)."""
+        n, b = ctypes.c_int32(), ctypes.c_int32()
+        N.check(self._lib.tav2_graph_info(self._ctx, ctypes.byref(n), ctypes.byref(b)))
+        return n.value, bool(b.value)
+
     def last_launch_count(self) -> int:
         return int(self._lib.tav2_last_launch_count(self._ctx))
 
