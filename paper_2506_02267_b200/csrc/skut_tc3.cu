@@ -34,6 +34,7 @@
 // A region [192, 256): LN1 out / Q' / O' (PV out) / LN2 out / x (pool).
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -81,22 +82,36 @@ __device__ __forceinline__ void t3_ld64(uint32_t ta, float* v) {
   tmem_ld32(ta + 32, r + 32);
   tmem_ld_wait();
 }
-// split n floats into packed bf16 hi/lo pairs: hi at [0, n/2), lo at [n/2, n)
-template <int N>
+// The operand format: F16 = false: bf16 hi/lo parts (bf16 mode); true: fp16
+// hi/lo parts (fp32 mode: 11-bit significands, ~2^-22 per 3-term product;
+// the softmax then uses the true row max so P stays in [0, 1], inside fp16's
+// normal range -- tools/split_precision_err.py).
+template <bool F16>
+__device__ __forceinline__ void t3_split(float a, float b, uint32_t& hi, uint32_t& lo) {
+  if constexpr (F16) split_pair_h(a, b, hi, lo);
+  else split_pair(a, b, hi, lo);
+}
+template <bool F16>
+__host__ __device__ constexpr uint32_t t3_idesc(int M, int N, int a_mn = 0, int b_mn = 0) {
+  return F16 ? idesc_f16(M, N, a_mn, b_mn) : idesc_bf16(M, N, a_mn, b_mn);
+}
+// split n floats into packed hi/lo pairs: hi at [0, n/2), lo at [n/2, n)
+template <int N, bool F16>
 __device__ __forceinline__ void t3_st_split(uint32_t ta, const float* v) {
 #pragma unroll
   for (int c = 0; c < N / 16; ++c) {
     uint32_t hi[8], lo[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) split_pair(v[16 * c + 2 * i], v[16 * c + 2 * i + 1], hi[i], lo[i]);
+    for (int i = 0; i < 8; ++i) t3_split<F16>(v[16 * c + 2 * i], v[16 * c + 2 * i + 1], hi[i], lo[i]);
     tmem_st8(ta + 8 * c, hi);
     tmem_st8(ta + N / 2 + 8 * c, lo);
   }
 }
+template <bool F16>
 __device__ __forceinline__ void t3_split8_store(uint8_t* hi_dst, uint8_t* lo_dst, const float* v) {
   uint32_t h[4], l[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) split_pair(v[2 * i], v[2 * i + 1], h[i], l[i]);
+  for (int i = 0; i < 4; ++i) t3_split<F16>(v[2 * i], v[2 * i + 1], h[i], l[i]);
   *reinterpret_cast<uint4*>(hi_dst) = make_uint4(h[0], h[1], h[2], h[3]);
   *reinterpret_cast<uint4*>(lo_dst) = make_uint4(l[0], l[1], l[2], l[3]);
 }
@@ -147,6 +162,7 @@ __device__ __forceinline__ void t3_mma3(uint32_t d, uint32_t a_col, uint32_t a_l
   }
 }
 
+template <bool F16>
 __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     Params p, SkutImages3 img, NNCfg nn, Staged st, const int32_t* idx, int n, float* logits,
     float* pooled_out, SelFlags sel) {
@@ -366,14 +382,14 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
           for (int j = 0; j < kDModel; ++j) a[j] = 0.0f;
         }
 #pragma unroll
-        for (int j = 0; j < kDModel; ++j) an2 = fmaf(a[j], a[j], an2);
+        for (int j = 0; j < kDModel; ++j) an2 = fmaf(a[j], a[j], an2);  // the shift's max ||a_j||
         // one bf16 hi/lo split of a, stored twice: the M1 A operand (TMEM,
         // warp-collective: never under a divergent branch) and this row's K
         // (K-major smem slabs: chunk c of row r at c*(S_pad*16) + r*16)
         {
           uint32_t hi[32], lo[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) split_pair(a[2 * i], a[2 * i + 1], hi[i], lo[i]);
+          for (int i = 0; i < 32; ++i) t3_split<F16>(a[2 * i], a[2 * i + 1], hi[i], lo[i]);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             tmem_st8(cA + 8 * c, hi + 8 * c);
@@ -398,14 +414,14 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       if (issue_warp) {  // M1: [Q' | V'] = A [Wqk | Wvo]   (N = 128, K = 64)
         issuer_wait_simt();
         stamp(28);
-        t3_mma3<4>(R + kCD, R + kCA, 32, wa(L), wa(L) + kImg3WA / 2, 128 * 16, idesc_bf16(128, 128));
+        t3_mma3<4>(R + kCD, R + kCA, 32, wa(L), wa(L) + kImg3WA / 2, 128 * 16, t3_idesc<F16>(128, 128));
         commit_w(&t3.mma[t]);
       }
       stamp(4);
       // ---- P2: Q' -> A, V' -> smem (MN-major) ----
       wait_mma();
       stamp(5);
-      float qn2 = 0.0f;
+      float qn2 = 0.0f, s_rr = 0.0f;
       {
         float v[32];
 #pragma unroll
@@ -418,11 +434,27 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
           }
 #pragma unroll
           for (int i = 0; i < 32; ++i) qn2 = fmaf(v[i], v[i], qn2);
+          if (F16 && mapped) {  // s_rr = q'_r . a_r from this row's K (fp16 hi + lo parts)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int off = (4 * h + c) * (S_pad * 16) + r * 16;
+              const uint4 kh = *reinterpret_cast<const uint4*>(Khi + off);
+              const uint4 kl = *reinterpret_cast<const uint4*>(Klo + off);
+              const uint32_t khw[4] = {kh.x, kh.y, kh.z, kh.w}, klw[4] = {kl.x, kl.y, kl.z, kl.w};
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&khw[i]));
+                const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&klw[i]));
+                s_rr = fmaf(v[8 * c + 2 * i], a0.x + a1.x, s_rr);
+                s_rr = fmaf(v[8 * c + 2 * i + 1], a0.y + a1.y, s_rr);
+              }
+            }
+          }
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
             uint32_t hi[8], lo[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) split_pair(v[16 * c + 2 * i], v[16 * c + 2 * i + 1], hi[i], lo[i]);
+            for (int i = 0; i < 8; ++i) t3_split<F16>(v[16 * c + 2 * i], v[16 * c + 2 * i + 1], hi[i], lo[i]);
             tmem_st8(cA + 16 * h + 8 * c, hi);
             tmem_st8(cA + 32 + 16 * h + 8 * c, lo);
           }
@@ -439,7 +471,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               const int off = (r >> 3) * 1024 + (4 * h + c) * 128 + (r & 7) * 16;
-              t3_split8_store(Vhi + off, Vlo + off, v + 8 * c);
+              t3_split8_store<F16>(Vhi + off, Vlo + off, v + 8 * c);
             }
           }
         }
@@ -452,7 +484,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       if (issue_warp) {  // M2: S = Q' K^T   (N = keys of this tile, K = 64)
         mbar_wait(&t3.kvready, n_kv & 1);
         fence_after();
-        t3_mma3<4>(R + kCD, R + kCA, 32, khi, klo, S_pad * 16, idesc_bf16(128, NK));
+        t3_mma3<4>(R + kCD, R + kCA, 32, khi, klo, S_pad * 16, t3_idesc<F16>(128, NK));
         commit_w(&t3.mma[t]);
       }
       stamp(7);
@@ -464,21 +496,23 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       stamp(8);
       float inv_l = 0.0f;
       {
-        mbar_wait_sleep(&t3.kvready, n_kv & 1);  // kmax_s[L] complete (already passed)
-        stamp(24);
-        const float mb = sqrtf(qn2 * __uint_as_float(kmax_s[L]));
         const uint32_t cs = lanebase + kCD;
         const int nch = NK / 16;
         const int jlast = min(nch - 1, (rpw * kb + rpw - 1) / 16);  // warp-uniform causal bound
+        float mb;
+        mbar_wait_sleep(&t3.kvready, n_kv & 1);  // kmax_s[L] complete (already passed)
+        stamp(24);
+        mb = sqrtf(qn2 * __uint_as_float(kmax_s[L]));  // Cauchy-Schwarz: >= every score of the row
+        if constexpr (F16) {
+          // fp32 mode (fp16 P parts): shift by the row's own diagonal score
+          // where the bound allows, m' = max(s_rr, m_cs - 15): then P_rr = 1
+          // (no underflow of the largest P's in fp16) unless the bound
+          // overshoots the diagonal by > 15 binades, and always
+          // P <= 2^(m_cs - m') <= 2^15 < fp16 max (no overflow)
+          mb = ok ? fmaxf(s_rr, mb - 15.0f) : 0.0f;
+        }
         const float2 nmb = make_float2(-mb, -mb);
         float2 l2 = make_float2(0.f, 0.f);
-        // the causal chunks, one at a time with the next chunk's TMEM load in
-        // flight while this one is exponentiated (2-deep software pipeline)
-        uint32_t sa[16], sb[16];
-        tmem_ld16(cs, sa);
-        // key-validity word of the chunk pair, read one pair ahead (its
-        // shared-memory latency otherwise sits on every chunk's mask)
-        uint32_t vw_cur = valid_w[0];
         // p = exp2(s - m') for one 16-key chunk, masked keys -> 0 (MASK: the
         // warp has a causal-diagonal or invalid key in the chunk)
         auto chunk = [&](const uint32_t* cur, uint32_t vm, uint32_t tcol, auto mask) {
@@ -499,26 +533,39 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
           }
           uint32_t hi[8], lo[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) split_pair_t(pv[2 * i], pv[2 * i + 1], hi[i], lo[i]);
+          for (int i = 0; i < 8; ++i) {
+            if constexpr (F16) split_pair_h(pv[2 * i], pv[2 * i + 1], hi[i], lo[i]);
+            else split_pair_t(pv[2 * i], pv[2 * i + 1], hi[i], lo[i]);
+          }
           tmem_st8(tcol, hi);
           tmem_st8(tcol + 8, lo);
         };
-        for (int j = 0; j <= jlast; j += 2) {
-          const uint32_t vw_next = valid_w[min((j >> 1) + 1, 7)];
+        // the causal chunks, one at a time with the next chunk's TMEM load in
+        // flight while this one is exponentiated (2-deep software pipeline)
+        auto exp_pass = [&]() {
+          uint32_t sa[16], sb[16];
+          tmem_ld16(cs, sa);
+          // key-validity word of the chunk pair, read one pair ahead (its
+          // shared-memory latency otherwise sits on every chunk's mask)
+          uint32_t vw_cur = valid_w[0];
+          for (int j = 0; j <= jlast; j += 2) {
+            const uint32_t vw_next = valid_w[min((j >> 1) + 1, 7)];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int jj = j + u;
-            if (jj > jlast) break;
-            tmem_ld_wait();
-            uint32_t* cur = u == 0 ? sa : sb;
-            uint32_t* nxt = u == 0 ? sb : sa;
-            if (jj + 1 <= jlast) tmem_ld16(cs + 16 * (jj + 1), nxt);  // warp-uniform
-            const uint32_t vm = ok ? allowed16(vw_cur >> (u * 16), 16 * jj, r) : 0u;
-            // (a warp-uniform unmasked fast path measured 4% slower: code size)
-            chunk(cur, vm, cs + 16 * jj, std::true_type{});
+            for (int u = 0; u < 2; ++u) {
+              const int jj = j + u;
+              if (jj > jlast) break;
+              tmem_ld_wait();
+              uint32_t* cur = u == 0 ? sa : sb;
+              uint32_t* nxt = u == 0 ? sb : sa;
+              if (jj + 1 <= jlast) tmem_ld16(cs + 16 * (jj + 1), nxt);  // warp-uniform
+              const uint32_t vm = ok ? allowed16(vw_cur >> (u * 16), 16 * jj, r) : 0u;
+              // (a warp-uniform unmasked fast path measured 4% slower: code size)
+              chunk(cur, vm, cs + 16 * jj, std::true_type{});
+            }
+            vw_cur = vw_next;
           }
-          vw_cur = vw_next;
-        }
+        };
+        exp_pass();
         const int jz = jlast + 1;
         stamp(25);
         {  // chunks past the warp's causal bound: P = 0 (the P.V MMA reads all NK keys)
@@ -538,7 +585,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       if (issue_warp) {  // M3: O' = P V'   (N = 64, K = keys; V' MN-major)
         issuer_wait_simt();
         stamp(29);
-        const uint32_t id = idesc_bf16(128, 64, 0, 1);
+        const uint32_t id = t3_idesc<F16>(128, 64, 0, 1);
         const int nk16 = NK / 16;  // <= 12 (S_pad <= 192); unrolled, warp-uniform bound
 #pragma unroll
         for (int j = 0; j < 12; ++j) {
@@ -574,7 +621,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
 #pragma unroll
           for (int j = 0; j < kDModel; ++j) d[j] = 0.0f;
         }
-        t3_st_split<64>(cA, d);
+        t3_st_split<64, F16>(cA, d);
         tmem_st_wait();
         done();
       }
@@ -582,7 +629,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       if (issue_warp) {  // M4: H = A W1   (N = 32, K = 64)
         issuer_wait_simt();
         stamp(30);
-        t3_mma3<4>(R + kCD, R + kCA, 32, wb(L), wb(L) + 4096, 32 * 16, idesc_bf16(128, 32));
+        t3_mma3<4>(R + kCD, R + kCA, 32, wb(L), wb(L) + 4096, 32 * 16, t3_idesc<F16>(128, 32));
         commit_w(&t3.mma[t]);
       }
       stamp(13);
@@ -595,14 +642,14 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < kFfn; ++j) h[j] = ok ? fmaxf(h[j], 0.0f) : 0.0f;
-        t3_st_split<32>(lanebase + kCA2, h);
+        t3_st_split<32, F16>(lanebase + kCA2, h);
         tmem_st_wait();
         done();
       }
       stamp(15);
       if (issue_warp) {  // M5: D2 = ReLU(H) W2   (N = 64, K = 32)
         issuer_wait_simt();
-        t3_mma3<2>(R + kCW2, R + kCA2, 16, wb(L) + 8192, wb(L) + 8192 + 4096, 64 * 16, idesc_bf16(128, 64));
+        t3_mma3<2>(R + kCW2, R + kCA2, 16, wb(L) + 8192, wb(L) + 8192 + 4096, 64 * 16, t3_idesc<F16>(128, 64));
         commit_w(&t3.mma[t]);
       }
       stamp(16);
@@ -625,14 +672,14 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     }
 
     // ---- K5: y = x out_linear, masked max over rows, CTR head ----
-    t3_st_split<64>(cA, x);  // invalid rows carry x = 0
+    t3_st_split<64, F16>(cA, x);  // invalid rows carry x = 0
     tmem_st_wait();
     done();
     stamp(19);
     if (issue_warp) {
       issuer_wait_simt();
       t3_mma3<4>(R + kCD, R + kCA, 32, wsm + NL * kW3Layer, wsm + NL * kW3Layer + 8192, 64 * 16,
-                 idesc_bf16(128, 64));
+                 t3_idesc<F16>(128, 64));
       commit_w(&t3.mma[t]);
     }
     stamp(20);
@@ -715,16 +762,17 @@ bool skut_tc3_supported(const NNCfg& nn, const Params& p) {
 }
 
 cudaError_t launch_skut_tc3(const Params& p, const SkutImages3& img, const NNCfg& nn, const Staged& st,
-                            const int32_t* idx, int n, float* logits, float* pooled, SelFlags sel,
+                            const int32_t* idx, int n, float* logits, float* pooled, SelFlags sel, bool f16,
                             cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const int S_pad = (nn.seq_len + 15) & ~15;
   const size_t smem = (size_t)p.num_layers * kW3Layer + kImg3WO + 4 * (size_t)S_pad * 128;
-  cudaError_t e = set_max_dyn_smem((const void*)skut_tc3_kernel, (int)smem);
+  auto kern = f16 ? skut_tc3_kernel<true> : skut_tc3_kernel<false>;
+  cudaError_t e = set_max_dyn_smem((const void*)kern, (int)smem);
   if (e != cudaSuccess) return e;
   const int sms = device_sms();
-  return launch_pdl(skut_tc3_kernel, dim3(n < sms ? n : sms), dim3(kT3Threads), smem, s, p, img, nn, st, idx, n,
-                    logits, pooled, sel);
+  return launch_pdl(kern, dim3(n < sms ? n : sms), dim3(kT3Threads), smem, s, p, img, nn, st, idx, n, logits,
+                    pooled, sel);
 }
 
 }  // namespace tav2

@@ -16,6 +16,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "tav2_common.cuh"
 
 using namespace tav2;
@@ -152,7 +154,8 @@ struct tav2_ctx {
   uint8_t* d_images = nullptr;  // bf16x3 weight images (tensor-core SKUT)
   SkutImages images{};
   uint8_t* d_images3 = nullptr;  // folded images of skut_tc3 (Wqk, Wvo)
-  SkutImages3 images3{};
+  SkutImages3 images3{};   // bf16x3 parts
+  SkutImages3 images3h{};  // fp16x3 parts (fp32 mode)
   bool params_ok = false;
   // Cauchy-Schwarz softmax shift range (tensor-core SKUTs): exponents stay
   // >= -2 m' with m' <= cs_bound*; usable while 2 m' <= 120 (ex2 range)
@@ -530,14 +533,19 @@ int tav2_load_params(tav2_ctx* c, int n, const char* const* names, const float* 
     memcpy(&f, &u, 4);
     return f;
   };
+  // fp16 (IEEE binary16, round-to-nearest-even, subnormals kept) parts of
+  // the fp16x3 images (skut_tc3 in fp32 mode)
+  auto f16 = [](float x) -> uint16_t { return __half_as_ushort(__float2half_rn(x)); };
+  auto f16f = [](uint16_t h) { return __half2float(__ushort_as_half(h)); };
+  bool put_f16 = false;  // the format `put` writes
   // write W^T of an [in, out] matrix into a (N = n_total, K) slab image at row offset n0
   auto put = [&](uint8_t* base, int n_total, int K, int n0, const float* W, int in, int out) {
     uint8_t* lo_base = base + (size_t)n_total * K * 2;
     for (int k = 0; k < in; ++k)
       for (int n = 0; n < out; ++n) {
         const float w = W[k * out + n];
-        const uint16_t hi = bf16(w);
-        const uint16_t lo = bf16(w - bf16f(hi));
+        const uint16_t hi = put_f16 ? f16(w) : bf16(w);
+        const uint16_t lo = put_f16 ? f16(w - f16f(hi)) : bf16(w - bf16f(hi));
         const size_t off = (size_t)(k / 8) * (n_total * 16) + (size_t)(n0 + n) * 16 + (k % 8) * 2;
         memcpy(base + off, &hi, 2);
         memcpy(lo_base + off, &lo, 2);
@@ -571,7 +579,7 @@ int tav2_load_params(tav2_ctx* c, int n, const char* const* names, const float* 
   {
     const size_t lay = (size_t)kImg3WA + kImg3WB;
     const size_t bytes3 = (size_t)L * lay + kImg3WO;
-    std::vector<uint8_t> img3(bytes3, 0);
+    std::vector<uint8_t> img3(bytes3, 0), img3h(bytes3, 0);
     std::vector<float> wqk(64 * 64), wvo(64 * 64);
     const double sc = 1.4426950408889634 / 8.0;
     for (int l = 0; l < L; ++l) {
@@ -606,19 +614,31 @@ int tav2_load_params(tav2_ctx* c, int n, const char* const* names, const float* 
         c->cs_bound3 = std::max(c->cs_bound3, spectral_norm64(m1) * A * A);
         c->cs_bound = std::max(c->cs_bound, spectral_norm64(m2) * spectral_norm64(m3) * sc * A * A);
       }
-      uint8_t* base = img3.data() + (size_t)l * lay;
-      put(base, 128, 64, 0, wqk.data(), 64, 64);
-      put(base, 128, 64, 64, wvo.data(), 64, 64);
-      put(base + kImg3WA, 32, 64, 0, host_of(P.w1[l]), 64, 32);
-      put(base + kImg3WA + 8192, 64, 32, 0, host_of(P.w2[l]), 32, 64);
+      for (int h16 = 0; h16 < 2; ++h16) {  // bf16x3 (bf16 mode) and fp16x3 (fp32 mode) images
+        put_f16 = h16 != 0;
+        uint8_t* base = (h16 ? img3h : img3).data() + (size_t)l * lay;
+        put(base, 128, 64, 0, wqk.data(), 64, 64);
+        put(base, 128, 64, 64, wvo.data(), 64, 64);
+        put(base + kImg3WA, 32, 64, 0, host_of(P.w1[l]), 64, 32);
+        put(base + kImg3WA + 8192, 64, 32, 0, host_of(P.w2[l]), 32, 64);
+      }
     }
-    put(img3.data() + (size_t)L * lay, 64, 64, 0, host_of(P.out_linear), 64, 64);
+    for (int h16 = 0; h16 < 2; ++h16) {
+      put_f16 = h16 != 0;
+      put((h16 ? img3h : img3).data() + (size_t)L * lay, 64, 64, 0, host_of(P.out_linear), 64, 64);
+    }
+    put_f16 = false;
     if (c->d_images3) cudaFree(c->d_images3);
     c->d_images3 = nullptr;
-    CU(cudaMalloc(&c->d_images3, bytes3));
+    CU(cudaMalloc(&c->d_images3, 2 * bytes3));
     CU(cudaMemcpy(c->d_images3, img3.data(), bytes3, cudaMemcpyHostToDevice));
-    for (int l = 0; l < L; ++l) c->images3.w[l] = c->d_images3 + (size_t)l * lay;
+    CU(cudaMemcpy(c->d_images3 + bytes3, img3h.data(), bytes3, cudaMemcpyHostToDevice));
+    for (int l = 0; l < L; ++l) {
+      c->images3.w[l] = c->d_images3 + (size_t)l * lay;
+      c->images3h.w[l] = c->d_images3 + bytes3 + (size_t)l * lay;
+    }
     c->images3.wout = c->d_images3 + (size_t)L * lay;
+    c->images3h.wout = c->d_images3 + bytes3 + (size_t)L * lay;
   }
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);  // captured with the old parameters
   c->graphs.clear();
@@ -999,9 +1019,13 @@ int run_score(tav2_ctx* c, int mode, const int32_t* idx, float* logits, float* p
   // tensor-core SKUTs only while their single-pass softmax shift provably
   // stays in the exp2 range (2 m' <= 120); the SIMT kernel keeps a running max
   const bool tc3_ok = c->cs_bound3 <= 60.0, tc_ok = c->cs_bound <= 60.0;
-  if (mode == TAV2_MODE_BF16 && tc3_ok && skut_tc3_supported(c->nn, c->params)) {
-    CU(timed(c, "skut_tc3", s, [&] {
-      return launch_skut_tc3(c->params, c->images3, c->nn, st, idx, st.n_items, logits, pooled, sel, s);
+  // S <= 192: the folded tensor-core SKUT -- bf16x3 parts in bf16 mode;
+  // fp16x3 parts with a true-max softmax in fp32 mode (logits within 1e-5)
+  if (tc3_ok && skut_tc3_supported(c->nn, c->params)) {
+    const bool f16 = mode == TAV2_MODE_FP32;
+    CU(timed(c, f16 ? "skut_tc3_f16" : "skut_tc3", s, [&] {
+      return launch_skut_tc3(c->params, f16 ? c->images3h : c->images3, c->nn, st, idx, st.n_items, logits, pooled,
+                             sel, f16, s);
     }));
     return TAV2_OK;
   }
