@@ -754,6 +754,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   cta_stamp(kDbgSkut, 1);
 }
 
+cudaError_t set_dbg_cta_skut3(long long* dev) { return set_dbg_cta_tu(dev); }
+
 cudaError_t set_debug_skut3(long long* dev) { return cudaMemcpyToSymbol(g_dbg_skut3, &dev, sizeof(dev)); }
 
 bool skut_tc3_supported(const NNCfg& nn, const Params& p) {

@@ -1292,7 +1292,8 @@ int tav2_debug_timeline(long long* dev, int block) {
 
 int tav2_debug_cta(long long* dev) {
   if (set_dbg_cta_prep(dev) != cudaSuccess || set_dbg_cta_scan(dev) != cudaSuccess ||
-      set_dbg_cta_select(dev) != cudaSuccess || set_dbg_cta_skut(dev) != cudaSuccess)
+      set_dbg_cta_select(dev) != cudaSuccess || set_dbg_cta_skut(dev) != cudaSuccess ||
+      set_dbg_cta_skut3(dev) != cudaSuccess)
     return fail(TAV2_ECUDA, "debug cta stamps");
   return TAV2_OK;
 }

@@ -276,6 +276,7 @@ cudaError_t set_dbg_cta_prep(long long* dev);
 cudaError_t set_dbg_cta_scan(long long* dev);
 cudaError_t set_dbg_cta_select(long long* dev);
 cudaError_t set_dbg_cta_skut(long long* dev);
+cudaError_t set_dbg_cta_skut3(long long* dev);
 bool make_rows32_map(CUtensorMap* map, const void* base, int64_t rows, int box_rows);
 cudaError_t launch_encode(const Staged& st, const NNCfg& nn, const Params& p, const int32_t* idx,
                           float* F, uint8_t* mask, cudaStream_t s);

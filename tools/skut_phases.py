@@ -24,7 +24,7 @@ n_cand = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
 nn = P.NNConfig()
 model = P.RankingModel.init(P.ModelConfig.for_nn(nn), seed=0)
 eng = Engine(model, capacity=Capacity(1, n_cand, 16896))
-r = P.generate_requests(1, n_cand, 16384, seed=1)[0]
+r = P.synthetic_requests(1, n_cand, 16384, 256, 256, seed=0)[0]
 eng.stage([(r.user, r.candidates, r.ctx)])
 logits = torch.empty((n_cand, 4), device="cuda")
 for _ in range(3):
