@@ -290,8 +290,13 @@ def run_gpu(args, rank, world, local_rank):
     from paper_2506_02267_b200.runtime import Capacity, Engine
     from paper_2506_02267_b200.serving import nearest_rank
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    shared = getattr(args, "share_gpu", False)
+    dev_i = local_rank % torch.cuda.device_count() if shared else local_rank
+    torch.cuda.set_device(dev_i)
+    dev = torch.device("cuda", dev_i)
+
+    def coll(t):  # gloo (--share-gpu) reduces host copies; NCCL the device tensor
+        return t.cpu() if shared else t
     n_req, n_cand, L, nn_t = CONFIGS[args.config]
     split = args.config == "c4"  # candidate split of one request (parallel.rank_split's layout)
     n_total = n_cand
@@ -304,7 +309,7 @@ def run_gpu(args, rank, world, local_rank):
     nn = P.NNConfig(*nn_t)
     model = P.RankingModel.init(P.ModelConfig.for_nn(nn), seed=0)
     cap = Capacity(n_req, n_req * n_total, n_req * (L + 512))
-    eng = Engine(model, capacity=cap, device=local_rank)
+    eng = Engine(model, capacity=cap, device=dev_i)
     # a pool of distinct requests per rank (different seeds per rank); the
     # candidate split shares one request across the ranks
     pool_n = max(2, args.pool)
@@ -331,7 +336,12 @@ def run_gpu(args, rank, world, local_rank):
     def step():
         if gather:
             eng.run_staged(mode, send[:n_cand])
-            dist.all_gather_into_tensor(recv, send)
+            if shared:
+                r_h = torch.empty((world * width, 4), dtype=torch.float32)
+                dist.all_gather_into_tensor(r_h, send.cpu())
+                recv.copy_(r_h)
+            else:
+                dist.all_gather_into_tensor(recv, send)
         else:
             eng.run_staged(mode, logits)
 
@@ -348,7 +358,7 @@ def run_gpu(args, rank, world, local_rank):
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     barrier()
     torch.cuda.synchronize()
-    with Clocks(local_rank) as clk:
+    with Clocks(dev_i) as clk:
         for i in range(args.steps):
             flush.fill_(float(i))  # evict the previous step's working set from L2 (untimed)
             starts[i].record()
@@ -371,7 +381,7 @@ def run_gpu(args, rank, world, local_rank):
     prof_ms = sum(v[0] for v in kt.values()) / n_prof
     eng.set_profiling(False)
     dev_ms = sum(step_ms)
-    t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+    t = coll(torch.tensor([dev_ms], dtype=torch.float64, device=dev))
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
@@ -391,7 +401,7 @@ def run_gpu(args, rank, world, local_rank):
     t0 = time.perf_counter()
     eng.rank_pipelined([packed[i % pool_n] for i in range(args.steps)], mode=mode, latencies=lat)
     e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    te = coll(torch.tensor([e2e_s], dtype=torch.float64, device=dev))
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = job_cand * args.steps / float(te.item())
@@ -626,6 +636,8 @@ def main():
     ap.add_argument("--pool", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dry-run", action="store_true", help="CPU stand-in ranks over gloo (launcher test)")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="validation only: N ranks on fewer GPUs (gloo, host-side collectives); not a scaling number")
     args = ap.parse_args()
     launched = "WORLD_SIZE" in os.environ
     if args.gpus > 1 and not launched and args.impl == "ours":
@@ -666,15 +678,17 @@ def main():
     import torch.distributed as dist
 
     if world > 1:
-        dist.init_process_group("gloo" if args.dry_run else "nccl", init_method="env://")
+        dist.init_process_group("gloo" if args.dry_run or args.share_gpu else "nccl", init_method="env://")
     if args.dry_run:
         out = run_dry(args, rank, world)
     else:
         import torch
 
-        if torch.cuda.device_count() < world:
+        if torch.cuda.device_count() < world and not args.share_gpu:
             raise SystemExit(f"bench: {world} ranks but only {torch.cuda.device_count()} visible GPU(s)")
         out = run_gpu(args, rank, world, local_rank)
+        if args.share_gpu:
+            out["shared_gpu"] = f"{world} ranks on {torch.cuda.device_count()} GPU(s): code-path validation, not scaling"
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             cb = cpu_baseline(args.config, steps=2, warmup=1, budget_s=15.0)
             out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
