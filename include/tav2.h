@@ -125,6 +125,15 @@ int tav2_encode(tav2_ctx* ctx, const int32_t* idx_dev, float* features_dev, uint
 int tav2_forward(tav2_ctx* ctx, int mode, const float* features_dev, const uint8_t* mask_dev,
                  int32_t n, float* u_dev, void* stream);
 
+/* forward_fused(..., extra_mask) (encoder.py:314-462, :366-377): as
+ * tav2_forward, with a custom attention mask ANDed into causal & key-valid
+ * (NAL training masks; not on the serving path).  extra_dev [seq_len,
+ * seq_len] u8 shared by the batch (extra_batched = 0) or [n, seq_len,
+ * seq_len] (extra_batched = 1); a row with no allowed key gets a zero
+ * attention output.  extra_dev == NULL is tav2_forward. */
+int tav2_forward_masked(tav2_ctx* ctx, int mode, const float* features_dev, const uint8_t* mask_dev,
+                        const uint8_t* extra_dev, int32_t extra_batched, int32_t n, float* u_dev, void* stream);
+
 /* Fused K3+K4+K5 on the staged batch: gather + Eq. 4 encode + SKUT + pool +
  * CTR head (trainer.py:345-366).  logits_dev [n_items, 4] f32 (pre-sigmoid);
  * pooled_dev (nullable) [n_items, 64] f32. */

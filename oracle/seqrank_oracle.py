@@ -261,10 +261,12 @@ def forward_layered(F, mask, P):
     return x
 
 
-def forward_fused(F, mask, P, tile=64):
-    """encoder.py:314-462 -- tiled online-softmax single-pass forward
-    (no extra_mask: the serving path never passes one).  Same operation
-    order as the reference so CPU timing is representative."""
+def forward_fused(F, mask, P, tile=64, extra_mask=None):
+    """encoder.py:314-462 -- tiled online-softmax single-pass forward.  Same
+    operation order as the reference so CPU timing is representative.
+    extra_mask ([S, S] or [B, S, S] bool, encoder.py:366-377): key j allowed
+    for row i only where set, on top of causal & key-valid; a row with no
+    allowed key gets a zero attention output (row_any)."""
     B, S, d = F.shape
     dtype = F.dtype
     neg = np.float32(-1e30) if dtype == np.float32 else np.float64(-1e300)
@@ -273,7 +275,13 @@ def forward_fused(F, mask, P, tile=64):
     x = np.array(F)
     a_in = np.empty_like(x)
     invalid = ~mask
-    row_any = np.maximum.accumulate(mask.astype(dtype), axis=1)  # :379-381
+    bad = None
+    if extra_mask is not None:  # :366-377
+        em = np.broadcast_to(np.asarray(extra_mask, bool), (B, S, S))
+        bad = ~em | np.triu(np.ones((S, S), bool), 1)[None] | invalid[:, None, :]
+        row_any = (~bad.all(-1)).astype(dtype)
+    else:
+        row_any = np.maximum.accumulate(mask.astype(dtype), axis=1)  # :379-381
     triu = np.triu(np.ones((tile, tile), bool), 1)
     nt = (S + tile - 1) // tile
     for L in _layers(P):
@@ -293,9 +301,12 @@ def forward_fused(F, mask, P, tile=64):
                 k = a_in[:, ks:ke] @ L["wk"]
                 v = a_in[:, ks:ke] @ L["wv"]
                 s = (q @ k.transpose(0, 2, 1)) * scale
-                s = np.where(invalid[:, None, ks:ke], neg, s)
-                if kj == qi:
-                    s = np.where(triu[:tq, :tk], neg, s)
+                if bad is not None:  # :418-419
+                    s = np.where(bad[:, qs:qe, ks:ke], neg, s)
+                else:
+                    s = np.where(invalid[:, None, ks:ke], neg, s)
+                    if kj == qi:
+                        s = np.where(triu[:tq, :tk], neg, s)
                 mn = np.maximum(s.max(-1), m)
                 al = np.exp(m - mn)
                 m = mn

@@ -32,7 +32,7 @@ EXPORTS = (
     "tav2_kernel_times", "tav2_tc_selftest", "tav2_debug_timeline", "tav2_debug_cta",
     "tav2_rank_submit", "tav2_rank_collect",
     "tav2_store_reserve", "tav2_store_put", "tav2_store_remove", "tav2_store_count",
-    "tav2_similarity", "tav2_pool", "tav2_rank_wait", "tav2_graph_info",
+    "tav2_similarity", "tav2_pool", "tav2_rank_wait", "tav2_graph_info", "tav2_forward_masked",
 )
 
 
@@ -92,6 +92,7 @@ def lib() -> ctypes.CDLL:
             L.tav2_similarity.argtypes = [vp, i32, i32, vp, vp]
             L.tav2_pool.argtypes = [vp, vp, vp, i32, vp, vp]
             L.tav2_forward.argtypes = [vp, ctypes.c_int, vp, vp, i32, vp, vp]
+            L.tav2_forward_masked.argtypes = [vp, ctypes.c_int, vp, vp, vp, i32, i32, vp, vp]
             L.tav2_score.argtypes = [vp, ctypes.c_int, vp, vp, vp, vp]
             L.tav2_rank.argtypes = [vp, ctypes.POINTER(Request), ctypes.c_int, ctypes.c_int, vp, vp,
                                     vp]

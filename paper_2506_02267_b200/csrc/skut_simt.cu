@@ -107,7 +107,8 @@ cudaError_t launch_encode(const Staged& st, const NNCfg& nn, const Params& p, co
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kSkutThreads, 1) skut_simt_kernel(
     Params p, NNCfg nn, Staged st, int use_staged, const int32_t* idx, const float* Fin,
-    const uint8_t* fmask, int n, float* scratch, float* U, float* logits, float* pooled_out, int cs_shift) {
+    const uint8_t* fmask, int n, float* scratch, float* U, float* logits, float* pooled_out, int cs_shift,
+    const uint8_t* extra, long long extra_stride) {
   __shared__ unsigned kmax_s;  // max_j ||k_j||^2 of the layer (single-pass shift)
   extern __shared__ __align__(16) float sm[];
   const int S = nn.seq_len;
@@ -173,6 +174,9 @@ __global__ void __launch_bounds__(kSkutThreads, 1) skut_simt_kernel(
         if (rmax < 0) continue;
         float q[kDModel], acc[kDModel];
         if (mine) load64(Q + r * kDModel, q);
+        // encoder.py:366-377 custom mask (extra_mask, NAL training): key j is
+        // allowed for row r only where extra[r, j] is set (2-D: shared)
+        const uint8_t* xrow = (extra && mine) ? extra + (size_t)item * extra_stride + (size_t)r * S : nullptr;
 #pragma unroll
         for (int j = 0; j < kDModel; ++j) acc[j] = 0.0f;
         float l = 0.0f;
@@ -198,7 +202,7 @@ __global__ void __launch_bounds__(kSkutThreads, 1) skut_simt_kernel(
               sdot = fmaf(q[4 * e + 2], kv.z, sdot);
               sdot = fmaf(q[4 * e + 3], kv.w, sdot);
             }
-            const float pj = (mine && j <= r) ? expf(sdot * 0.125f - mb) : 0.0f;
+            const float pj = (mine && j <= r && (!xrow || xrow[j])) ? expf(sdot * 0.125f - mb) : 0.0f;
             l += pj;
             const float4* vr = reinterpret_cast<const float4*>(Vs + j * kDModel);
 #pragma unroll
@@ -224,7 +228,7 @@ __global__ void __launch_bounds__(kSkutThreads, 1) skut_simt_kernel(
               sdot = fmaf(q[4 * e + 2], kv.z, sdot);
               sdot = fmaf(q[4 * e + 3], kv.w, sdot);
             }
-            const bool use = mine && j <= r;
+            const bool use = mine && j <= r && (!xrow || xrow[j]);
             const float sc = sdot * 0.125f;  // 1/sqrt(64)
             const float mn = use ? fmaxf(m, sc) : m;
             const float alpha = use ? expf(m - mn) : 1.0f;
@@ -243,8 +247,9 @@ __global__ void __launch_bounds__(kSkutThreads, 1) skut_simt_kernel(
           }
         }
         if (!mine) continue;
-        // row r is a valid key of itself, so l > 0 and row_any = 1
-        const float inv = 1.0f / l;
+        // row r is a valid key of itself, so l > 0 and row_any = 1 -- unless
+        // an extra mask disallows every key: zero attention output (:379-381)
+        const float inv = l > 0.0f ? 1.0f / l : 0.0f;
 #pragma unroll
         for (int j = 0; j < kDModel; ++j) acc[j] *= inv;
         float x[kDModel], t[kDModel];
@@ -343,7 +348,7 @@ size_t skut_simt_scratch_floats(int seq_len) { return (size_t)2 * seq_len * kDMo
 cudaError_t launch_skut_simt(const Params& p, const NNCfg& nn, const Staged* st,
                              const int32_t* idx, const float* F, const uint8_t* fmask, int n,
                              float* scratch, float* U, float* logits, float* pooled, int cs_shift,
-                             cudaStream_t s) {
+                             cudaStream_t s, const uint8_t* extra, long long extra_stride) {
   if (n == 0) return cudaSuccess;
   const int S = nn.seq_len;
   size_t smem = (size_t)(2 * S * kDModel + kSkutWarps * kDModel + 112 + kHidden) * 4 + kMaxSeq * 4;
@@ -351,7 +356,8 @@ cudaError_t launch_skut_simt(const Params& p, const NNCfg& nn, const Staged* st,
   if (e != cudaSuccess) return e;
   Staged dummy{};
   skut_simt_kernel<<<skut_simt_grid(n), kSkutThreads, smem, s>>>(
-      p, nn, st ? *st : dummy, st != nullptr, idx, F, fmask, n, scratch, U, logits, pooled, cs_shift);
+      p, nn, st ? *st : dummy, st != nullptr, idx, F, fmask, n, scratch, U, logits, pooled, cs_shift, extra,
+      extra_stride);
   return cudaGetLastError();
 }
 

@@ -129,6 +129,13 @@ struct tav2_ctx {
 
   int32_t* idx = nullptr;
   float* logits = nullptr;
+  // tav2_rank_submit: per-slot index / logit buffers, so the result copies
+  // of one request (on d2h_stream, after ev_comp[slot]) overlap the next
+  // request's kernels on the compute stream instead of sitting between them
+  int32_t* idx_s[kStageSlots] = {nullptr, nullptr};
+  float* logits_s[kStageSlots] = {nullptr, nullptr};
+  cudaEvent_t ev_comp[kStageSlots] = {nullptr, nullptr};
+  cudaStream_t d2h_stream = nullptr;
   uint32_t* sel_done = nullptr;  // per-(candidate, source) select flags (SelFlags)
   uint32_t* sel_epoch = nullptr; // device word: the current run's flag epoch (prep bumps it)
   // CUDA graphs of the launch chain prep .. SKUT (run_chain): one per
@@ -137,6 +144,7 @@ struct tav2_ctx {
   struct GraphEntry {
     int slot, mode;
     const float* logits;
+    const int32_t* idx;
     Plan plan;
     cudaGraphExec_t exec;
     int launches;
@@ -262,8 +270,12 @@ int free_all(tav2_ctx* c) {
     cudaFreeHost(c->h_idx[k]);
     if (c->ev_staged[k]) cudaEventDestroy(c->ev_staged[k]);
     if (c->ev_done[k]) cudaEventDestroy(c->ev_done[k]);
+    if (c->ev_comp[k]) cudaEventDestroy(c->ev_comp[k]);
+    cudaFree(c->idx_s[k]);
+    cudaFree(c->logits_s[k]);
   }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
   cudaFree(c->st_emb);
   cudaFree(c->st_act);
   cudaFree(c->st_surf);
@@ -396,6 +408,7 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
     if ((e = cudaMallocHost(&c->h_idx[k], (size_t)N * S * 4)) != cudaSuccess) return bad(e, "pinned indices");
     if ((e = cudaEventCreateWithFlags(&c->ev_staged[k], cudaEventDisableTiming)) != cudaSuccess) return bad(e, "event");
     if ((e = cudaEventCreateWithFlags(&c->ev_done[k], cudaEventDisableTiming)) != cudaSuccess) return bad(e, "event");
+    if ((e = cudaEventCreateWithFlags(&c->ev_comp[k], cudaEventDisableTiming)) != cudaSuccess) return bad(e, "event");
   }
   if ((e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking)) != cudaSuccess)
     return bad(e, "copy stream");
@@ -429,6 +442,12 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
   if ((e = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking)) != cudaSuccess)
     return bad(e, "capture stream");
   if ((e = cudaMalloc(&c->logits, (size_t)N * kHeads * 4)) != cudaSuccess) return bad(e, "logits");
+  for (int k = 0; k < tav2_ctx::kStageSlots; ++k) {
+    if ((e = cudaMalloc(&c->idx_s[k], (size_t)N * S * 4)) != cudaSuccess) return bad(e, "slot idx");
+    if ((e = cudaMalloc(&c->logits_s[k], (size_t)N * kHeads * 4)) != cudaSuccess) return bad(e, "slot logits");
+  }
+  if ((e = cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return bad(e, "d2h stream");
   {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -1068,12 +1087,12 @@ bool same_plan(const Plan& a, const Plan& b) {  // field by field (no padding by
 // the plan, the mode and the output buffer -- the flag epoch lives in
 // device memory), so a repeated shape costs one cudaGraphLaunch instead of
 // six launches.  Profiling (per-kernel events) launches directly.
-int run_chain(tav2_ctx* c, int mode, float* logits, cudaStream_t s) {
+int run_chain(tav2_ctx* c, int mode, float* logits, int32_t* idx, cudaStream_t s) {
   const SelFlags sel = next_sel(c);
   const Plan& pl = c->plans[c->cur];
   if (!c->profiling && graphs_enabled() && !c->graph_broken) {
     for (auto& g : c->graphs) {
-      if (g.slot == c->cur && g.mode == mode && g.logits == logits && same_plan(g.plan, pl)) {
+      if (g.slot == c->cur && g.mode == mode && g.logits == logits && g.idx == idx && same_plan(g.plan, pl)) {
         g.last_use = ++c->graph_tick;
         c->launches = g.launches;
         CU(cudaGraphLaunch(g.exec, s));
@@ -1088,8 +1107,8 @@ int run_chain(tav2_ctx* c, int mode, float* logits, cudaStream_t s) {
       c->launches = 0;
       int rc = TAV2_OK;
       if (cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
-        rc = run_nn(c, c->idx, nullptr, c->cap_stream, sel);
-        if (!rc) rc = run_score(c, mode, c->idx, logits, nullptr, c->cap_stream, sel);
+        rc = run_nn(c, idx, nullptr, c->cap_stream, sel);
+        if (!rc) rc = run_score(c, mode, idx, logits, nullptr, c->cap_stream, sel);
         const cudaError_t e = cudaStreamEndCapture(c->cap_stream, &graph);
         if (!rc && e == cudaSuccess && graph && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
           if (c->graphs.size() >= 8) {  // evict the least recently used
@@ -1099,7 +1118,7 @@ int run_chain(tav2_ctx* c, int mode, float* logits, cudaStream_t s) {
             cudaGraphExecDestroy(lru->exec);
             c->graphs.erase(lru);
           }
-          c->graphs.push_back({c->cur, mode, logits, pl, exec, c->launches, ++c->graph_tick});
+          c->graphs.push_back({c->cur, mode, logits, idx, pl, exec, c->launches, ++c->graph_tick});
           if (graph) cudaGraphDestroy(graph);
           CU(cudaGraphLaunch(exec, s));
           return TAV2_OK;
@@ -1114,8 +1133,8 @@ int run_chain(tav2_ctx* c, int mode, float* logits, cudaStream_t s) {
     }
   }
   c->launches = 0;
-  int rc = run_nn(c, c->idx, nullptr, s, sel);
-  if (!rc) rc = run_score(c, mode, c->idx, logits, nullptr, s, sel);
+  int rc = run_nn(c, idx, nullptr, s, sel);
+  if (!rc) rc = run_score(c, mode, idx, logits, nullptr, s, sel);
   return rc;
 }
 
@@ -1197,6 +1216,26 @@ int tav2_forward(tav2_ctx* c, int mode, const float* features_dev, const uint8_t
   return TAV2_OK;
 }
 
+int tav2_forward_masked(tav2_ctx* c, int mode, const float* features_dev, const uint8_t* mask_dev,
+                        const uint8_t* extra_dev, int32_t extra_batched, int32_t n, float* u_dev, void* stream) {
+  if (!extra_dev) return tav2_forward(c, mode, features_dev, mask_dev, n, u_dev, stream);
+  if (!c) return fail(TAV2_EINVAL, "null context");
+  if (!c->params_ok) return fail(TAV2_ESTATE, "parameters not loaded");
+  if (mode != TAV2_MODE_FP32 && mode != TAV2_MODE_BF16)
+    return fail(TAV2_EINVAL, "unknown precision mode %d", mode);
+  if (n < 0) return fail(TAV2_EINVAL, "negative batch");
+  if (n == 0) return TAV2_OK;
+  if (!features_dev || !mask_dev || !u_dev) return fail(TAV2_EINVAL, "null device pointer");
+  CU(cudaSetDevice(c->device));
+  // f32 SIMT transformer with the running-max softmax (the custom mask may
+  // drop a row's own key, so the diagonal-based shifts do not apply); it
+  // meets both modes' tolerances
+  const long long S = c->nn.seq_len;
+  CU(launch_skut_simt(c->params, c->nn, nullptr, nullptr, features_dev, mask_dev, n, c->skut_scratch, u_dev,
+                      nullptr, nullptr, 0, (cudaStream_t)stream, extra_dev, extra_batched ? S * S : 0));
+  return TAV2_OK;
+}
+
 int tav2_score(tav2_ctx* c, int mode, const int32_t* idx_dev, float* logits_dev, float* pooled_dev,
                void* stream) {
   int rc = check_ready(c, mode);
@@ -1215,7 +1254,7 @@ int tav2_run_staged(tav2_ctx* c, int mode, float* logits_dev, void* stream) {
   if (rc) return rc;
   CU(cudaSetDevice(c->device));
   cudaStream_t s = (cudaStream_t)stream;
-  if ((rc = run_chain(c, mode, logits_dev ? logits_dev : c->logits, s))) return rc;
+  if ((rc = run_chain(c, mode, logits_dev ? logits_dev : c->logits, c->idx, s))) return rc;
   return mark_used(c, s);
 }
 
@@ -1229,13 +1268,19 @@ int tav2_rank_submit(tav2_ctx* c, const tav2_request* reqs, int n_req, int mode,
   int rc = tav2_stage(c, reqs, n_req, stream, &n);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  if ((rc = run_chain(c, mode, c->logits, s))) return rc;
-  CU(cudaMemcpyAsync(c->h_out[slot], c->logits, (size_t)n * kHeads * 4, cudaMemcpyDeviceToHost, s));
+  if ((rc = run_chain(c, mode, c->logits_s[slot], c->idx_s[slot], s))) return rc;
+  // result copies on the d2h stream: the compute stream goes straight on to
+  // the next request's kernels
+  CU(cudaEventRecord(c->ev_comp[slot], s));
+  CU(cudaStreamWaitEvent(c->d2h_stream, c->ev_comp[slot], 0));
+  CU(cudaMemcpyAsync(c->h_out[slot], c->logits_s[slot], (size_t)n * kHeads * 4, cudaMemcpyDeviceToHost,
+                     c->d2h_stream));
   if (want_idx)
-    CU(cudaMemcpyAsync(c->h_idx[slot], c->idx, (size_t)n * c->nn.seq_len * 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(c->h_idx[slot], c->idx_s[slot], (size_t)n * c->nn.seq_len * 4, cudaMemcpyDeviceToHost,
+                       c->d2h_stream));
   c->out_n[slot] = n;
   c->out_idx[slot] = want_idx != 0;
-  if ((rc = mark_used(c, s))) return rc;
+  CU(cudaEventRecord(c->ev_done[slot], c->d2h_stream));  // kernels + result copies of this slot
   *slot_out = slot;
   return TAV2_OK;
 }

@@ -283,7 +283,7 @@ cudaError_t launch_encode(const Staged& st, const NNCfg& nn, const Params& p, co
 cudaError_t launch_skut_simt(const Params& p, const NNCfg& nn, const Staged* st,
                              const int32_t* idx, const float* F, const uint8_t* fmask, int n,
                              float* scratch, float* U, float* logits, float* pooled, int cs_shift,
-                             cudaStream_t s);
+                             cudaStream_t s, const uint8_t* extra = nullptr, long long extra_stride = 0);
 cudaError_t launch_skut_tc(const Params& p, const SkutImages& img, const NNCfg& nn,
                            const Staged* st, const int32_t* idx, const float* F,
                            const uint8_t* fmask, int n, float* U, float* logits, float* pooled,

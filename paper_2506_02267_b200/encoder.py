@@ -178,16 +178,16 @@ def forward_fused(features, mask, params_or_engine, extra_mask=None, arena=None,
     calling thread's implicit engine) or an
     :class:`~paper_2506_02267_b200.runtime.Engine` holding the model.
     Padded query rows are not computed (never read: keys mask them and
-    pooling skips them) and come back as zeros.  ``extra_mask`` (NAL training
-    masks, encoder.py:366-377) is not on the serving path.
+    pooling skips them) and come back as zeros.  ``extra_mask`` ([L, L] or
+    [B, L, L] bool; the NAL training masks, encoder.py:366-377) is ANDed into
+    causal & key-valid; a row with no allowed key gets a zero attention
+    output (tav2_forward_masked: the f32 running-max kernel).
     """
-    if extra_mask is not None:
-        raise ValidationError("extra_mask is a training-only feature and not on the serving path")
     f = np.asarray(features)
     if f.ndim != 3:
         raise ValidationError("expected a (batch, length, d_model) feature tensor")
     eng = _engine(params_or_engine, _layout_nn(f.shape[1]))
-    return eng.forward(f, np.asarray(mask, bool), mode=mode)
+    return eng.forward(f, np.asarray(mask, bool), mode=mode, extra_mask=extra_mask)
 
 
 def forward_reference(enc: EncodedSequence, params, extra_mask=None, mode: str = "fp32") -> np.ndarray:

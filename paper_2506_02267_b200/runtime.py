@@ -381,8 +381,9 @@ class Engine:
         return out.cpu().numpy()
 
     @_locked
-    def forward(self, features: np.ndarray, mask: np.ndarray, mode: str = "fp32") -> np.ndarray:
-        """forward_fused over caller features (B, S, 64) -> U (valid rows)."""
+    def forward(self, features: np.ndarray, mask: np.ndarray, mode: str = "fp32", extra_mask=None) -> np.ndarray:
+        """forward_fused over caller features (B, S, 64) -> U (valid rows);
+        extra_mask [S, S] or [B, S, S] (encoder.py:366-377) -> tav2_forward_masked."""
         if self.model is None:
             raise ValidationError("no model loaded")
         B, S, d = features.shape
@@ -391,8 +392,16 @@ class Engine:
         F = torch.from_numpy(np.ascontiguousarray(features, np.float32)).to(self.torch_device)
         m = torch.from_numpy(np.ascontiguousarray(mask, np.uint8)).to(self.torch_device)
         U = torch.empty_like(F)
-        N.check(self._lib.tav2_forward(self._ctx, self._mode(mode), N.ptr(F), N.ptr(m), B, N.ptr(U),
-                                       self.stream()))
+        if extra_mask is None:
+            N.check(self._lib.tav2_forward(self._ctx, self._mode(mode), N.ptr(F), N.ptr(m), B, N.ptr(U),
+                                           self.stream()))
+        else:
+            em = np.asarray(extra_mask, bool)
+            if em.shape not in ((S, S), (B, S, S)):
+                raise ValidationError("extra_mask must be (L, L) or (B, L, L)")
+            X = torch.from_numpy(np.ascontiguousarray(em, np.uint8)).to(self.torch_device)
+            N.check(self._lib.tav2_forward_masked(self._ctx, self._mode(mode), N.ptr(F), N.ptr(m), N.ptr(X),
+                                                  int(em.ndim == 3), B, N.ptr(U), self.stream()))
         return U.cpu().numpy()
 
     @_locked

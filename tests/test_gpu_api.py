@@ -144,3 +144,21 @@ def test_capacity_overflow_splits_and_falls_back():
     assert np.array_equal(got, ref) and tiny.overflow_count == 1
     out = tiny.rank_pipelined([packed[:1], packed[1:]])
     assert np.array_equal(np.concatenate(out), ref) and tiny.overflow_count == 3
+
+
+@pytest.mark.parametrize("mode", ["fp32", "bf16"])
+def test_forward_fused_extra_mask(mode):
+    """forward_fused(..., extra_mask) (encoder.py:366-377) on
+    the GPU vs the live reference, shared [L, L] and per-item [B, L, L]
+    masks, including rows with no allowed key and rows without their own key."""
+    import os
+
+    from conftest import GOLDEN
+
+    z = np.load(os.path.join(GOLDEN, "shapes", "extra_mask.npz"))
+    nn = P.NNConfig()
+    model = P.RankingModel.init(P.ModelConfig.for_nn(nn), seed=int(z["seed"]))
+    m = z["mask"][:, :, None]
+    for em, U in ((z["extra2"], z["U2"]), (z["extra3"], z["U3"])):
+        got = P.forward_fused(z["F"], z["mask"], model.encoder, extra_mask=em, mode=mode)
+        assert np.abs((got - U) * m).max() <= 2e-5

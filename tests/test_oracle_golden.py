@@ -2,11 +2,12 @@
 live reference produced (oracle/gen_golden.py).  Pins the oracle before any
 GPU result is compared with it."""
 import hashlib
+import os
 
 import numpy as np
 import pytest
 
-from conftest import golden_cases, load_case
+from conftest import GOLDEN, golden_cases, load_case
 from helpers import to_user
 from oracle import seqrank_oracle as orc
 
@@ -89,3 +90,14 @@ def test_nn_feature_log_bytes_match_reference(case):
     assert len(recs) == len(off) - 1
     for i, rec in enumerate(recs):
         assert rec == blob[off[i]:off[i + 1]], f"{case}: record {i} differs"
+
+
+def test_oracle_extra_mask_matches_reference():
+    """forward_fused(extra_mask) restated in the oracle == the live reference's
+    output (tests/golden/shapes/extra_mask.npz, oracle/gen_extra_mask_golden.py)."""
+    z = np.load(os.path.join(GOLDEN, "shapes", "extra_mask.npz"))
+    P = orc.model_init(int(z["seed"]), seq_len=z["mask"].shape[1])
+    m = z["mask"][:, :, None]
+    for em, U in ((z["extra2"], z["U2"]), (z["extra3"], z["U3"])):
+        O = orc.forward_fused(z["F"], z["mask"], P, extra_mask=em)
+        assert np.abs((O - U) * m).max() <= 1e-6

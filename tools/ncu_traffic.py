@@ -11,7 +11,7 @@ import re
 import subprocess
 import sys
 
-NAMES = {"prep_kernel": "prep", "nn_bound_kernel": "nn_bound", "nn_select_kernel": "nn_select",
+NAMES = {"prep_kernel": "prep", "skut_tc3_f16_kernel": "skut_tc3_f16", "nn_bound_kernel": "nn_bound", "nn_select_kernel": "nn_select",
          "skut_tc3_kernel": "skut_tc3", "skut_tc2_kernel": "skut_tc", "skut_simt_kernel": "skut_simt"}
 
 
@@ -26,10 +26,12 @@ def main(rep, out="profiles/traffic.json"):
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     acc = {}
     for r in rows[2:]:
-        m = re.search(r"(\w+_kernel)\(", r[ik])
+        m = re.search(r"(\w+_kernel)(<(\w+)>)?\(", r[ik])
         if not m:
             continue
         name = m.group(1)
+        if name == "skut_tc3_kernel" and m.group(3) == "true":
+            name = "skut_tc3_f16_kernel"
         if name == "nn_scan_kernel":  # launches alternate pass 1 / pass 2
             name = "nn_scan1" if acc.get("_scan_toggle", 0) == 0 else "nn_scan2"
             acc["_scan_toggle"] = 1 - acc.get("_scan_toggle", 0)
