@@ -91,6 +91,12 @@ bool tav2::pdl_enabled() {
   return on;
 }
 
+// A/B switches read from the environment on every call (cheap; test-only)
+static bool getenv_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && e[0] == '1';
+}
+
 struct tav2_ctx {
   tav2_config cfg;
   tav2_capacity cap;
@@ -1045,6 +1051,16 @@ int run_score(tav2_ctx* c, int mode, const int32_t* idx, float* logits, float* p
     CU(timed(c, f16 ? "skut_tc3_f16" : "skut_tc3", s, [&] {
       return launch_skut_tc3(c->params, f16 ? c->images3h : c->images3, c->nn, st, idx, st.n_items, logits, pooled,
                              sel, f16, s);
+    }));
+    return TAV2_OK;
+  }
+  // 192 < S <= 384 (the k_ll = 128 / 256 sweep points): the same folded
+  // bf16x3 / fp16x3 transformer on 2-CTA clusters, keys shared over DSMEM
+  if (tc3_ok && skut_tc4_supported(c->nn, c->params) && !getenv_flag("TAV2_NO_TC4")) {
+    const bool f16 = mode == TAV2_MODE_FP32;
+    CU(timed(c, f16 ? "skut_tc4_f16" : "skut_tc4", s, [&] {
+      return launch_skut_tc4(c->params, f16 ? c->images3h : c->images3, c->nn, st, idx, st.n_items, logits, pooled,
+                             f16, s);
     }));
     return TAV2_OK;
   }

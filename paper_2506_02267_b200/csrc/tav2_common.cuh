@@ -261,6 +261,9 @@ bool skut_tc3_supported(const NNCfg& nn, const Params& p);
 cudaError_t launch_skut_tc3(const Params& p, const SkutImages3& img, const NNCfg& nn, const Staged& st,
                             const int32_t* idx, int n, float* logits, float* pooled, SelFlags sel, bool f16,
                             cudaStream_t s);
+bool skut_tc4_supported(const NNCfg& nn, const Params& p);
+cudaError_t launch_skut_tc4(const Params& p, const SkutImages3& img, const NNCfg& nn, const Staged& st,
+                            const int32_t* idx, int n, float* logits, float* pooled, bool f16, cudaStream_t s);
 cudaError_t launch_nn_scan(const Staged& st, const NNCfg& nn, const NNScan& sc, int pass,
                            cudaStream_t s);
 cudaError_t launch_nn_bound(const Staged& st, const NNCfg& nn, const NNScan& sc, cudaStream_t s);

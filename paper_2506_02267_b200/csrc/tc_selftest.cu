@@ -6,6 +6,10 @@
 //   2 bf16, A smem K-major, B smem MN-major
 //   3 i8,   A smem K-major, B loaded by TMA (3-D chunk-major map)
 //   4 i8,   A smem K-major, B smem K-major (manual load)
+//   5 bf16, A smem K-major, B smem MN-major with the core matrices tiled
+//     k-group-fastest: (k, n) at (n/8)*(K*16) + (k/8)*128 + (k%8)*16 +
+//     (n%8)*2 (LBO = 128, SBO = K*16) -- skut_tc4 reads its key buffer,
+//     written K-major for S = Q'K^T, as this MN-major B of P.a
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -24,7 +28,7 @@ __global__ void __launch_bounds__(128) tc_selftest_kernel(int which, const uint8
   __shared__ uint32_t taddr_s;
   __shared__ __align__(8) uint64_t bar[2];
   const int tid = threadIdx.x, warp = tid >> 5;
-  const bool i8 = which >= 3;
+  const bool i8 = which == 3 || which == 4;
   const int esz = i8 ? 1 : 2;
   const int kbytes = K * esz;           // bytes per row
   const int nchunk = kbytes / 16;       // 16-byte K chunks
@@ -36,7 +40,13 @@ __global__ void __launch_bounds__(128) tc_selftest_kernel(int which, const uint8
         *reinterpret_cast<const int4*>(A + (size_t)tid * kbytes + c * 16);
   }
   // ---- B ----
-  if (which == 2) {  // MN-major: global [K][N] bf16
+  if (which == 5) {  // MN-major, k-groups fastest: global [K][N] bf16
+    for (int e = tid; e < K * (N / 8); e += 128) {
+      int k = e / (N / 8), g = e % (N / 8);
+      *reinterpret_cast<int4*>(Bs + g * (K * 16) + (k / 8) * 128 + (k % 8) * 16) =
+          *reinterpret_cast<const int4*>(B + ((size_t)k * N + g * 8) * 2);
+    }
+  } else if (which == 2) {  // MN-major: global [K][N] bf16
     const int lbo = (N / 8) * 128;
     for (int e = tid; e < K * (N / 8); e += 128) {
       int k = e / (N / 8), g = e % (N / 8);
@@ -81,10 +91,11 @@ __global__ void __launch_bounds__(128) tc_selftest_kernel(int which, const uint8
   }
   if (tid == 0) {
     if (!i8) {
-      const uint32_t id = idesc_bf16(128, N, 0, which == 2);
+      const uint32_t id = idesc_bf16(128, N, 0, which == 2 || which == 5);
       for (int j = 0; j < K / 16; ++j) {
-        uint64_t bd = which == 2 ? sdesc(smem_u32(Bs) + 2 * j * (N / 8) * 128, (N / 8) * 128, 128)
-                                 : sdesc(smem_u32(Bs) + 2 * j * N * 16, N * 16, 128);
+        uint64_t bd = which == 2   ? sdesc(smem_u32(Bs) + 2 * j * (N / 8) * 128, (N / 8) * 128, 128)
+                      : which == 5 ? sdesc(smem_u32(Bs) + 2 * j * 128, 128, K * 16)
+                                   : sdesc(smem_u32(Bs) + 2 * j * N * 16, N * 16, 128);
         if (which == 1) {
           mma_bf16_ts(t, t + 256 + j * 8, bd, id, j > 0);
         } else {
@@ -150,12 +161,12 @@ bool make_rows32_map(CUtensorMap* map, const void* base, int64_t rows, int box_r
 extern "C" int tav2_tc_selftest(int which, const void* A, const void* B, void* D, int N, int K,
                                 void* stream) {
   using namespace tav2;
-  if (which < 0 || which > 4 || N < 16 || N > 256 || N % 16 || K < 16 || K > 256 || K % 16)
+  if (which < 0 || which > 5 || N < 16 || N > 256 || N % 16 || K < 16 || K > 256 || K % 16)
     return TAV2_EINVAL;
-  if (which >= 3 && K != 32) return TAV2_EINVAL;
+  if ((which == 3 || which == 4) && K != 32) return TAV2_EINVAL;
   CUtensorMap map{};
   if (which == 3 && !make_rows32_map(&map, B, N, N)) return TAV2_ECUDA;
-  const int esz = which >= 3 ? 1 : 2;
+  const int esz = (which == 3 || which == 4) ? 1 : 2;
   size_t smem = (size_t)(128 + N) * K * esz + 1024;
   if (cudaFuncSetAttribute(tc_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
