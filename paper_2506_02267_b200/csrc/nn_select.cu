@@ -30,8 +30,8 @@
 namespace tav2 {
 
 constexpr int kSelWarps = 2;
-constexpr int kSelCap = 256;    // shared-memory key array per warp (2 KB)
-constexpr int kSelCache = 256;  // survivors sorted in registers
+constexpr int kSelCap = 512;    // shared-memory key array per warp (4 KB)
+constexpr int kSelCache = 512;  // survivors whose keys are staged (k_ll = 256: ~k + a few dozen)
 constexpr int kCaps0 = 16384;   // LIFELONG_CAP (core.py:31): source positions per bitmap
 
 // (index + 1 | f32 score): sorts by storage index, never 0 (0 pads)
@@ -297,6 +297,71 @@ __device__ __forceinline__ void warp_bitonic_desc_smem(uint64_t* a, int n, int l
       __syncwarp();
     }
   }
+}
+
+// The k largest of 256 < n <= kSelCap keys a[0..n) (shared; the k_ll = 256
+// sweep point: about k + a few dozen survivors): MSB-first radix select on
+// the cached keys (8-bit digits, warp-aggregated histogram; usually done
+// after the first one or two digits), winners marked in the bitmap.
+__device__ __forceinline__ void select_radix_cached(const uint64_t* a, int n, int k, int lane, unsigned* hist,
+                                                    uint32_t* bm, int words) {
+  uint64_t prefix = 0ull, pmask = 0ull;
+  int want = k;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = lane; i < 256; i += 32) hist[i] = 0u;
+    __syncwarp();
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      const uint64_t x = i < n ? a[i] : 0ull;
+      const int dg = (i < n && (x & pmask) == prefix) ? (int)((x >> shift) & 255) : 256;
+      const unsigned peers = __match_any_sync(0xffffffffu, dg);
+      if (dg < 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[dg], (unsigned)__popc(peers));
+    }
+    __syncwarp();
+    unsigned c8[8], tot = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      c8[j] = hist[255 - 8 * lane - j];
+      tot += c8[j];
+    }
+    unsigned incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const unsigned excl = incl - tot;
+    const unsigned sel = __ballot_sync(0xffffffffu, excl < (unsigned)want && (unsigned)want <= incl);
+    const int srcl = __ffs(sel) - 1;
+    int digit = 0, above = 0, inb = 0;
+    if (lane == srcl) {
+      unsigned run = excl;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (run + c8[j] >= (unsigned)want) {
+          digit = 255 - 8 * lane - j;
+          above = (int)run;
+          inb = (int)c8[j];
+          break;
+        }
+        run += c8[j];
+      }
+    }
+    digit = __shfl_sync(0xffffffffu, digit, srcl);
+    above = __shfl_sync(0xffffffffu, above, srcl);
+    inb = __shfl_sync(0xffffffffu, inb, srcl);
+    want -= above;
+    prefix |= (uint64_t)digit << shift;
+    pmask |= 255ull << shift;
+    __syncwarp();
+    if (inb == want) break;  // the k-th key's bucket is selected whole
+  }
+  // winners: exactly k keys (unique) have (key & pmask) >= prefix
+  for (int i = lane; i < n; i += 32) {
+    const uint64_t x = a[i];
+    if ((x & pmask) >= prefix) bm_mark(bm, words, key_index(x));
+  }
+  __syncwarp();
 }
 
 // Path for n > kSelCache: MSB-first radix select (8-bit digits,
@@ -621,7 +686,8 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
     const int np = max(n, k);
     if (np <= 64) select_rank<2>(a, n, k, lane, bm, words);
     else if (np <= 128) select_bisect<4>(a, n, k, lane, bm, words);
-    else select_bisect<8>(a, n, k, lane, bm, words);
+    else if (np <= 256) select_bisect<8>(a, n, k, lane, bm, words);
+    else select_radix_cached(a, n, k, lane, hist_s[warp], bm, words);
     if (kDebug && lane == 0) sel_record_phase(item * 3 + s, 1, gtimer() - t_start);
     emit_bitmap(bm, words, k, lane, orow, srow, ks);
   } else {

@@ -1,6 +1,7 @@
 // SKUT v4 on the 5th-gen tensor cores for long layouts (192 < S <= 384,
 // <= 2 layers; the k_ll = 128 / 256 points of the C5 sweep): one candidate
-// per 2-CTA cluster iteration (persistent over candidates).
+// per CTA (S_pad <= 256) or per 2-CTA cluster (S_pad <= 384) iteration,
+// persistent over candidates.
 //
 // Reference: encoder.py:161-188 (encode_batch), :196-211 (layer_norm,
 // masked_softmax), :314-462 (forward_fused), trainer.py:354-366 (pool + head).
@@ -195,7 +196,11 @@ __device__ __forceinline__ void t4_mma3(uint32_t d, uint32_t a_col, uint32_t a_l
   }
 }
 
-template <bool F16>
+// CL = 2: the 2-CTA cluster layout above (256 < S_pad <= 384).  CL = 1:
+// one CTA holds all rows (192 < S_pad <= 256: 8 blocks of S_pad/8 rows,
+// tile 0 = blocks 0-3, tile 1 = 7-4 as in skut_tc3), keys 64 KB + weights
+// 112 KB; no distributed shared memory.
+template <bool F16, int CL>
 __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutImages3 img, NNCfg nn, Staged st,
                                                                  const int32_t* idx, int n, float* logits,
                                                                  float* pooled_out) {
@@ -214,7 +219,7 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
 
   const int S = nn.seq_len;
   const int S_pad = (S + 15) & ~15;
-  const int rpw = S_pad >> 4;  // rows per warp block (16 blocks over the pair)
+  const int rpw = CL == 2 ? S_pad >> 4 : S_pad >> 3;  // rows per warp block (8 blocks per CTA)
   const int NL = p.num_layers;
   const int wbytes = NL * kW4Layer + kImg3WO;
   uint8_t* Wsm = sm;
@@ -223,20 +228,21 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
   const uint32_t wsm = smem_u32(Wsm);
   const uint32_t khi = smem_u32(Khi), klo = smem_u32(Klo);
 
-  const uint32_t crank = cluster_rank(), peer = crank ^ 1u;
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const uint32_t crank = CL == 2 ? cluster_rank() : 0u, peer = crank ^ 1u;
+  const int pair = CL == 2 ? blockIdx.x >> 1 : blockIdx.x, npairs = CL == 2 ? gridDim.x >> 1 : gridDim.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = warp >> 2, q = warp & 3;
   // row blocks: CTA 0 = {q, 15 - q}, CTA 1 = {4 + q, 11 - q} (tile 0, tile 1)
-  const int kb = crank == 0 ? (t == 0 ? q : 15 - q) : (t == 0 ? 4 + q : 11 - q);
-  const int maxblk = crank == 0 ? (t == 0 ? 3 : 15) : (t == 0 ? 7 : 11);
+  const int kb = CL == 1 ? (t == 0 ? q : 7 - q)
+                         : (crank == 0 ? (t == 0 ? q : 15 - q) : (t == 0 ? 4 + q : 11 - q));
+  const int maxblk = CL == 1 ? (t == 0 ? 3 : 7) : (crank == 0 ? (t == 0 ? 3 : 15) : (t == 0 ? 7 : 11));
   const int NK = (((maxblk + 1) * rpw) + 15) & ~15;  // keys this tile's rows can see
   const int nchunks = (NK + kT4Chunk - 1) / kT4Chunk;
   const bool mapped = lane < rpw;
   const int r = rpw * kb + lane;
   const bool in_seq = mapped && r < S;
   // does the peer's tile see this row's key?  (CTA 1 sees keys < 12 rpw)
-  const bool to_peer = crank == 1 || t == 0;
+  const bool to_peer = CL == 2 && (crank == 1 || t == 0);
 
   if (tid == 0) {
     mbar_init(&t4.simt[0], 128);
@@ -245,8 +251,8 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
     mbar_init(&t4.mma[1], 1);
     mbar_init(&t4.m3[0], 1);
     mbar_init(&t4.m3[1], 1);
-    mbar_init(&t4.kvready, 2 * kT4Threads);
-    mbar_init(&t4.kvfree, 4);
+    mbar_init(&t4.kvready, CL * kT4Threads);
+    mbar_init(&t4.kvfree, 2 * CL);
     mbar_init(&t4.wfull, 1);
     mbar_init(&t4.poolready[0], kDModel + 1);
     mbar_init(&t4.poolready[1], kDModel + 1);
@@ -273,16 +279,21 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
     for (int L = 0; L < NL; ++L) bulk_g2s(Wsm + L * kW4Layer, img.w[L], kW4Layer, &t4.wfull);
     bulk_g2s(Wsm + NL * kW4Layer, img.wout, kImg3WO, &t4.wfull);
   }
-  cluster_sync_all();  // both CTAs' barriers initialised before any remote arrival
+  if constexpr (CL == 2) cluster_sync_all();  // both CTAs' barriers initialised before any remote arrival
+  else __syncthreads();
 
   // peer addresses (distributed shared memory)
-  const uint32_t p_khi = dsmem_addr(khi, peer), p_klo = dsmem_addr(klo, peer);
-  const uint32_t p_valid = dsmem_addr(smem_u32(&valid_w[0][0]), peer);
-  const uint32_t p_kmax = dsmem_addr(smem_u32(&kmax_s[0][0]), peer);
-  const uint32_t p_kvready = dsmem_addr(smem_u32(&t4.kvready), peer);
-  const uint32_t p_pool = dsmem_addr(smem_u32(&pool_s[0][0]), peer);
-  const uint32_t p_pany = dsmem_addr(smem_u32(&pany_s[0]), peer);
-  const uint32_t p_poolready = dsmem_addr(smem_u32(&t4.poolready[0]), peer);
+  uint32_t p_khi = 0, p_klo = 0, p_valid = 0, p_kmax = 0, p_kvready = 0, p_pool = 0, p_pany = 0, p_poolready = 0;
+  if constexpr (CL == 2) {
+    p_khi = dsmem_addr(khi, peer);
+    p_klo = dsmem_addr(klo, peer);
+    p_valid = dsmem_addr(smem_u32(&valid_w[0][0]), peer);
+    p_kmax = dsmem_addr(smem_u32(&kmax_s[0][0]), peer);
+    p_kvready = dsmem_addr(smem_u32(&t4.kvready), peer);
+    p_pool = dsmem_addr(smem_u32(&pool_s[0][0]), peer);
+    p_pany = dsmem_addr(smem_u32(&pany_s[0]), peer);
+    p_poolready = dsmem_addr(smem_u32(&t4.poolready[0]), peer);
+  }
 
   const bool issue_warp = q == 0;
   const uint32_t R = 256u * t;
@@ -351,10 +362,10 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
         const unsigned long long w = (unsigned long long)b << (r0 & 31);
         const int w0 = r0 >> 5;
         atomicOr(&valid_w[par][w0], (uint32_t)w);
-        atom_or_dsmem(p_valid + 4u * (uint32_t)(12 * par + w0), (uint32_t)w);
+        if (CL == 2) atom_or_dsmem(p_valid + 4u * (uint32_t)(12 * par + w0), (uint32_t)w);
         if ((uint32_t)(w >> 32)) {
           atomicOr(&valid_w[par][w0 + 1], (uint32_t)(w >> 32));
-          atom_or_dsmem(p_valid + 4u * (uint32_t)(12 * par + w0 + 1), (uint32_t)(w >> 32));
+          if (CL == 2) atom_or_dsmem(p_valid + 4u * (uint32_t)(12 * par + w0 + 1), (uint32_t)(w >> 32));
         }
       }
     }
@@ -398,13 +409,13 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
         for (int o = 16; o > 0; o >>= 1) an2 = fmaxf(an2, __shfl_xor_sync(0xffffffffu, an2, o));
         if (lane == 0) {
           atomicMax(&kmax_s[par][L], __float_as_uint(an2));
-          atom_max_dsmem(p_kmax + 4u * (uint32_t)(2 * par + L), __float_as_uint(an2));
+          if (CL == 2) atom_max_dsmem(p_kmax + 4u * (uint32_t)(2 * par + L), __float_as_uint(an2));
         }
         tmem_st_wait();
         fence_proxy_async_all();  // generic-proxy key writes (both CTAs) -> tensor core
         done();
         mbar_arrive(&t4.kvready);
-        mbar_arrive_dsmem(p_kvready);
+        if (CL == 2) mbar_arrive_dsmem(p_kvready);
       }
       if (issue_warp) {  // M1: Q' = A Wqk   (N = 64: the first 64 rows of the [Wqk|Wvo] image)
         issuer_wait_simt();
@@ -558,7 +569,8 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
             commit_w(&t4.mma[t]);
           } else {
             commit_w(&t4.mma[t]);
-            commit_mc_w(&t4.kvfree, 0x3);  // this tile no longer reads either CTA's keys
+            if (CL == 2) commit_mc_w(&t4.kvfree, 0x3);  // this tile no longer reads either CTA's keys
+            else commit_w(&t4.kvfree);
           }
         }
       }
@@ -651,7 +663,7 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
       commit_w(&t4.mma[t]);
     }
     wait_mma();
-    const bool head = (uint32_t)par == crank;  // the head alternates between the pair's CTAs
+    const bool head = CL == 1 || (uint32_t)par == crank;  // the head alternates between the pair's CTAs
     {
       float y[kDModel];
       t4_ld64(lanebase + k4CD, y);
@@ -681,10 +693,10 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
       continue;
     }
     // head CTA: combine with the peer's maxima (trainer.py:354-359)
-    mbar_wait_cl(&t4.poolready[par], (k >> 1) & 1);
+    if (CL == 2) mbar_wait_cl(&t4.poolready[par], (k >> 1) & 1);
     if (tid < kDModel) {
-      v = fmaxf(v, pool_s[par][tid]);
-      const bool any = any_s || pany_s[par];
+      if (CL == 2) v = fmaxf(v, pool_s[par][tid]);
+      const bool any = any_s || (CL == 2 && pany_s[par]);
       v = any ? v : 0.0f;  // empty user -> pooled = 0 (trainer.py:358-359)
       z_s[tid] = v;
       if (pooled_out) pooled_out[(size_t)item * kDModel + tid] = v;
@@ -720,9 +732,10 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
   }
   fence_before();
   __syncthreads();
-  cluster_sync_all();  // no distributed shared memory traffic targets an exited CTA
+  if constexpr (CL == 2) cluster_sync_all();  // no distributed shared memory traffic targets an exited CTA
   if (warp == 0) tmem_free<512>(0u);
 }
+
 
 bool skut_tc4_supported(const NNCfg& nn, const Params& p) {
   const int S_pad = (nn.seq_len + 15) & ~15;
@@ -734,25 +747,34 @@ cudaError_t launch_skut_tc4(const Params& p, const SkutImages3& img, const NNCfg
   if (n == 0) return cudaSuccess;
   const int S_pad = (nn.seq_len + 15) & ~15;
   const size_t smem = (size_t)p.num_layers * kW4Layer + kImg3WO + 2 * (size_t)S_pad * 128;
-  auto kern = f16 ? skut_tc4_kernel<true> : skut_tc4_kernel<false>;
+  const int CL = S_pad > 256 ? 2 : 1;
+  auto kern = CL == 2 ? (f16 ? skut_tc4_kernel<true, 2> : skut_tc4_kernel<false, 2>)
+                      : (f16 ? skut_tc4_kernel<true, 1> : skut_tc4_kernel<false, 1>);
   cudaError_t e = set_max_dyn_smem((const void*)kern, (int)smem);
   if (e != cudaSuccess) return e;
-  const int pairs_max = device_sms() / 2;
-  const int pairs = n < pairs_max ? n : pairs_max;
+  const int units_max = device_sms() / CL;
+  const int units = n < units_max ? n : units_max;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * pairs);
+  cfg.gridDim = dim3(CL * units);
   cfg.blockDim = dim3(kT4Threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
+  int na = 0;
+  if (CL == 2) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 2;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, kern, p, img, nn, st, idx, n, logits, pooled);
 }
 
