@@ -148,14 +148,20 @@ int tav2_rank(tav2_ctx* ctx, const tav2_request* reqs, int n_req, int mode, floa
               int32_t* idx_host, void* stream);
 
 /* Pipelined rank (the serving loop): stage + nn_select + score + result
- * copies are enqueued without waiting, into one of two staging slots, so the
+ * copies are enqueued without waiting, into one of TAV2_STAGE_SLOTS staging slots, so the
  * host packing and H2D copy of the next request overlap the kernels of the
- * current one.  Returns the slot in *slot_out; at most two submits may be in
+ * current one.  Returns the slot in *slot_out; at most TAV2_STAGE_SLOTS submits may be in
  * flight: collect a slot before submitting into it again (submit blocks until
  * the slot's previous rank finished).  want_idx: also copy the NN indices
- * (NN-feature logging). */
+ * (NN-feature logging).  The chain runs on the slot's own internal compute
+ * stream, ordered after the work already enqueued on `stream`; the two
+ * slots' kernels may overlap on the device (slot-private workspaces). */
 int tav2_rank_submit(tav2_ctx* ctx, const tav2_request* reqs, int n_req, int mode, int want_idx,
                      void* stream, int32_t* slot_out);
+
+/* Number of staging slots (submits that may be in flight at once). */
+#define TAV2_STAGE_SLOTS 3
+int tav2_stage_slots(void);
 
 /* Block until a submitted rank's kernels and result copies finished, without
  * touching the context's staging state: a completion thread may wait here

@@ -33,6 +33,7 @@ EXPORTS = (
     "tav2_rank_submit", "tav2_rank_collect",
     "tav2_store_reserve", "tav2_store_put", "tav2_store_remove", "tav2_store_count",
     "tav2_similarity", "tav2_pool", "tav2_rank_wait", "tav2_graph_info", "tav2_forward_masked",
+    "tav2_stage_slots",
 )
 
 
@@ -114,6 +115,7 @@ def lib() -> ctypes.CDLL:
             L.tav2_debug_timeline.argtypes = [vp, ctypes.c_int]
             L.tav2_debug_cta.argtypes = [vp]
             L.tav2_tc_selftest.argtypes = [ctypes.c_int, vp, vp, vp, ctypes.c_int, ctypes.c_int, vp]
+            L.tav2_stage_slots.argtypes = []
             L.tav2_last_error.restype = ctypes.c_char_p
             L.tav2_build_info.restype = ctypes.c_char_p
             for name in EXPORTS:

@@ -112,38 +112,49 @@ struct tav2_ctx {
   // copy_stream; ev_staged[s]: slot s's copy done (host arena reusable, the
   // compute stream may read it); ev_done[s]: the kernels (and result copies)
   // of slot s done (device region and pinned outputs reusable).
-  static constexpr int kStageSlots = 2;
-  unsigned char* h_arena[kStageSlots] = {nullptr, nullptr};
-  unsigned char* d_staged[kStageSlots] = {nullptr, nullptr};
+  static constexpr int kStageSlots = TAV2_STAGE_SLOTS;
+  unsigned char* h_arena[kStageSlots] = {};
+  unsigned char* d_staged[kStageSlots] = {};
   int64_t staged_cap = 0;
-  cudaEvent_t ev_staged[kStageSlots] = {nullptr, nullptr};
-  cudaEvent_t ev_done[kStageSlots] = {nullptr, nullptr};
+  cudaEvent_t ev_staged[kStageSlots] = {};
+  cudaEvent_t ev_done[kStageSlots] = {};
   cudaStream_t copy_stream = nullptr;
   Plan plans[kStageSlots]{};
   int cur = 0;        // slot of the current staged batch
   int next_slot = 0;  // slot the next stage uses
-  float* h_out[kStageSlots] = {nullptr, nullptr};     // pinned logits of a submitted rank
-  int32_t* h_idx[kStageSlots] = {nullptr, nullptr};   // pinned NN indices (optional)
-  int out_n[kStageSlots] = {0, 0};
-  bool out_idx[kStageSlots] = {false, false};
-  // derived device buffers
-  float* tok_unit = nullptr;
-  uint32_t* tok_img = nullptr;
-  float* cand_unit = nullptr;
-  float* tok_feat = nullptr;   // [T, 64] Eq. 4 token features (prep, bf16 SKUT gather)
-  NNScan scan{};               // threshold-scan NN buffers (nn_scan.cu)
+  float* h_out[kStageSlots] = {};     // pinned logits of a submitted rank
+  int32_t* h_idx[kStageSlots] = {};   // pinned NN indices (optional)
+  int out_n[kStageSlots] = {};
+  bool out_idx[kStageSlots] = {};
+  // Derived device buffers, one set per staging slot: the launch chains of
+  // two submitted requests (tav2_rank_submit, one compute stream per slot)
+  // may then run concurrently -- request i+1's NN kernels on the SMs that
+  // request i's SKUT tail frees.  A slot's buffers are reused only after
+  // ev_done[slot] (tav2_stage orders the next use of the slot after it).
+  struct Derived {
+    float* tok_unit = nullptr;
+    uint32_t* tok_img = nullptr;
+    float* cand_unit = nullptr;
+    float* tok_feat = nullptr;    // [T, 64] Eq. 4 token features (prep, bf16 SKUT gather)
+    NNScan scan{};                // threshold-scan NN buffers (nn_scan.cu)
+    uint32_t* sel_done = nullptr;   // per-(candidate, source) select flags (SelFlags)
+    uint32_t* sel_epoch = nullptr;  // device word: the current run's flag epoch (prep bumps it)
+    float* skut_scratch = nullptr;  // SIMT SKUT scratch
+  };
+  Derived dv[kStageSlots];
+  cudaStream_t slot_stream[kStageSlots] = {};  // tav2_rank_submit compute streams
+  cudaEvent_t ev_caller[kStageSlots] = {};     // caller-stream order -> slot stream
+  Derived& cur_dv() { return dv[cur]; }
 
   int32_t* idx = nullptr;
   float* logits = nullptr;
   // tav2_rank_submit: per-slot index / logit buffers, so the result copies
   // of one request (on d2h_stream, after ev_comp[slot]) overlap the next
   // request's kernels on the compute stream instead of sitting between them
-  int32_t* idx_s[kStageSlots] = {nullptr, nullptr};
-  float* logits_s[kStageSlots] = {nullptr, nullptr};
-  cudaEvent_t ev_comp[kStageSlots] = {nullptr, nullptr};
+  int32_t* idx_s[kStageSlots] = {};
+  float* logits_s[kStageSlots] = {};
+  cudaEvent_t ev_comp[kStageSlots] = {};
   cudaStream_t d2h_stream = nullptr;
-  uint32_t* sel_done = nullptr;  // per-(candidate, source) select flags (SelFlags)
-  uint32_t* sel_epoch = nullptr; // device word: the current run's flag epoch (prep bumps it)
   // CUDA graphs of the launch chain prep .. SKUT (run_chain): one per
   // (staging slot, mode, output buffer, batch plan), captured the second
   // time a shape is seen and replayed after; invalidated by tav2_load_params
@@ -161,7 +172,6 @@ struct tav2_ctx {
   cudaStream_t cap_stream = nullptr;
   uint64_t graph_tick = 0;
   bool graph_broken = false;  // a capture failed: launch directly from then on
-  float* skut_scratch = nullptr;
   // params
   float* d_params = nullptr;
   Params params{};
@@ -242,10 +252,11 @@ Staged staged_view(tav2_ctx* c) {
   s.action = reinterpret_cast<const uint16_t*>(b + p.off_action);
   s.surface = reinterpret_cast<const uint8_t*>(b + p.off_surface);
   s.emb = reinterpret_cast<const int8_t*>(b + p.off_emb);
-  s.tok_unit = c->tok_unit;
-  s.tok_img = c->tok_img;
-  s.cand_unit = c->cand_unit;
-  s.tok_feat = c->tok_feat;
+  const tav2_ctx::Derived& d = c->dv[c->cur];
+  s.tok_unit = d.tok_unit;
+  s.tok_img = d.tok_img;
+  s.cand_unit = d.cand_unit;
+  s.tok_feat = d.tok_feat;
   s.n_req = p.n_req;
   s.n_items = p.n_items;
   s.n_tok = p.n_tok;
@@ -285,22 +296,28 @@ int free_all(tav2_ctx* c) {
   cudaFree(c->st_emb);
   cudaFree(c->st_act);
   cudaFree(c->st_surf);
-  cudaFree(c->tok_unit);
-  cudaFree(c->tok_img);
-  cudaFree(c->cand_unit);
-  cudaFree(c->tok_feat);
+  for (auto& d : c->dv) {
+    cudaFree(d.tok_unit);
+    cudaFree(d.tok_img);
+    cudaFree(d.cand_unit);
+    cudaFree(d.tok_feat);
+    cudaFree(d.scan.gmax);
+    cudaFree(d.scan.bound);
+    cudaFree(d.scan.count);
+    cudaFree(d.scan.surv);
+    cudaFree(d.sel_done);
+    cudaFree(d.sel_epoch);
+    cudaFree(d.skut_scratch);
+  }
+  for (int k = 0; k < tav2_ctx::kStageSlots; ++k) {
+    if (c->slot_stream[k]) cudaStreamDestroy(c->slot_stream[k]);
+    if (c->ev_caller[k]) cudaEventDestroy(c->ev_caller[k]);
+  }
   cudaFree(c->d_images3);
-  cudaFree(c->scan.gmax);
-  cudaFree(c->scan.bound);
-  cudaFree(c->scan.count);
-  cudaFree(c->scan.surv);
   cudaFree(c->idx);
-  cudaFree(c->sel_done);
-  cudaFree(c->sel_epoch);
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   cudaFree(c->logits);
-  cudaFree(c->skut_scratch);
   cudaFree(c->d_params);
   cudaFree(c->d_images);
   for (auto& sl : c->slots) {
@@ -419,32 +436,43 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
   if ((e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking)) != cudaSuccess)
     return bad(e, "copy stream");
 
-  // padded to whole 64-token tiles (+1): the NN kernel bulk-copies full tiles
-  if ((e = cudaMalloc(&c->tok_unit, (size_t)(cdiv((int)std::max<int64_t>(T, 1), 64) + 1) * 64 * kEmbed * 4)) !=
-      cudaSuccess)
-    return bad(e, "tok_unit");
-  if ((e = cudaMalloc(&c->tok_img, (size_t)(cdiv((int)std::max<int64_t>(T, 1), kScanTile) + 1) * kScanTileBytes)) !=
-      cudaSuccess)
-    return bad(e, "token image");
-  if ((e = cudaMalloc(&c->cand_unit, (size_t)N * kEmbed * 4)) != cudaSuccess) return bad(e, "cand_unit");
-  if ((e = cudaMalloc(&c->tok_feat, (size_t)std::max<int64_t>(T, 1) * kDModel * 4)) != cudaSuccess)
-    return bad(e, "token features");
-  // scan buffers: a source has at most max(8k + 2, 16384/32 + 2) groups
-  // (planner), a (candidate, source) at most its source length of survivors
-  c->scan.gcap = (std::max(8 * c->kmax + 2, kCaps[0] / 32 + 2) + 8 + 7) & ~7;  // + 8: aligned rows
-  c->scan.surv_stride =
-      (int)((std::min<int64_t>(std::max<int64_t>(T, 8), kCaps[0] + kCaps[1] + kCaps[2]) + 7) & ~int64_t(7));
-  if ((e = cudaMalloc(&c->scan.gmax, (size_t)N * 3 * c->scan.gcap * 4)) != cudaSuccess)
-    return bad(e, "scan group maxima");
-  if ((e = cudaMalloc(&c->scan.bound, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "scan bounds");
-  if ((e = cudaMalloc(&c->scan.count, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "scan counts");
-  if ((e = cudaMalloc(&c->scan.surv, (size_t)N * c->scan.surv_stride * 2)) != cudaSuccess)
-    return bad(e, "scan survivors");
+  for (int k = 0; k < tav2_ctx::kStageSlots; ++k) {
+    tav2_ctx::Derived& d = c->dv[k];
+    // padded to whole 64-token tiles (+1): the NN kernel bulk-copies full tiles
+    if ((e = cudaMalloc(&d.tok_unit, (size_t)(cdiv((int)std::max<int64_t>(T, 1), 64) + 1) * 64 * kEmbed * 4)) !=
+        cudaSuccess)
+      return bad(e, "tok_unit");
+    if ((e = cudaMalloc(&d.tok_img, (size_t)(cdiv((int)std::max<int64_t>(T, 1), kScanTile) + 1) * kScanTileBytes)) !=
+        cudaSuccess)
+      return bad(e, "token image");
+    if ((e = cudaMalloc(&d.cand_unit, (size_t)N * kEmbed * 4)) != cudaSuccess) return bad(e, "cand_unit");
+    if ((e = cudaMalloc(&d.tok_feat, (size_t)std::max<int64_t>(T, 1) * kDModel * 4)) != cudaSuccess)
+      return bad(e, "token features");
+    // scan buffers: a source has at most max(8k + 2, 16384/32 + 2) groups
+    // (planner), a (candidate, source) at most its source length of survivors
+    d.scan.gcap = (std::max(8 * c->kmax + 2, kCaps[0] / 32 + 2) + 8 + 7) & ~7;  // + 8: aligned rows
+    d.scan.surv_stride =
+        (int)((std::min<int64_t>(std::max<int64_t>(T, 8), kCaps[0] + kCaps[1] + kCaps[2]) + 7) & ~int64_t(7));
+    if ((e = cudaMalloc(&d.scan.gmax, (size_t)N * 3 * d.scan.gcap * 4)) != cudaSuccess)
+      return bad(e, "scan group maxima");
+    if ((e = cudaMalloc(&d.scan.bound, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "scan bounds");
+    if ((e = cudaMalloc(&d.scan.count, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "scan counts");
+    if ((e = cudaMalloc(&d.scan.surv, (size_t)N * d.scan.surv_stride * 2)) != cudaSuccess)
+      return bad(e, "scan survivors");
+    if ((e = cudaMalloc(&d.sel_done, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "select flags");
+    if ((e = cudaMemset(d.sel_done, 0, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "select flags");
+    if ((e = cudaMalloc(&d.sel_epoch, 4)) != cudaSuccess) return bad(e, "select epoch");
+    if ((e = cudaMemset(d.sel_epoch, 0, 4)) != cudaSuccess) return bad(e, "select epoch");
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if ((e = cudaMalloc(&d.skut_scratch, (size_t)sms * skut_simt_scratch_floats(S) * 4)) != cudaSuccess)
+      return bad(e, "skut scratch");
+    if ((e = cudaStreamCreateWithFlags(&c->slot_stream[k], cudaStreamNonBlocking)) != cudaSuccess)
+      return bad(e, "slot stream");
+    if ((e = cudaEventCreateWithFlags(&c->ev_caller[k], cudaEventDisableTiming)) != cudaSuccess)
+      return bad(e, "event");
+  }
   if ((e = cudaMalloc(&c->idx, (size_t)N * S * 4)) != cudaSuccess) return bad(e, "idx");
-  if ((e = cudaMalloc(&c->sel_done, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "select flags");
-  if ((e = cudaMemset(c->sel_done, 0, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "select flags");
-  if ((e = cudaMalloc(&c->sel_epoch, 4)) != cudaSuccess) return bad(e, "select epoch");
-  if ((e = cudaMemset(c->sel_epoch, 0, 4)) != cudaSuccess) return bad(e, "select epoch");
   if ((e = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking)) != cudaSuccess)
     return bad(e, "capture stream");
   if ((e = cudaMalloc(&c->logits, (size_t)N * kHeads * 4)) != cudaSuccess) return bad(e, "logits");
@@ -454,12 +482,6 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
   }
   if ((e = cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking)) != cudaSuccess)
     return bad(e, "d2h stream");
-  {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    size_t n = (size_t)sms * skut_simt_scratch_floats(S);
-    if ((e = cudaMalloc(&c->skut_scratch, n * 4)) != cudaSuccess) return bad(e, "skut scratch");
-  }
   *out = c;
   return TAV2_OK;
 }
@@ -986,7 +1008,7 @@ int tav2_stage(tav2_ctx* c, const tav2_request* reqs, int n_req, void* stream, i
   CU(cudaStreamWaitEvent(s, c->ev_staged[slot], 0));
   c->plans[slot] = p;
   c->cur = slot;
-  c->next_slot = slot ^ 1;
+  c->next_slot = (slot + 1) % tav2_ctx::kStageSlots;
   c->staged = true;
   if (n_items) *n_items = N;
   return TAV2_OK;
@@ -1017,7 +1039,7 @@ SelFlags next_sel(tav2_ctx* c) {
 #ifdef TAV2_NO_SELFLAGS
   return SelFlags{nullptr, nullptr, 0};
 #endif
-  return SelFlags{c->sel_done, c->sel_epoch, device_sms()};
+  return SelFlags{c->cur_dv().sel_done, c->cur_dv().sel_epoch, device_sms()};
 }
 
 // NN selection (both precision modes: the scan's survivors are re-scored with
@@ -1025,12 +1047,12 @@ SelFlags next_sel(tav2_ctx* c) {
 int run_nn(tav2_ctx* c, int32_t* idx, double* scores, cudaStream_t s, SelFlags sel = {nullptr, 0, 0}) {
   Staged st = staged_view(c);
   CU(timed(c, "prep", s, [&] {
-    return launch_prep(st, c->params_ok ? &c->params : nullptr, s, sel.done ? c->sel_epoch : nullptr);
+    return launch_prep(st, c->params_ok ? &c->params : nullptr, s, sel.done ? c->cur_dv().sel_epoch : nullptr);
   }));
-  CU(timed(c, "nn_scan1", s, [&] { return launch_nn_scan(st, c->nn, c->scan, 1, s); }));
-  CU(timed(c, "nn_bound", s, [&] { return launch_nn_bound(st, c->nn, c->scan, s); }));
-  CU(timed(c, "nn_scan2", s, [&] { return launch_nn_scan(st, c->nn, c->scan, 2, s); }));
-  CU(timed(c, "nn_select", s, [&] { return launch_nn_select(st, c->nn, c->scan, idx, scores, sel, s); }));
+  CU(timed(c, "nn_scan1", s, [&] { return launch_nn_scan(st, c->nn, c->cur_dv().scan, 1, s); }));
+  CU(timed(c, "nn_bound", s, [&] { return launch_nn_bound(st, c->nn, c->cur_dv().scan, s); }));
+  CU(timed(c, "nn_scan2", s, [&] { return launch_nn_scan(st, c->nn, c->cur_dv().scan, 2, s); }));
+  CU(timed(c, "nn_select", s, [&] { return launch_nn_select(st, c->nn, c->cur_dv().scan, idx, scores, sel, s); }));
   return TAV2_OK;
 }
 
@@ -1073,7 +1095,7 @@ int run_score(tav2_ctx* c, int mode, const int32_t* idx, float* logits, float* p
   }
   CU(timed(c, "skut_simt", s, [&] {
     return launch_skut_simt(c->params, c->nn, &st, idx, nullptr, nullptr, st.n_items,
-                            c->skut_scratch, nullptr, logits, pooled, (int)tc_ok, s);
+                            c->cur_dv().skut_scratch, nullptr, logits, pooled, (int)tc_ok, s);
   }));
   return TAV2_OK;
 }
@@ -1227,7 +1249,7 @@ int tav2_forward(tav2_ctx* c, int mode, const float* features_dev, const uint8_t
     return TAV2_OK;
   }
   CU(launch_skut_simt(c->params, c->nn, nullptr, nullptr, features_dev, mask_dev, n,
-                      c->skut_scratch, u_dev, nullptr, nullptr, (int)(c->cs_bound <= 60.0),
+                      c->cur_dv().skut_scratch, u_dev, nullptr, nullptr, (int)(c->cs_bound <= 60.0),
                       (cudaStream_t)stream));
   return TAV2_OK;
 }
@@ -1247,7 +1269,7 @@ int tav2_forward_masked(tav2_ctx* c, int mode, const float* features_dev, const 
   // drop a row's own key, so the diagonal-based shifts do not apply); it
   // meets both modes' tolerances
   const long long S = c->nn.seq_len;
-  CU(launch_skut_simt(c->params, c->nn, nullptr, nullptr, features_dev, mask_dev, n, c->skut_scratch, u_dev,
+  CU(launch_skut_simt(c->params, c->nn, nullptr, nullptr, features_dev, mask_dev, n, c->cur_dv().skut_scratch, u_dev,
                       nullptr, nullptr, 0, (cudaStream_t)stream, extra_dev, extra_batched ? S * S : 0));
   return TAV2_OK;
 }
@@ -1280,10 +1302,16 @@ int tav2_rank_submit(tav2_ctx* c, const tav2_request* reqs, int n_req, int mode,
   const int slot = c->next_slot;
   // the slot's pinned outputs are free once its previous rank finished
   CU(cudaEventSynchronize(c->ev_done[slot]));
+  // Each slot's chain runs on the slot's own compute stream (after the
+  // caller's stream: work the caller enqueued first stays first), so two
+  // submitted requests' kernels can overlap: request i+1's NN chain fills
+  // the SMs request i's SKUT tail frees (slot-private derived buffers).
+  cudaStream_t s = c->slot_stream[slot];
+  CU(cudaEventRecord(c->ev_caller[slot], (cudaStream_t)stream));
+  CU(cudaStreamWaitEvent(s, c->ev_caller[slot], 0));
   int32_t n = 0;
-  int rc = tav2_stage(c, reqs, n_req, stream, &n);
+  int rc = tav2_stage(c, reqs, n_req, s, &n);
   if (rc) return rc;
-  cudaStream_t s = (cudaStream_t)stream;
   if ((rc = run_chain(c, mode, c->logits_s[slot], c->idx_s[slot], s))) return rc;
   // result copies on the d2h stream: the compute stream goes straight on to
   // the next request's kernels
@@ -1335,6 +1363,8 @@ int tav2_rank(tav2_ctx* c, const tav2_request* reqs, int n_req, int mode, float*
 }
 
 int tav2_last_launch_count(const tav2_ctx* c) { return c ? c->launches : 0; }
+
+int tav2_stage_slots(void) { return TAV2_STAGE_SLOTS; }
 
 int tav2_graph_info(const void* ctx, int32_t* n_graphs, int32_t* broken) {
   const tav2_ctx* c = static_cast<const tav2_ctx*>(ctx);

@@ -438,16 +438,18 @@ class Engine:
                        latencies: list | None = None):
         """Serving loop (tav2_rank_submit / tav2_rank_collect): every batch of
         (user, candidates, ctx) requests is submitted -- host packing into one
-        of two pinned staging slots, H2D copy, kernels and result copies all
-        enqueued -- before the previous batch is collected, so the host work
-        and H2D of batch i+1 overlap the kernels of batch i.  Returns the list
+        of the pinned staging slots (tav2_stage_slots), H2D copy, kernels and
+        result copies all enqueued -- while up to slots - 1 earlier batches are
+        still in flight, so the host work, H2D and NN kernels of batch i+1
+        overlap the kernels of batch i.  Returns the list
         of logits arrays (with indices if requested) in batch order;
         `latencies` (optional list) receives each batch's submit-to-collect
         wall time in seconds."""
         if self.model is None:
             raise ValidationError("no model loaded")
         mode_i = self._mode(mode)
-        out, pending = [], None
+        out, pending = [], []
+        depth = self._lib.tav2_stage_slots() - 1  # submits kept in flight beyond the newest
 
         def collect(p):
             slot, n, _pack, t0 = p
@@ -463,9 +465,8 @@ class Engine:
             reqs = list(reqs)
             ch = list(self._chunks(reqs))
             if len(ch) > 1 or (ch and ch[0][1]):  # overflow: drain, then the counted slow path
-                if pending is not None:
-                    collect(pending)
-                    pending = None
+                while pending:
+                    collect(pending.pop(0))
                 out.append(self.rank_requests(reqs, mode=mode, return_indices=return_indices))
                 if latencies is not None:
                     latencies.append(time.perf_counter() - t0)
@@ -475,11 +476,11 @@ class Engine:
             slot = ctypes.c_int32()
             N.check(self._lib.tav2_rank_submit(self._ctx, pack.arr, len(reqs), mode_i, int(return_indices),
                                                self.stream(), ctypes.byref(slot)))
-            if pending is not None:
-                collect(pending)
-            pending = (slot.value, n, pack, t0)
-        if pending is not None:
-            collect(pending)
+            pending.append((slot.value, n, pack, t0))
+            if len(pending) > depth:
+                collect(pending.pop(0))
+        while pending:
+            collect(pending.pop(0))
         return out
 
     # ---- the serving loop's primitives (serving.PipelinedHandler) ----

@@ -394,15 +394,15 @@ def batcher_handler(engines, store, mode: str = "bf16", stats: LatencyStats | No
 
 
 class PipelinedHandler:
-    """Pipelined ``DynamicBatcher`` handler over one engine's two staging
+    """Pipelined ``DynamicBatcher`` handler over one engine's staging
     slots (tav2_rank_submit / tav2_rank_wait / tav2_rank_collect).
 
     ``handler(batch, worker_index)`` packs the batch and submits its whole
     rank (staging copy, kernels, result copy) and returns at once; a
     completion thread waits for each submitted rank in order, collects its
     logits and completes the Pending results.  So while batch i runs on the
-    GPU, the batcher already forms, packs and stages batch i+1.  At most two
-    ranks are in flight (one per staging slot).  A batch beyond the engine
+    GPU, the batcher already forms, packs and stages batch i+1.  At most
+    tav2_stage_slots() ranks are in flight (one per staging slot).  A batch beyond the engine
     capacity takes the engine's counted overflow path synchronously.
 
     Stages recorded in ``stats``: queueing (enqueue -> handler), batch_prep
@@ -414,7 +414,7 @@ class PipelinedHandler:
         self.store = store
         self.mode = mode
         self.stats = stats
-        self._slots = threading.Semaphore(2)
+        self._slots = threading.Semaphore(engine._lib.tav2_stage_slots())
         self._inflight: queue.Queue = queue.Queue()
         self._submit_lock = threading.Lock()
         self._thread = threading.Thread(target=self._complete, daemon=True)
