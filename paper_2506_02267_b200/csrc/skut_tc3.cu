@@ -64,7 +64,7 @@ constexpr int kW3Layer = kImg3WA + kImg3WB;  // 48 KB per layer
 __device__ long long* g_dbg_skut3 = nullptr;
 
 struct T3Bars {
-  uint64_t simt[2], mma[2], kvready, kvfree, wfull;
+  uint64_t simt[2], mma[2], kvready, kvfree, wfull, order;
 };
 __shared__ __align__(8) T3Bars t3;
 
@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     mbar_init(&t3.kvready, kT3Threads);
     mbar_init(&t3.kvfree, 2);
     mbar_init(&t3.wfull, 1);
+    mbar_init(&t3.order, 1);
     mbar_fence_init();
   }
   if (warp == 0) tmem_alloc<512>(&taddr_s);
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   const bool issuer = (tid & 127) == 0;  // debug stamps only
   const bool issue_warp = q == 0;         // warp 4t issues tile t's MMAs (warp-collective)
   long long* dbg = (kDebug && blockIdx.x == 0 && issuer && g_dbg_skut3) ? g_dbg_skut3 + 32 * (tid >> 7) : nullptr;
-  long long t_last = 0;
+  long long t_last = 0, dbg_m3 = 0;
   auto stamp = [&](int id) {
     if (kDebug && dbg) {
       const long long now = clock64();
@@ -243,7 +244,22 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   const uint32_t cA = lanebase + kCA;
   const bool in_seq = mapped && r < S;
   uint32_t n_mma = 0, n_kv = 0;
-  uint32_t ph_simt = 0;
+  uint32_t ph_simt = 0, ph_order = 0;
+  // Tile 1 (the late rows: twice the attention work) is the critical path;
+  // the two tiles share the SM's tensor pipe and issue M1 and M2 at the
+  // same moments, so tile 0's issuer waits until tile 1's MMAs of that
+  // phase are queued (tile 0 has slack: it waits at kvfree / the pool).
+  auto order_after_tile1 = [&]() {
+#ifndef TAV2_NO_TILE_ORDER
+    if (t == 0) {
+      mbar_wait(&t3.order, ph_order);
+      ph_order ^= 1u;
+    } else {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&t3.order);
+    }
+#endif
+  };
   auto wait_mma = [&]() {
     __syncwarp();
     mbar_wait_sleep(&t3.mma[t], n_mma & 1);
@@ -414,8 +430,10 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       if (issue_warp) {  // M1: [Q' | V'] = A [Wqk | Wvo]   (N = 128, K = 64)
         issuer_wait_simt();
         stamp(28);
+        if (t == 0) order_after_tile1();
         t3_mma3<4>(R + kCD, R + kCA, 32, wa(L), wa(L) + kImg3WA / 2, 128 * 16, t3_idesc<F16>(128, 128));
         commit_w(&t3.mma[t]);
+        if (t == 1) order_after_tile1();
       }
       stamp(4);
       // ---- P2: Q' -> A, V' -> smem (MN-major) ----
@@ -484,8 +502,10 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       if (issue_warp) {  // M2: S = Q' K^T   (N = keys of this tile, K = 64)
         mbar_wait(&t3.kvready, n_kv & 1);
         fence_after();
+        if (t == 0) order_after_tile1();
         t3_mma3<4>(R + kCD, R + kCA, 32, khi, klo, S_pad * 16, t3_idesc<F16>(128, NK));
         commit_w(&t3.mma[t]);
+        if (t == 1) order_after_tile1();
       }
       stamp(7);
       // ---- P3: causal key-masked softmax -> P (bf16 hi/lo, in place over S) ----
@@ -587,6 +607,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         stamp(29);
         const uint32_t id = t3_idesc<F16>(128, 64, 0, 1);
         const int nk16 = NK / 16;  // <= 12 (S_pad <= 192); unrolled, warp-uniform bound
+        const long long t_iss = kDebug ? clock64() : 0;
 #pragma unroll
         for (int j = 0; j < 12; ++j) {
           if (j < nk16) {
@@ -599,6 +620,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         }
         commit_w(&t3.mma[t]);
         commit_w(&t3.kvfree);  // this tile no longer reads K / V' of this layer
+        if (kDebug) dbg_m3 += clock64() - t_iss;  // the M3 issue alone, no stamp in between
       }
       stamp(10);
       ++n_kv;
@@ -748,6 +770,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     // (z_s / hid_s / red_s are rewritten only after the next item's barriers)
     stamp(23);
   }
+  if (kDebug && dbg) dbg[27] += dbg_m3;
   fence_before();
   __syncthreads();
   if (warp == 0) tmem_free<512>(0u);

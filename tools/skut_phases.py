@@ -17,7 +17,7 @@ NAMES = ["encode", "encode barrier", "kvfree wait", "P1 LN1->A,K", "issue M1 QV'
          "P2 Q'->A,V'->smem", "kvready+issue M2 S", "wait M2", "P3 softmax", "issue M3 PV",
          "wait M3", "P4 x+=O'/l,LN2", "issue M4 W1", "wait M4", "P5 ReLU", "issue M5 W2", "wait M5",
          "P6 x+=", "pool x->A", "issue pool", "wait pool", "max-pool+barriers", "head",
-         "P3a kvready wait", "P3b exp loop", "P3c zero fill", "(unused)",
+         "P3a kvready wait", "P3b exp loop", "P3c zero fill", "(M3 issue alone, in 10)",
          "M1 simt wait", "M3 simt wait", "M4 simt wait"]
 
 n_cand = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
