@@ -116,7 +116,7 @@ __device__ __forceinline__ void commit_mc_w(uint64_t* bar, uint16_t mask) {
 }
 
 struct T4Bars {
-  uint64_t simt[2], mma[2], m3[2], kvready, kvfree, wfull, poolready[2];
+  uint64_t simt[2], mma[2], m3[2], kvready, kvfree, wfull, poolready[2], order;
 };
 __shared__ T4Bars t4;
 
@@ -254,6 +254,7 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
     mbar_init(&t4.kvready, CL * kT4Threads);
     mbar_init(&t4.kvfree, 2 * CL);
     mbar_init(&t4.wfull, 1);
+    mbar_init(&t4.order, 1);
     mbar_init(&t4.poolready[0], kDModel + 1);
     mbar_init(&t4.poolready[1], kDModel + 1);
     mbar_fence_init();
@@ -299,7 +300,23 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
   const uint32_t R = 256u * t;
   const uint32_t lanebase = ((uint32_t)(32 * q) << 16) + R;
   const uint32_t cA = lanebase + k4CA;
-  uint32_t n_mma = 0, n_m3 = 0, n_kv = 0, ph_simt = 0;
+  uint32_t n_mma = 0, n_m3 = 0, n_kv = 0, ph_simt = 0, ph_order = 0;
+  // tile 1 (the later rows: more keys) is the critical path; tile 0's
+  // issuer queues its M1 / first M2 after tile 1's (as skut_tc3)
+  // (CL = 2: measured slower -- the cluster-wide kvready couples all four
+  // tiles, so no single tile is critical)
+  auto order_after_tile1 = [&]() {
+#ifndef TAV2_NO_TILE_ORDER
+    if (CL == 2) return;
+    if (t == 0) {
+      mbar_wait(&t4.order, ph_order);
+      ph_order ^= 1u;
+    } else {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&t4.order);
+    }
+#endif
+  };
   auto wait_mma = [&]() {
     __syncwarp();
     mbar_wait_sleep(&t4.mma[t], n_mma & 1);
@@ -419,8 +436,10 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
       }
       if (issue_warp) {  // M1: Q' = A Wqk   (N = 64: the first 64 rows of the [Wqk|Wvo] image)
         issuer_wait_simt();
+        if (t == 0) order_after_tile1();
         t4_mma3<4>(R + k4CD, R + k4CA, 32, wa(L), wa(L) + kImg3WA / 2, 128 * 16, t4_idesc<F16>(128, 64));
         commit_w(&t4.mma[t]);
+        if (t == 1) order_after_tile1();
       }
       // ---- P2: Q' -> A; ||q'||^2 (and s_rr = q'_r . a_r in fp32 mode) ----
       wait_mma();
@@ -470,8 +489,10 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
         mbar_wait_cl(&t4.kvready, n_kv & 1);  // every key of this layer in place (both CTAs)
         fence_after();
         const int cc = NK < kT4Chunk ? NK : kT4Chunk;
+        if (t == 0) order_after_tile1();
         t4_mma3<4>(R + k4CD, R + k4CA, 32, khi, klo, S_pad * 16, t4_idesc<F16>(128, cc));
         commit_w(&t4.mma[t]);
+        if (t == 1) order_after_tile1();
       }
       // ---- P3: causal key-masked softmax over key chunks; O'' = P a in TMEM ----
       // Single pass with the Cauchy-Schwarz shift m' = ||q'_r|| max_j ||a_j||
