@@ -27,6 +27,7 @@ prints the same metric with per-request p50/p99.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import multiprocessing as mp
 import os
@@ -397,6 +398,8 @@ def run_gpu(args, rank, world, local_rank):
     eng.rank_pipelined([packed[i % pool_n] for i in range(args.warmup)], mode=mode)
     barrier()
     torch.cuda.synchronize()
+    gc.collect()  # the start-up heap (generated requests) frozen, as a serving process does
+    gc.freeze()
     lat = []
     t0 = time.perf_counter()
     eng.rank_pipelined([packed[i % pool_n] for i in range(args.steps)], mode=mode, latencies=lat)
@@ -531,8 +534,24 @@ def _open_loop(eng, pool, mode, rate, seconds=2.0):
     try:
         for i in range(20):  # warm the loop
             b.submit(payloads[i % len(payloads)], n_item).done.wait(10)
+        # untimed warm-up at the target rate (0.5 s): the measured window
+        # starts in steady state (the first paced second showed one-off
+        # multi-ms stalls: thread start-up, allocator and graph warm-up)
+        t0 = time.perf_counter()
+        warm = []
+        for i in range(max(10, int(rate * 0.5))):
+            dt = t0 + i / rate - time.perf_counter()
+            if dt > 0:
+                time.sleep(dt)
+            warm.append(b.submit(payloads[i % len(payloads)], n_item))
+        for p in warm:
+            p.done.wait(30)
         stats = S.LatencyStats(window=3600.0)
         h.stats = stats
+        # a serving process freezes its start-up heap: a full collection of
+        # the generated request objects otherwise lands in the timed window
+        gc.collect()
+        gc.freeze()
         t0 = time.perf_counter()
         ps = []
         for i in range(n):

@@ -1,0 +1,24 @@
+"""Open-loop latency at fixed arrival rates through DynamicBatcher +
+PipelinedHandler (bench.py's open_loop leg), repeated, with the slowest
+requests' arrival times -- are tail latencies steady-state or one-off
+stalls?"""
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import bench  # noqa: E402
+import paper_2506_02267_b200 as P  # noqa: E402
+from paper_2506_02267_b200.runtime import Capacity, Engine  # noqa: E402
+
+nn = P.NNConfig()
+model = P.RankingModel.init(P.ModelConfig.for_nn(nn), seed=0)
+eng = Engine(model, capacity=Capacity(1, 1000, 16896))
+pool = [[r] for r in P.synthetic_requests(4, 1000, 16384, 256, 256, seed=0)]
+for frac in (0.5, 0.5, 0.7, 0.85):
+    rate = frac * 4.6e6 / 1000
+    r = bench._open_loop(eng, pool, "bf16", rate, seconds=2.0)
+    print(f"rate {rate:.0f} req/s: p50 {r['p50_request_ms']} p99 {r['p99_request_ms']} ms, achieved "
+          f"{r['achieved_cand_s'] / 1e6:.2f}M cand/s; queueing p99 {r['stages_ms']['queueing']['p99']} "
+          f"forward p99 {r['stages_ms']['forward']['p99']}", flush=True)
