@@ -160,7 +160,7 @@ int tav2_rank_submit(tav2_ctx* ctx, const tav2_request* reqs, int n_req, int mod
                      void* stream, int32_t* slot_out);
 
 /* Number of staging slots (submits that may be in flight at once). */
-#define TAV2_STAGE_SLOTS 3
+#define TAV2_STAGE_SLOTS 4
 int tav2_stage_slots(void);
 
 /* Block until a submitted rank's kernels and result copies finished, without
