@@ -300,6 +300,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   // the gather's index chain (idx -> token) of the next candidate is resolved
   // during the last layer of the current one
   int tok_pf = (in_seq && (int)blockIdx.x < n) ? slot_token(st, nn, idx, blockIdx.x, r) : -1;
+  int pf_idx = -1, pf_req = 0, pf_off = 0;  // the next item's index chain, in flight
+  const int r_src = r < nn.seg_start[1] ? 0 : (r < nn.seg_start[3] ? 1 : 2);  // this row's source
   // Tile 1's rows' position embeddings stay in TMEM for the kernel's
   // lifetime: tile 0's columns [128, 192) are never used by tile 0 (its
   // scores span <= 96 keys, its widest output 128 columns), and tile 1's
@@ -388,7 +390,17 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
           griddep_wait();
           sel_all = true;
         }
+#ifdef TAV2_OLD_PF
         tok_pf = (in_seq && nx < n) ? slot_token(st, nn, idx, nx, r) : -1;
+#else
+        // The next item's index chain (slot_token: idx -> item_req -> req
+        // tok_off) in three steps whose loads are consumed a phase later:
+        // here idx and item_req (independent), the request's token offset
+        // after P2, the sum at the pool.  (slot_token here put its dependent
+        // L2 round trips on the critical tile's path at the layer top.)
+        pf_idx = (in_seq && nx < n) ? idx[(size_t)nx * S + r] : -1;
+        pf_req = nx < n ? st.item_req[nx] : 0;
+#endif
       }
       // ---- P1: a = LN1(x) -> A (TMEM) and K = a (smem); ||a||^2 -> kmax ----
       if (n_kv > 0) mbar_wait_sleep(&t3.kvfree, (n_kv - 1) & 1);  // both tiles' previous P.V retired
@@ -441,6 +453,9 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       }
       stamp(4);
       // ---- P2: Q' -> A, V' -> smem (MN-major) ----
+#ifndef TAV2_OLD_PF
+      if (L == NL - 1 && in_seq) pf_off = st.req[pf_req].tok_off[r_src];
+#endif
       wait_mma();
       stamp(5);
       float qn2 = 0.0f, s_rr = 0.0f;
@@ -725,6 +740,9 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         if (lane == 0) red_s[warp][j] = v;
       }
     }
+#ifndef TAV2_OLD_PF
+    tok_pf = pf_idx >= 0 ? pf_off + pf_idx : -1;
+#endif
     {  // the next item's token row (tok_pf resolved in the last layer), under
        // the head; always overwritten (row 0 for padding slots) so tfv is dead
        // through the layers
