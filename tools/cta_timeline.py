@@ -64,6 +64,11 @@ if sel.any():
           [(int(i) // 3, int(i) % 3, int(rec_n[i])) for i in np.argsort(-rec_t)[:5]])
     st_t, bi_t = t[6, 2], t[7, 0]
     for src in range(3):
+        m = sel & (np.arange(len(rec_t)) % 3 == src)
+        if m.any():
+            print(f"  source {src}: survivors med {np.median(rec_n[m]):.0f} p90 {np.percentile(rec_n[m], 90):.0f} "
+                  f"max {rec_n[m].max()}, warp time med {np.median(rec_t[m]) / 1e3:.2f} max {rec_t[m].max() / 1e3:.2f} us")
+    for src in range(3):
         m = sel & (np.arange(len(rec_t)) % 3 == src) & (st_t > 0)
         if m.any():
             print(f"  source {src}: warps {m.sum()} total med {np.median(rec_t[m]) / 1e3:.2f} us, keys staged+scored "
