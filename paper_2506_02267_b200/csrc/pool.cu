@@ -50,6 +50,95 @@ __global__ void __launch_bounds__(256) pool_kernel(const float* U, const uint8_t
   }
 }
 
+// CTR head (trainer.py:361-366) over the pooled vectors skut_tc3 wrote:
+// z = [pooled | unit(c) | ctx] (104), h = ReLU(z W1 + b1), logits = h W2 + b2.
+// Warp per candidate, W1 / b1 / W2 staged in shared memory once per CTA.
+// The summation order is skut_tc3's former in-kernel head (two halves of 52
+// inputs, even / odd accumulators, then an 8-lane tree per head), so the
+// logits are bit-identical to it.  Split out of the transformer kernel: its
+// ~2.9K cycles per candidate sat on tile 0 at every candidate boundary and
+// delayed the next candidate's first K/V handover to the critical tile.
+// spin (the pooled workspace of a fused run): no wait for the whole
+// transformer grid -- each lane polls its two pooled entries until they are
+// no longer kPooledEmpty (a value written by a plain store is read whole, so
+// no flag and no fence is needed), so the heads of the early candidates run
+// on the SMs the transformer's tail frees; the entries are reset to
+// kPooledEmpty after use.  Otherwise griddep_wait up front.
+constexpr int kHeadWarps = 8;
+__global__ void __launch_bounds__(32 * kHeadWarps) head_kernel(Params p, Staged st, float* pooled, int n,
+                                                              float* logits, int spin) {
+  __shared__ float w1_s[(kDModel + kEmbed + kCtx) * kHidden];  // 26 KB
+  __shared__ float w2_s[kHidden * kHeads];
+  __shared__ float b1_s[kHidden];
+  __shared__ float z_s[kHeadWarps][kDModel + kEmbed + kCtx];
+  __shared__ float hid_s[kHeadWarps][kHidden];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < (kDModel + kEmbed + kCtx) * kHidden; i += 32 * kHeadWarps) w1_s[i] = p.head_w1[i];
+  for (int i = tid; i < kHidden * kHeads; i += 32 * kHeadWarps) w2_s[i] = p.head_w2[i];
+  if (tid < kHidden) b1_s[tid] = p.head_b1[tid];
+  griddep_launch();
+  if (!spin) griddep_wait();  // pooled vectors written
+  __syncthreads();
+  for (int item = blockIdx.x * kHeadWarps + warp; item < n; item += gridDim.x * kHeadWarps) {
+    float* z = z_s[warp];
+    float* pv = pooled + (size_t)item * kDModel;
+    float v0, v1;
+    if (spin) {
+      const volatile uint32_t* pu = reinterpret_cast<const volatile uint32_t*>(pv);
+      uint32_t u0, u1;
+      while ((u0 = pu[lane]) == kPooledEmpty || (u1 = pu[lane + 32]) == kPooledEmpty) __nanosleep(64);
+      v0 = __uint_as_float(u0);
+      v1 = __uint_as_float(u1);
+      pv[lane] = __uint_as_float(kPooledEmpty);  // for the next run
+      pv[lane + 32] = __uint_as_float(kPooledEmpty);
+    } else {
+      v0 = pv[lane];
+      v1 = pv[lane + 32];
+    }
+    z[lane] = v0;
+    z[lane + 32] = v1;
+    z[kDModel + lane] = st.cand_unit[(size_t)item * kEmbed + lane];
+    if (lane < kCtx) z[kDModel + kEmbed + lane] = st.ctx[st.item_req[item] * kCtx + lane];
+    __syncwarp();
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {  // hidden units lane, lane + 32
+      const int hu = lane + 32 * hh;
+      float hp[2];
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 52; i += 2) {
+          a0 = fmaf(z[52 * part + i], w1_s[(52 * part + i) * kHidden + hu], a0);
+          a1 = fmaf(z[52 * part + i + 1], w1_s[(52 * part + i + 1) * kHidden + hu], a1);
+        }
+        hp[part] = a0 + a1;
+      }
+      hid_s[warp][hu] = fmaxf((hp[0] + hp[1]) + b1_s[hu], 0.0f);
+    }
+    __syncwarp();
+    {  // lane: head (lane & 3), hidden slice 8 * (lane >> 2) .. + 8
+      const int hd = lane & 3, j0 = 8 * (lane >> 2);
+      float o = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o = fmaf(hid_s[warp][j0 + j], w2_s[(j0 + j) * kHeads + hd], o);
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) o += __shfl_xor_sync(0xffffffffu, o, off);
+      if (lane < kHeads) logits[(size_t)item * kHeads + lane] = o + __ldg(p.head_b2 + lane);
+    }
+    __syncwarp();
+  }
+  // completion implies the transformer grid's (the next kernel's griddep_wait)
+  if (spin) griddep_wait();
+}
+
+cudaError_t launch_head(const Params& p, const Staged& st, float* pooled, int n, float* logits, bool spin,
+                        cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = (n + kHeadWarps - 1) / kHeadWarps;  // a warp per candidate
+  return launch_pdl(head_kernel, dim3(blocks), dim3(32 * kHeadWarps), 0, s, p, st, pooled, n, logits, (int)spin);
+}
+
 cudaError_t launch_pool(const float* U, const uint8_t* mask, const float* out_linear, int n, int S, float* pooled,
                         cudaStream_t s) {
   if (n <= 0) return cudaSuccess;

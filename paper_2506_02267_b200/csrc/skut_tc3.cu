@@ -1,6 +1,8 @@
 // SKUT v3 on the 5th-gen tensor cores (S <= 192, <= 2 layers): gather +
 // Eq. 4 encode, 2 x pre-norm causal transformer layers, linear + masked
-// max-pool and the CTR head, one candidate per CTA iteration (persistent).
+// max-pool, one candidate per CTA iteration (persistent).  The CTR head on
+// the pooled vectors is head_kernel (pool.cu), which starts per candidate
+// as the pooled vectors land.
 //
 // Reference: encoder.py:161-188 (encode_batch), :196-211 (layer_norm,
 // masked_softmax), :221-246 / :314-462 (forward_reference / forward_fused),
@@ -172,9 +174,6 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   __shared__ uint32_t valid_w[8];  // key-validity bitmask, bit r of word r/32
   __shared__ __align__(16) float lnp_s[2][4][kDModel];
   __shared__ float red_s[kT3Warps][kDModel];
-  __shared__ float z_s[kDModel + kEmbed + kCtx];
-  __shared__ float hpart_s[4][kHidden];
-  __shared__ float hid_s[kHidden];
   __shared__ int any_s;
   __shared__ unsigned kmax_s[2];
 
@@ -376,9 +375,6 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       }
     }
     stamp(0);
-#ifdef TAV2_HEAD_ALL
-    named_bar_sync(1, kT3Threads);  // valid_w complete
-#endif
     // (no barrier: valid_w is read only in the softmax, after kvready -- every
     // thread arrives there after its own validity bits)
     stamp(1);
@@ -752,90 +748,15 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     }
     named_bar_sync(1, kT3Threads);
     stamp(22);
-#ifdef TAV2_HEAD_ALL
-    // head (trainer.py:361-365): z = [pooled | unit(c) | ctx]; 4 threads per hidden unit
+    // pooled vector -> pooled_out (the CTR head is head_kernel, pool.cu, which
+    // may already be polling it: plain stores, no fence)
     if (tid < kDModel) {
       float v = -INFINITY;
 #pragma unroll
       for (int w = 0; w < kT3Warps; ++w) v = fmaxf(v, red_s[w][tid]);
-      v = any_s ? v : 0.0f;  // empty user -> pooled = 0 (trainer.py:358-359)
-      z_s[tid] = v;
-      if (pooled_out) pooled_out[(size_t)item * kDModel + tid] = v;
-    } else if (tid < kDModel + kEmbed) {
-      z_s[tid] = st.cand_unit[(size_t)item * kEmbed + tid - kDModel];
-    } else if (tid < kDModel + kEmbed + kCtx) {
-      z_s[tid] = st.ctx[st.item_req[item] * kCtx + tid - kDModel - kEmbed];
+      pooled_out[(size_t)item * kDModel + tid] = any_s ? v : 0.0f;  // empty user -> 0 (trainer.py:358-359)
     }
-    named_bar_sync(1, kT3Threads);
-    {
-      const int hu = tid & 63, part = tid >> 6;  // inputs [26 part, 26 part + 26)
-      float acc = 0.0f;
-#pragma unroll
-      for (int i = 0; i < 26; ++i) acc = fmaf(z_s[26 * part + i], __ldg(p.head_w1 + (26 * part + i) * kHidden + hu), acc);
-      hpart_s[part][hu] = acc;
-    }
-    named_bar_sync(1, kT3Threads);
-    if (tid < kHidden) {
-      const float hsum = ((hpart_s[0][tid] + hpart_s[1][tid]) + (hpart_s[2][tid] + hpart_s[3][tid])) +
-                         __ldg(p.head_b1 + tid);
-      hid_s[tid] = fmaxf(hsum, 0.0f);
-    }
-    named_bar_sync(1, kT3Threads);
-    if (warp == 0) {  // lane: head (lane & 3), hidden slice 8 * (lane >> 2) .. + 8
-      const int hd = lane & 3, j0 = 8 * (lane >> 2);
-      float o = 0.0f;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) o = fmaf(hid_s[j0 + j], __ldg(p.head_w2 + (j0 + j) * kHeads + hd), o);
-#pragma unroll
-      for (int off = 4; off < 32; off <<= 1) o += __shfl_xor_sync(0xffffffffu, o, off);
-      if (lane < kHeads) logits[(size_t)item * kHeads + lane] = o + __ldg(p.head_b2 + lane);
-    }
-#else
-    // The head (trainer.py:361-365) runs on tile 0's 128 threads only (named
-    // barrier 2): tile 1 -- the critical path, the late rows -- goes straight
-    // on to the next item's gather and first layer while tile 0, which has
-    // slack (it otherwise waits at kvfree and at the pool barrier), finishes
-    // this item.  red_s / z_s / hpart_s / hid_s are rewritten only after the
-    // next item's pool barriers, which tile 0 reaches after this head.
-    if (t == 0) {
-      if (tid < kDModel) {
-        float v = -INFINITY;
-#pragma unroll
-        for (int w = 0; w < kT3Warps; ++w) v = fmaxf(v, red_s[w][tid]);
-        v = any_s ? v : 0.0f;  // empty user -> pooled = 0 (trainer.py:358-359)
-        z_s[tid] = v;
-        if (pooled_out) pooled_out[(size_t)item * kDModel + tid] = v;
-      } else if (tid < kDModel + kEmbed) {
-        z_s[tid] = st.cand_unit[(size_t)item * kEmbed + tid - kDModel];
-      } else if (tid < kDModel + kEmbed + kCtx) {
-        z_s[tid] = st.ctx[st.item_req[item] * kCtx + tid - kDModel - kEmbed];
-      }
-      named_bar_sync(2, 128);
-      {  // z = [pooled | unit(c) | ctx] (104 inputs): 2 threads per hidden unit
-        const int hu = tid & 63, part = tid >> 6;  // inputs [52 part, 52 part + 52)
-        float a0 = 0.0f, a1 = 0.0f;
-#pragma unroll
-        for (int i = 0; i < 52; i += 2) {
-          a0 = fmaf(z_s[52 * part + i], __ldg(p.head_w1 + (52 * part + i) * kHidden + hu), a0);
-          a1 = fmaf(z_s[52 * part + i + 1], __ldg(p.head_w1 + (52 * part + i + 1) * kHidden + hu), a1);
-        }
-        hpart_s[part][hu] = a0 + a1;
-      }
-      named_bar_sync(2, 128);
-      if (tid < kHidden) hid_s[tid] = fmaxf((hpart_s[0][tid] + hpart_s[1][tid]) + __ldg(p.head_b1 + tid), 0.0f);
-      named_bar_sync(2, 128);
-      if (warp == 0) {  // lane: head (lane & 3), hidden slice 8 * (lane >> 2) .. + 8
-        const int hd = lane & 3, j0 = 8 * (lane >> 2);
-        float o = 0.0f;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) o = fmaf(hid_s[j0 + j], __ldg(p.head_w2 + (j0 + j) * kHeads + hd), o);
-#pragma unroll
-        for (int off = 4; off < 32; off <<= 1) o += __shfl_xor_sync(0xffffffffu, o, off);
-        if (lane < kHeads) logits[(size_t)item * kHeads + lane] = o + __ldg(p.head_b2 + lane);
-      }
-    }
-#endif
-    // (z_s / hid_s / red_s are rewritten only after the next item's barriers)
+    // (red_s is rewritten only after the next item's pool barrier)
     stamp(23);
   }
   if (kDebug && dbg) dbg[27] += dbg_m3;

@@ -140,6 +140,7 @@ struct tav2_ctx {
     uint32_t* sel_done = nullptr;   // per-(candidate, source) select flags (SelFlags)
     uint32_t* sel_epoch = nullptr;  // device word: the current run's flag epoch (prep bumps it)
     float* skut_scratch = nullptr;  // SIMT SKUT scratch
+    float* pooled = nullptr;        // [N, 64] skut_tc3 pooled vectors -> head_kernel
   };
   Derived dv[kStageSlots];
   cudaStream_t slot_stream[kStageSlots] = {};  // tav2_rank_submit compute streams
@@ -308,6 +309,7 @@ int free_all(tav2_ctx* c) {
     cudaFree(d.sel_done);
     cudaFree(d.sel_epoch);
     cudaFree(d.skut_scratch);
+    cudaFree(d.pooled);
   }
   for (int k = 0; k < tav2_ctx::kStageSlots; ++k) {
     if (c->slot_stream[k]) cudaStreamDestroy(c->slot_stream[k]);
@@ -467,6 +469,9 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if ((e = cudaMalloc(&d.skut_scratch, (size_t)sms * skut_simt_scratch_floats(S) * 4)) != cudaSuccess)
       return bad(e, "skut scratch");
+    if ((e = cudaMalloc(&d.pooled, (size_t)N * kDModel * 4)) != cudaSuccess) return bad(e, "pooled");
+    // every entry kPooledEmpty between runs (head_kernel restores it)
+    if ((e = cudaMemset(d.pooled, 0xff, (size_t)N * kDModel * 4)) != cudaSuccess) return bad(e, "pooled");
     if ((e = cudaStreamCreateWithFlags(&c->slot_stream[k], cudaStreamNonBlocking)) != cudaSuccess)
       return bad(e, "slot stream");
     if ((e = cudaEventCreateWithFlags(&c->ev_caller[k], cudaEventDisableTiming)) != cudaSuccess)
@@ -1070,10 +1075,15 @@ int run_score(tav2_ctx* c, int mode, const int32_t* idx, float* logits, float* p
   // fp16x3 parts with a true-max softmax in fp32 mode (logits within 1e-5)
   if (tc3_ok && skut_tc3_supported(c->nn, c->params)) {
     const bool f16 = mode == TAV2_MODE_FP32;
+    // the CTR head runs as its own kernel over the pooled vectors (head_kernel);
+    // into the workspace (kPooledEmpty between runs) it starts per candidate as
+    // soon as the candidate's pooled vector has landed
+    float* pw = pooled ? pooled : c->cur_dv().pooled;
     CU(timed(c, f16 ? "skut_tc3_f16" : "skut_tc3", s, [&] {
-      return launch_skut_tc3(c->params, f16 ? c->images3h : c->images3, c->nn, st, idx, st.n_items, logits, pooled,
+      return launch_skut_tc3(c->params, f16 ? c->images3h : c->images3, c->nn, st, idx, st.n_items, logits, pw,
                              sel, f16, s);
     }));
+    CU(timed(c, "head", s, [&] { return launch_head(c->params, st, pw, st.n_items, logits, pooled == nullptr, s); }));
     return TAV2_OK;
   }
   // 192 < S <= 384 (the k_ll = 128 / 256 sweep points): the same folded

@@ -292,6 +292,9 @@ cudaError_t launch_skut_tc(const Params& p, const SkutImages& img, const NNCfg& 
                            const uint8_t* fmask, int n, float* U, float* logits, float* pooled,
                            cudaStream_t s);
 cudaError_t launch_similarity(const Staged& st, int item, int source, int n, double* out, cudaStream_t s);
+cudaError_t launch_head(const Params& p, const Staged& st, float* pooled, int n, float* logits, bool spin,
+                        cudaStream_t s);
+constexpr uint32_t kPooledEmpty = 0xffffffffu;  // a NaN no arithmetic produces: "not written yet"
 cudaError_t launch_pool(const float* U, const uint8_t* mask, const float* out_linear, int n, int S, float* pooled,
                         cudaStream_t s);
 int skut_simt_grid(int n);
