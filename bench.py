@@ -463,7 +463,9 @@ def run_gpu(args, rank, world, local_rank):
     if dom:
         name, (ms, n) = dom
         per_launch_ms = ms / max(n, 1)
-        if name.startswith("skut"):
+        if name.startswith("skut_tc3"):  # the CTR head is its own kernel (head_kernel)
+            work = cand_step * (fl["transformer"] + fl["pool"])
+        elif name.startswith("skut"):
             work = cand_step * (fl["transformer"] + fl["pool"] + fl["head"])
         elif name.startswith("nn_"):
             work = cand_step * fl["nn"]
