@@ -12,7 +12,8 @@ import subprocess
 import sys
 
 NAMES = {"prep_kernel": "prep", "skut_tc3_f16_kernel": "skut_tc3_f16", "nn_bound_kernel": "nn_bound", "nn_select_kernel": "nn_select",
-         "skut_tc3_kernel": "skut_tc3", "skut_tc2_kernel": "skut_tc", "skut_simt_kernel": "skut_simt"}
+         "skut_tc3_kernel": "skut_tc3", "skut_tc2_kernel": "skut_tc", "skut_simt_kernel": "skut_simt",
+         "head_kernel": "head"}
 
 
 def main(rep, out="profiles/traffic.json"):
