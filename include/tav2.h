@@ -32,8 +32,10 @@ extern "C" {
 
 /* Precision modes of the scoring path (north_star: fp32 parity mode and the
  * bf16 headline mode). */
-#define TAV2_MODE_FP32 0  /* SIMT fp32 transformer, f64 NN scores (ref-faithful) */
-#define TAV2_MODE_BF16 1  /* tcgen05: fp16 NN scan + f64 re-scoring, bf16x3 SKUT */
+#define TAV2_MODE_FP32 0  /* logits within 1e-5: fp16x3 split GEMMs on tcgen05 (S <= 384) */
+#define TAV2_MODE_BF16 1  /* logits within 2e-3 (observed ~4e-5): bf16x3 split GEMMs  */
+/* Both modes select the NN index sets identically: fp16 tcgen05 threshold
+ * scan + exact f64 re-scoring of the survivors (the reference's formula). */
 
 /* ModelConfig (trainer.py:42-70) + NNConfig (nnsearch.py:25-46) as ints. */
 typedef struct {
