@@ -128,7 +128,7 @@ __device__ __forceinline__ void mma3_kmajor(uint32_t d, uint32_t a_col, uint32_t
 // AND causal (key <= r)
 static __device__ __forceinline__ uint32_t allowed16(uint32_t bits, int k0, int r) {
   const int n = r - k0 + 1;  // keys k0..r are causal-visible
-  const uint32_t causal = n >= 16 ? 0xffffu : (n <= 0 ? 0u : ((1u << n) - 1u));
+  const uint32_t causal = 0xffffu >> min(max(16 - n, 0), 16);  // branch-free (skut_tc3)
   return bits & causal;
 }
 

@@ -122,7 +122,7 @@ __shared__ T4Bars t4;
 
 static __device__ __forceinline__ uint32_t allowed16_4(uint32_t bits, int k0, int r) {
   const int n = r - k0 + 1;
-  const uint32_t causal = n >= 16 ? 0xffffu : (n <= 0 ? 0u : ((1u << n) - 1u));
+  const uint32_t causal = 0xffffu >> min(max(16 - n, 0), 16);  // branch-free (skut_tc3)
   return bits & causal;
 }
 
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
               if (jj + 1 <= jlast) tmem_ld16(cs + 16 * (jj + 1), nxt);  // warp-uniform
               const int g = (k0 >> 4) + jj;  // global 16-key sub-chunk
               const uint32_t vw = valid_w[par][g >> 1] >> ((g & 1) * 16);
-              const uint32_t vm = ok ? allowed16_4(vw, 16 * g, r) : 0u;
+              const uint32_t vm = allowed16_4(vw, 16 * g, r) & (ok ? 0xffffffffu : 0u);
               chunk16(cur, vm, cs + 16 * jj);
             }
           }
