@@ -80,6 +80,11 @@ static __device__ __forceinline__ uint32_t allowed16(uint32_t bits, int k0, int 
   return bits & causal;
 }
 
+// v if m = ~0, +0 if m = 0: branch-free row masking (an `if (!ok)` block
+// around a register array is a divergent branch in every warp: its lanes
+// >= rows-per-warp are never ok)
+__device__ __forceinline__ float t3_keep(float v, uint32_t m) { return __uint_as_float(__float_as_uint(v) & m); }
+
 __device__ __forceinline__ void t3_ld64(uint32_t ta, float* v) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
   tmem_ld32(ta, r);
@@ -363,10 +368,9 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         for (int e = 0; e < 16; ++e) x[16 * c16 + e] = (tfv[16 * c16 + e] + cc[e]) + pp[e];
       }
     }
-    if (!ok) {
+    const uint32_t okm = ok ? 0xffffffffu : 0u;  // this row's mask for the item
 #pragma unroll
-      for (int j = 0; j < kDModel; ++j) x[j] = 0.0f;
-    }
+    for (int j = 0; j < kDModel; ++j) x[j] = t3_keep(x[j], okm);
     {
       const unsigned b = __ballot_sync(0xffffffffu, ok);  // lanes >= rpw are never ok
       if (lane == 0 && b) {
@@ -407,10 +411,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         float a[kDModel];
         t3_layer_norm(x, lnp_s[L][0], lnp_s[L][1], a);
         float an2 = 0.0f;
-        if (!ok) {
 #pragma unroll
-          for (int j = 0; j < kDModel; ++j) a[j] = 0.0f;
-        }
+        for (int j = 0; j < kDModel; ++j) a[j] = t3_keep(a[j], okm);
 #pragma unroll
         for (int j = 0; j < kDModel; ++j) an2 = fmaf(a[j], a[j], an2);  // the shift's max ||a_j||
         // one bf16 hi/lo split of a, stored twice: the M1 A operand (TMEM,
@@ -463,10 +465,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         for (int h = 0; h < 2; ++h) {
           tmem_ld32(lanebase + kCD + 32 * h, reinterpret_cast<uint32_t*>(v));
           tmem_ld_wait();
-          if (!ok) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.0f;
-          }
+          // (rows that are not ok have a = 0 in A, so Q' and V' are exactly 0)
 #pragma unroll
           for (int i = 0; i < 32; ++i) qn2 = fmaf(v[i], v[i], qn2);
           if (F16 && mapped) {  // s_rr = q'_r . a_r from this row's K (fp16 hi + lo parts)
@@ -499,10 +498,6 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
           tmem_ld32(lanebase + kCD + 64 + 32 * h, reinterpret_cast<uint32_t*>(v));
           tmem_ld_wait();
           if (mapped) {
-            if (!ok) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = 0.0f;
-            }
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               const int off = (r >> 3) * 1024 + (4 * h + c) * 128 + (r & 7) * 16;
@@ -579,7 +574,6 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         };
         // the causal chunks, one at a time with the next chunk's TMEM load in
         // flight while this one is exponentiated (2-deep software pipeline)
-        const uint32_t okm = ok ? 0xffffffffu : 0u;
         auto exp_pass = [&]() {
           uint32_t sa[16], sb[16];
           tmem_ld16(cs, sa);
@@ -648,19 +642,16 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       {
         float d[kDModel];
         t3_ld64(cA, d);
-        if (ok) {
+        // (a row that is not ok has P = 0: O' = 0 and inv_l = 0, x stays 0)
 #pragma unroll
-          for (int j = 0; j < kDModel; j += 2) {
-            const float2 o = __ffma2_rn(make_float2(d[j], d[j + 1]), make_float2(inv_l, inv_l), make_float2(x[j], x[j + 1]));
-            x[j] = o.x;
-            x[j + 1] = o.y;
-          }
+        for (int j = 0; j < kDModel; j += 2) {
+          const float2 o = __ffma2_rn(make_float2(d[j], d[j + 1]), make_float2(inv_l, inv_l), make_float2(x[j], x[j + 1]));
+          x[j] = o.x;
+          x[j + 1] = o.y;
         }
         t3_layer_norm(x, lnp_s[L][2], lnp_s[L][3], d);
-        if (!ok) {
 #pragma unroll
-          for (int j = 0; j < kDModel; ++j) d[j] = 0.0f;
-        }
+        for (int j = 0; j < kDModel; ++j) d[j] = t3_keep(d[j], okm);
         t3_st_split<64, F16>(cA, d);
         tmem_st_wait();
         done();
@@ -681,7 +672,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         tmem_ld32(lanebase + kCD, reinterpret_cast<uint32_t*>(h));
         tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < kFfn; ++j) h[j] = ok ? fmaxf(h[j], 0.0f) : 0.0f;
+        for (int j = 0; j < kFfn; ++j) h[j] = t3_keep(fmaxf(h[j], 0.0f), okm);
         t3_st_split<32, F16>(lanebase + kCA2, h);
         tmem_st_wait();
         done();
@@ -699,13 +690,12 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       {
         float d[kDModel];
         t3_ld64(lanebase + kCW2, d);
-        if (ok) {
+        // (a row that is not ok has ReLU(H) = 0: D2 = 0, x stays 0)
 #pragma unroll
-          for (int j = 0; j < kDModel; j += 2) {
-            const float2 o = __fadd2_rn(make_float2(d[j], d[j + 1]), make_float2(x[j], x[j + 1]));
-            x[j] = o.x;
-            x[j + 1] = o.y;
-          }
+        for (int j = 0; j < kDModel; j += 2) {
+          const float2 o = __fadd2_rn(make_float2(d[j], d[j + 1]), make_float2(x[j], x[j + 1]));
+          x[j] = o.x;
+          x[j + 1] = o.y;
         }
       }
       stamp(18);
