@@ -534,7 +534,11 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         float mb;
         mbar_wait_sleep(&t3.kvready, n_kv & 1);  // kmax_s[L] complete (already passed)
         stamp(24);
-        mb = sqrtf(qn2 * __uint_as_float(kmax_s[L]));  // Cauchy-Schwarz: >= every score of the row
+        {  // Cauchy-Schwarz: >= every score of the row (up to the MUFU rsqrt's
+           // ~2 ulp: any shift works, this one keeps exp2 in range)
+          const float m2 = qn2 * __uint_as_float(kmax_s[L]);
+          mb = m2 > 0.0f ? m2 * rsqrtf(m2) : 0.0f;
+        }
         if constexpr (F16) {
           // fp32 mode (fp16 P parts): shift by the row's own diagonal score
           // where the bound allows, m' = max(s_rr, m_cs - 15): then P_rr = 1
@@ -609,7 +613,9 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         }
         const float l = l2.x + l2.y;
         stamp(26);
-        inv_l = l > 0.0f ? 1.0f / l : 0.0f;  // a valid row always sees itself
+        // a valid row always sees itself (l >= P_rr > 0); the approximate
+        // reciprocal (2 ulp) keeps the IEEE division's slow-path branch out
+        inv_l = l > 0.0f ? __fdividef(1.0f, l) : 0.0f;
         tmem_st_wait();
         done();
       }
