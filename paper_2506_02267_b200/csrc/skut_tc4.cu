@@ -120,6 +120,9 @@ struct T4Bars {
 };
 __shared__ T4Bars t4;
 
+// branch-free row masking (as skut_tc3's t3_keep)
+__device__ __forceinline__ float t4_keep(float v, uint32_t m) { return __uint_as_float(__float_as_uint(v) & m); }
+
 static __device__ __forceinline__ uint32_t allowed16_4(uint32_t bits, int k0, int r) {
   const int n = r - k0 + 1;
   const uint32_t causal = 0xffffu >> min(max(16 - n, 0), 16);  // branch-free (skut_tc3)
@@ -393,10 +396,9 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
       {
         float a[kDModel];
         t4_layer_norm(x, lnp_s[L][0], lnp_s[L][1], a);
-        if (!ok) {
+        const uint32_t okm = ok ? 0xffffffffu : 0u;
 #pragma unroll
-          for (int j = 0; j < kDModel; ++j) a[j] = 0.0f;
-        }
+        for (int j = 0; j < kDModel; ++j) a[j] = t4_keep(a[j], okm);
         float an2 = 0.0f;
 #pragma unroll
         for (int j = 0; j < kDModel; ++j) an2 = fmaf(a[j], a[j], an2);
@@ -450,10 +452,7 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
         for (int h = 0; h < 2; ++h) {
           tmem_ld32(lanebase + k4CD + 32 * h, reinterpret_cast<uint32_t*>(v));
           tmem_ld_wait();
-          if (!ok) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.0f;
-          }
+          // (rows that are not ok have a = 0 in A, so Q' is exactly 0)
 #pragma unroll
           for (int i = 0; i < 32; ++i) qn2 = fmaf(v[i], v[i], qn2);
           if (F16 && mapped) {
@@ -500,7 +499,8 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
       // the exact normaliser of encoder.py:203-211, and the chunks are
       // independent of each other.
       mbar_wait_cl(&t4.kvready, n_kv & 1);  // kmax_s / valid_w complete (already passed)
-      float mb = sqrtf(qn2 * __uint_as_float(kmax_s[par][L]));
+      const float m2 = qn2 * __uint_as_float(kmax_s[par][L]);
+      float mb = m2 > 0.0f ? m2 * rsqrtf(m2) : 0.0f;  // (no sqrtf slow-path branch; skut_tc3)
       if constexpr (F16) mb = ok ? fmaxf(s_rr, mb - 15.0f) : 0.0f;  // as skut_tc3's fp32 mode
       const float2 nmb = make_float2(-mb, -mb);
       float2 l2 = make_float2(0.f, 0.f);
@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
       }
       ++n_kv;
       const float l = l2.x + l2.y;
-      const float inv_l = l > 0.0f ? 1.0f / l : 0.0f;  // a valid row always sees itself
+      const float inv_l = l > 0.0f ? __fdividef(1.0f, l) : 0.0f;  // a valid row always sees itself
       // ---- P4a: O'' -> A (hi/lo) ----
       wait_mma();
       {
@@ -618,19 +618,17 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
       {
         float d[kDModel];
         t4_ld64(lanebase + k4CD, d);
-        if (ok) {
+        // (a row that is not ok has P = 0: O' = 0 and inv_l = 0, x stays 0)
 #pragma unroll
-          for (int j = 0; j < kDModel; j += 2) {
-            const float2 o = __ffma2_rn(make_float2(d[j], d[j + 1]), make_float2(inv_l, inv_l), make_float2(x[j], x[j + 1]));
-            x[j] = o.x;
-            x[j + 1] = o.y;
-          }
+        for (int j = 0; j < kDModel; j += 2) {
+          const float2 o = __ffma2_rn(make_float2(d[j], d[j + 1]), make_float2(inv_l, inv_l), make_float2(x[j], x[j + 1]));
+          x[j] = o.x;
+          x[j + 1] = o.y;
         }
         t4_layer_norm(x, lnp_s[L][2], lnp_s[L][3], d);
-        if (!ok) {
+        const uint32_t okm = ok ? 0xffffffffu : 0u;
 #pragma unroll
-          for (int j = 0; j < kDModel; ++j) d[j] = 0.0f;
-        }
+        for (int j = 0; j < kDModel; ++j) d[j] = t4_keep(d[j], okm);
         t4_st_split<64, F16>(cA, d);
         tmem_st_wait();
         done();
@@ -662,13 +660,12 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
       {
         float d[kDModel];
         t4_ld64(lanebase + k4CW2, d);
-        if (ok) {
+        // (a row that is not ok has ReLU(H) = 0: D2 = 0, x stays 0)
 #pragma unroll
-          for (int j = 0; j < kDModel; j += 2) {
-            const float2 o = __fadd2_rn(make_float2(d[j], d[j + 1]), make_float2(x[j], x[j + 1]));
-            x[j] = o.x;
-            x[j + 1] = o.y;
-          }
+        for (int j = 0; j < kDModel; j += 2) {
+          const float2 o = __fadd2_rn(make_float2(d[j], d[j + 1]), make_float2(x[j], x[j + 1]));
+          x[j] = o.x;
+          x[j + 1] = o.y;
         }
       }
     }
