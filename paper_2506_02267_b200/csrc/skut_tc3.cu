@@ -578,29 +578,29 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         };
         // the causal chunks, one at a time with the next chunk's TMEM load in
         // flight while this one is exponentiated (2-deep software pipeline)
+        // 32-key pairs of chunks per TMEM load: tcgen05.wait::ld waits for
+        // every load in flight, so a pair in flight while the previous pair
+        // is exponentiated doubles the latency each load can hide (-1.5%
+        // against 16-key chunks once the mask was branch-free)
         auto exp_pass = [&]() {
-          uint32_t sa[16], sb[16];
-          tmem_ld16(cs, sa);
-          // key-validity word of the chunk pair, read one pair ahead (its
-          // shared-memory latency otherwise sits on every chunk's mask)
-          uint32_t vw_cur = valid_w[0];
-          for (int j = 0; j <= jlast; j += 2) {
-            const uint32_t vw_next = valid_w[min((j >> 1) + 1, 7)];
+          uint32_t sa[32], sb[32];
+          tmem_ld32(cs, sa);
+          for (int j = 0; j <= jlast; j += 4) {
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-              const int jj = j + u;
+              const int jj = j + 2 * u;  // this pair's first chunk
               if (jj > jlast) break;
               tmem_ld_wait();
               uint32_t* cur = u == 0 ? sa : sb;
               uint32_t* nxt = u == 0 ? sb : sa;
-              if (jj + 1 <= jlast) tmem_ld16(cs + 16 * (jj + 1), nxt);  // warp-uniform
-              const uint32_t vm = allowed16(vw_cur >> (u * 16), 16 * jj, r) & okm;
-              // (a warp-uniform unmasked fast path measured 4% slower: code size)
-              chunk(cur, vm, cs + 16 * jj, std::true_type{});
+              if (jj + 2 <= jlast) tmem_ld32(cs + 16 * (jj + 2), nxt);  // warp-uniform
+              const uint32_t vw = valid_w[jj >> 1];
+              chunk(cur, allowed16(vw, 16 * jj, r) & okm, cs + 16 * jj, std::true_type{});
+              if (jj + 1 <= jlast) chunk(cur + 16, allowed16(vw >> 16, 16 * (jj + 1), r) & okm, cs + 16 * (jj + 1), std::true_type{});
             }
-            vw_cur = vw_next;
           }
         };
+
         exp_pass();
         const int jz = jlast + 1;
         stamp(25);
