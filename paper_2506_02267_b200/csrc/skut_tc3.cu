@@ -157,14 +157,19 @@ __device__ __forceinline__ void t3_layer_norm(const float* x, const float* g, co
 }
 
 // D += A(TMEM hi/lo) x B(smem hi/lo, K-major slabs), 3 terms per k-step;
-// warp-collective (one elected lane issues), fully unrolled
+// warp-collective (one elected lane issues), fully unrolled.  bh0 / bl0 are
+// the k-step-0 B descriptors (precomputed per CTA in desc_s); k-step j adds
+// j * step16 to the 14-bit start-address field (step16 = 2 lbo / 16; smem
+// addresses < 256 KB never carry out of the field).  (Building each
+// descriptor from the shared-window address instead cost an S2R + LDC +
+// address chain per k-step: the register-starved kernel rematerialises it.)
 template <int KSTEPS>
-__device__ __forceinline__ void t3_mma3(uint32_t d, uint32_t a_col, uint32_t a_lo_off, uint32_t b_hi,
-                                        uint32_t b_lo, uint32_t lbo, uint32_t idesc) {
+__device__ __forceinline__ void t3_mma3(uint32_t d, uint32_t a_col, uint32_t a_lo_off, uint64_t bh0,
+                                        uint64_t bl0, uint32_t step16, uint32_t idesc) {
 #pragma unroll
   for (int j = 0; j < KSTEPS; ++j) {
-    const uint64_t bh = sdesc(b_hi + 2 * j * lbo, lbo, 128);
-    const uint64_t bl = sdesc(b_lo + 2 * j * lbo, lbo, 128);
+    const uint64_t bh = bh0 + (uint64_t)(j * step16);
+    const uint64_t bl = bl0 + (uint64_t)(j * step16);
     mma_bf16_ts_w(d, a_col + 8 * j, bh, idesc, j > 0);
     mma_bf16_ts_w(d, a_col + 8 * j, bl, idesc, 1);
     mma_bf16_ts_w(d, a_col + a_lo_off + 8 * j, bh, idesc, 1);
@@ -178,6 +183,10 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   extern __shared__ __align__(1024) uint8_t sm[];
   cta_stamp(kDbgSkut, 0);
   __shared__ uint32_t taddr_s;
+  // B-operand descriptors of every GEMM at k-step 0: [2L, 2L+1] M1 (layer L
+  // hi / lo), [4, 5] M2 keys, [6, 7] M3 V', [8 + 2L ..] M4, [12 + 2L ..] M5,
+  // [16, 17] pool
+  __shared__ uint64_t desc_s[18];
   __shared__ uint32_t valid_w[8];  // key-validity bitmask, bit r of word r/32
   __shared__ __align__(16) float lnp_s[2][4][kDModel];
   __shared__ float red_s[kT3Warps][kDModel];
@@ -219,6 +228,23 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   if (warp == 0) tmem_alloc<512>(&taddr_s);
   if (tid < 8) valid_w[tid] = 0u;
   if (tid < 2) kmax_s[tid] = 0u;
+  if (tid == 0) {
+    for (int L = 0; L < NL; ++L) {
+      const uint32_t a = wsm + L * kW3Layer, b = a + kImg3WA;
+      desc_s[2 * L] = sdesc(a, 128 * 16, 128);
+      desc_s[2 * L + 1] = sdesc(a + kImg3WA / 2, 128 * 16, 128);
+      desc_s[8 + 2 * L] = sdesc(b, 32 * 16, 128);
+      desc_s[9 + 2 * L] = sdesc(b + 4096, 32 * 16, 128);
+      desc_s[12 + 2 * L] = sdesc(b + 8192, 64 * 16, 128);
+      desc_s[13 + 2 * L] = sdesc(b + 8192 + 4096, 64 * 16, 128);
+    }
+    desc_s[4] = sdesc(khi, S_pad * 16, 128);
+    desc_s[5] = sdesc(klo, S_pad * 16, 128);
+    desc_s[6] = sdesc(vhi, 1024, 128);
+    desc_s[7] = sdesc(vlo, 1024, 128);
+    desc_s[16] = sdesc(wsm + NL * kW3Layer, 64 * 16, 128);
+    desc_s[17] = sdesc(wsm + NL * kW3Layer + 8192, 64 * 16, 128);
+  }
   for (int i = tid; i < NL * 4 * kDModel; i += kT3Threads) {
     const int L = i / (4 * kDModel), w = (i / kDModel) % 4, j = i % kDModel;
     const float* src = w == 0 ? p.ln1_scale[L] : w == 1 ? p.ln1_shift[L] : w == 2 ? p.ln2_scale[L] : p.ln2_shift[L];
@@ -281,8 +307,6 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     ph_simt ^= 1u;
     fence_after();
   };
-  auto wa = [&](int L) { return wsm + L * kW3Layer; };
-  auto wb = [&](int L) { return wsm + L * kW3Layer + kImg3WA; };
 
   griddep_launch();
   // NN selection (idx) and prep (tok_feat, cand_unit) complete: the whole
@@ -447,7 +471,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         issuer_wait_simt();
         stamp(28);
         if (t == 0) order_after_tile1();
-        t3_mma3<4>(R + kCD, R + kCA, 32, wa(L), wa(L) + kImg3WA / 2, 128 * 16, t3_idesc<F16>(128, 128));
+        t3_mma3<4>(R + kCD, R + kCA, 32, desc_s[2 * L], desc_s[2 * L + 1], (2 * 128 * 16) >> 4, t3_idesc<F16>(128, 128));
         commit_w(&t3.mma[t]);
         if (t == 1) order_after_tile1();
       }
@@ -515,7 +539,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         mbar_wait(&t3.kvready, n_kv & 1);
         fence_after();
         if (t == 0) order_after_tile1();
-        t3_mma3<4>(R + kCD, R + kCA, 32, khi, klo, S_pad * 16, t3_idesc<F16>(128, NK));
+        t3_mma3<4>(R + kCD, R + kCA, 32, desc_s[4], desc_s[5], 2 * S_pad, t3_idesc<F16>(128, NK));
         commit_w(&t3.mma[t]);
         if (t == 1) order_after_tile1();
       }
@@ -625,12 +649,13 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         stamp(29);
         const uint32_t id = t3_idesc<F16>(128, 64, 0, 1);
         const int nk16 = NK / 16;  // <= 12 (S_pad <= 192); unrolled, warp-uniform bound
+        const uint64_t bv_hi = desc_s[6], bv_lo = desc_s[7];
         const long long t_iss = kDebug ? clock64() : 0;
 #pragma unroll
         for (int j = 0; j < 12; ++j) {
           if (j < nk16) {
-            const uint64_t bh = sdesc(vhi + 2 * j * 1024, 1024, 128);
-            const uint64_t bl = sdesc(vlo + 2 * j * 1024, 1024, 128);
+            const uint64_t bh = bv_hi + (uint64_t)(j * ((2 * 1024) >> 4));
+            const uint64_t bl = bv_lo + (uint64_t)(j * ((2 * 1024) >> 4));
             mma_bf16_ts_w(R + kCA, R + kCD + 16 * j, bh, id, j > 0);
             mma_bf16_ts_w(R + kCA, R + kCD + 16 * j, bl, id, 1);
             mma_bf16_ts_w(R + kCA, R + kCD + 16 * j + 8, bh, id, 1);
@@ -666,7 +691,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       if (issue_warp) {  // M4: H = A W1   (N = 32, K = 64)
         issuer_wait_simt();
         stamp(30);
-        t3_mma3<4>(R + kCD, R + kCA, 32, wb(L), wb(L) + 4096, 32 * 16, t3_idesc<F16>(128, 32));
+        t3_mma3<4>(R + kCD, R + kCA, 32, desc_s[8 + 2 * L], desc_s[9 + 2 * L], (2 * 32 * 16) >> 4, t3_idesc<F16>(128, 32));
         commit_w(&t3.mma[t]);
       }
       stamp(13);
@@ -686,7 +711,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       stamp(15);
       if (issue_warp) {  // M5: D2 = ReLU(H) W2   (N = 64, K = 32)
         issuer_wait_simt();
-        t3_mma3<2>(R + kCW2, R + kCA2, 16, wb(L) + 8192, wb(L) + 8192 + 4096, 64 * 16, t3_idesc<F16>(128, 64));
+        t3_mma3<2>(R + kCW2, R + kCA2, 16, desc_s[12 + 2 * L], desc_s[13 + 2 * L], (2 * 64 * 16) >> 4, t3_idesc<F16>(128, 64));
         commit_w(&t3.mma[t]);
       }
       stamp(16);
@@ -714,7 +739,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     stamp(19);
     if (issue_warp) {
       issuer_wait_simt();
-      t3_mma3<4>(R + kCD, R + kCA, 32, wsm + NL * kW3Layer, wsm + NL * kW3Layer + 8192, 64 * 16,
+      t3_mma3<4>(R + kCD, R + kCA, 32, desc_s[16], desc_s[17], (2 * 64 * 16) >> 4,
                  t3_idesc<F16>(128, 64));
       commit_w(&t3.mma[t]);
     }
