@@ -75,6 +75,9 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(smem)), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // Keys of n <= kSelCache survivors into a[]: the warp stages kRowBatch token
 // rows at a time in shared memory with cp.async (8 lanes x 16 B per row, all
@@ -93,22 +96,39 @@ __device__ __forceinline__ void keys_staged(const KeySrc& ks, int n, int lane, f
     if (i < n) sidx[i] = (uint16_t)ks.token(i);
   }
   __syncwarp();
-  for (int b0 = 0; b0 < n; b0 += kRowBatch) {
-    const int nb = min(kRowBatch, n - b0);
+  // 32-row batches double-buffered in the two halves of `rows`: batch b + 1
+  // is in flight (cp.async group) while batch b is scored, so the L2 round
+  // trips overlap instead of one per 64-row batch
+  constexpr int kHalf = kRowBatch / 2;
+  auto issue = [&](int b) {
+    const int b0 = b * kHalf, nb = min(kHalf, n - b0);
+    float4* dst = rows + (b & 1) * kHalf * 8;
     for (int rr = lane >> 3; rr < nb; rr += 4) {
       const int t = sidx[b0 + rr];
       const int c = lane & 7;
-      cp_async16(rows + rr * 8 + (c ^ (rr & 7)), ks.tok + (size_t)t * kEmbed + 4 * c);
+      cp_async16(dst + rr * 8 + (c ^ (rr & 7)), ks.tok + (size_t)t * kEmbed + 4 * c);
     }
-    cp_async_wait_all();
+    cp_async_commit();
+  };
+  const int nbat = (n + kHalf - 1) / kHalf;
+  if (nbat > 0) issue(0);
+  for (int b = 0; b < nbat; ++b) {
+    if (b + 1 < nbat) {
+      issue(b + 1);
+      cp_async_wait_group<1>();
+    } else {
+      cp_async_wait_group<0>();
+    }
     __syncwarp();
-    for (int rr = lane; rr < nb; rr += 32) {
+    const int rr = lane, b0 = b * kHalf;
+    if (b0 + rr < n) {
+      const float4* src = rows + (b & 1) * kHalf * 8;
       float4 r[8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) r[c] = rows[rr * 8 + (c ^ (rr & 7))];
+      for (int c = 0; c < 8; ++c) r[c] = src[rr * 8 + (c ^ (rr & 7))];
       a[b0 + rr] = score_key(dot_exact(r, ks.uc), sidx[b0 + rr]);
     }
-    __syncwarp();
+    __syncwarp();  // this half is refilled by issue(b + 2)
   }
 }
 
@@ -482,42 +502,50 @@ __device__ __forceinline__ void select_direct(const KeySrc& ks, const float* ucf
 #pragma unroll
   for (int b = 0; b < kDirBins / 32; ++b) hist[b * 32 + lane] = 0u;
   float ap[kDirectMax / 32];
-#pragma unroll
-  for (int bb = 0; bb < kDirectMax / kRowBatch; ++bb) {
-    const int b0 = bb * kRowBatch;
-    if (b0 < n) {  // (warp-uniform)
-      const int nb = min(kRowBatch, n - b0);
-      for (int i = lane; i < nb * 8; i += 32) {
-        const int rr = i >> 3, c = i & 7;
-        cp_async16(rows + rr * 8 + (c ^ (rr & 7)), ks.tok + (size_t)(lo + b0 + rr) * kEmbed + 4 * c);
-      }
-      cp_async_wait_all();
-      __syncwarp();
-#pragma unroll
-      for (int h = 0; h < kRowBatch / 32; ++h) {
-        const int rr = 32 * h + lane;
-        float v = -INFINITY;
-        if (rr < nb) {
-          float e0 = 0.f, e1 = 0.f;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 x = rows[rr * 8 + (q ^ (rr & 7))];
-            float& e = (q & 1) ? e1 : e0;
-            e = fmaf(x.x, ucf[4 * q], e);
-            e = fmaf(x.y, ucf[4 * q + 1], e);
-            e = fmaf(x.z, ucf[4 * q + 2], e);
-            e = fmaf(x.w, ucf[4 * q + 3], e);
-          }
-          v = e0 + e1;
-          atomicAdd(hist + min(max((int)((v + 1.0f) * (kDirBins / 2)), 0), kDirBins - 1), 1u);
-        }
-        ap[bb * (kRowBatch / 32) + h] = v;
-      }
-      __syncwarp();
-    } else {
-#pragma unroll
-      for (int h = 0; h < kRowBatch / 32; ++h) ap[bb * (kRowBatch / 32) + h] = -INFINITY;
+  // 32-row batches double-buffered (as keys_staged): batch b + 1 in flight
+  // while batch b is scored; fully unrolled so ap[] stays in registers
+  constexpr int kHalf = kRowBatch / 2;
+  auto issue = [&](int b) {
+    const int b0 = b * kHalf, nb = min(kHalf, n - b0);
+    float4* dst = rows + (b & 1) * kHalf * 8;
+    for (int i = lane; i < nb * 8; i += 32) {
+      const int rr = i >> 3, c = i & 7;
+      cp_async16(dst + rr * 8 + (c ^ (rr & 7)), ks.tok + (size_t)(lo + b0 + rr) * kEmbed + 4 * c);
     }
+    cp_async_commit();
+  };
+  const int nbat = (n + kHalf - 1) / kHalf;
+  if (nbat > 0) issue(0);
+#pragma unroll
+  for (int b = 0; b < kDirectMax / 32; ++b) {
+    float v = -INFINITY;
+    if (b < nbat) {  // (warp-uniform)
+      if (b + 1 < nbat) {
+        issue(b + 1);
+        cp_async_wait_group<1>();
+      } else {
+        cp_async_wait_group<0>();
+      }
+      __syncwarp();
+      const int rr = lane;
+      if (b * kHalf + rr < n) {
+        const float4* src = rows + (b & 1) * kHalf * 8;
+        float e0 = 0.f, e1 = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 x = src[rr * 8 + (q ^ (rr & 7))];
+          float& e = (q & 1) ? e1 : e0;
+          e = fmaf(x.x, ucf[4 * q], e);
+          e = fmaf(x.y, ucf[4 * q + 1], e);
+          e = fmaf(x.z, ucf[4 * q + 2], e);
+          e = fmaf(x.w, ucf[4 * q + 3], e);
+        }
+        v = e0 + e1;
+        atomicAdd(hist + min(max((int)((v + 1.0f) * (kDirBins / 2)), 0), kDirBins - 1), 1u);
+      }
+      __syncwarp();  // this half is refilled by issue(b + 2)
+    }
+    ap[b] = v;
   }
   __syncwarp();
   // bin of the k-th largest approximation: lane l owns bins 255 - 8l .. 248 - 8l
