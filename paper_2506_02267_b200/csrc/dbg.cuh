@@ -47,7 +47,7 @@ __device__ __forceinline__ void sel_record(int slot, long long dur, long long n)
 __device__ __forceinline__ void sel_record_phase(int slot, int phase, long long dur) {
   if constexpr (!kDebug) return;
   long long* d = g_dbg_cta;
-  if (d != nullptr && slot < kDbgCtas) d[(phase == 0 ? 6 * 3 + 2 : 7 * 3 + 0) * kDbgCtas + slot] = dur;
+  if (d != nullptr && slot < kDbgCtas) d[(phase == 0 ? 6 * 3 + 2 : 7 * 3 + phase - 1) * kDbgCtas + slot] = dur;
 }
 __device__ __forceinline__ long long gtimer() {
   long long t;

@@ -152,7 +152,7 @@ __device__ __forceinline__ void bm_clear(uint32_t* bm, int words, int lane) {
 // segment order, nnsearch.py:364): lane l scans its words high first; a warp
 // prefix sum of the per-lane counts places its bits.
 __device__ __forceinline__ void emit_bitmap(const uint32_t* bm, int words, int k, int lane, int32_t* orow,
-                                            double* srow, const KeySrc& ks) {
+                                            double* srow, const KeySrc& ks, int dbg_slot = -1, long long t0 = 0) {
   const int per = (words + 31) / 32;
   const int w_hi = words - per * lane;  // this lane's logical words: [w_hi - per, w_hi)
   int cnt = 0;
@@ -164,6 +164,7 @@ __device__ __forceinline__ void emit_bitmap(const uint32_t* bm, int words, int k
     if (lane >= o) incl += y;
   }
   int pos = incl - cnt;
+  if (kDebug && dbg_slot >= 0 && lane == 0) sel_record_phase(dbg_slot, 2, gtimer() - t0);
   for (int j = 0; j < per && w_hi - 1 - j >= 0; ++j) {
     const int w = w_hi - 1 - j;
     uint32_t m = bm[j * 32 + lane];
@@ -717,7 +718,7 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
     else if (np <= 256) select_bisect<8>(a, n, k, lane, bm, words);
     else select_radix_cached(a, n, k, lane, hist_s[warp], bm, words);
     if (kDebug && lane == 0) sel_record_phase(item * 3 + s, 1, gtimer() - t_start);
-    emit_bitmap(bm, words, k, lane, orow, srow, ks);
+    emit_bitmap(bm, words, k, lane, orow, srow, ks, kDebug ? item * 3 + s : -1, t_start);
   } else {
     select_radix(ks, n, k, lane, buf[warp], hist_s[warp], orow, srow);
   }

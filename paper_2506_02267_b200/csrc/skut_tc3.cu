@@ -438,7 +438,15 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
 #pragma unroll
         for (int j = 0; j < kDModel; ++j) a[j] = t3_keep(a[j], okm);
 #pragma unroll
-        for (int j = 0; j < kDModel; ++j) an2 = fmaf(a[j], a[j], an2);  // the shift's max ||a_j||
+        {  // the shift's max ||a_j||: paired FFMA2 chains (a 64-deep FMA chain was ~260 cycles)
+          float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int j = 0; j < kDModel; j += 4) {
+            s0 = __ffma2_rn(make_float2(a[j], a[j + 1]), make_float2(a[j], a[j + 1]), s0);
+            s1 = __ffma2_rn(make_float2(a[j + 2], a[j + 3]), make_float2(a[j + 2], a[j + 3]), s1);
+          }
+          an2 = (s0.x + s0.y) + (s1.x + s1.y);
+        }
         // one bf16 hi/lo split of a, stored twice: the M1 A operand (TMEM,
         // warp-collective: never under a divergent branch) and this row's K
         // (K-major smem slabs: chunk c of row r at c*(S_pad*16) + r*16)
@@ -482,7 +490,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
 #endif
       wait_mma();
       stamp(5);
-      float qn2 = 0.0f, s_rr = 0.0f;
+      float s_rr = 0.0f, qn2;
+      float2 qa = make_float2(0.f, 0.f), qb = make_float2(0.f, 0.f);  // ||q'||^2 in paired chains
       {
         float v[32];
 #pragma unroll
@@ -491,7 +500,10 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
           tmem_ld_wait();
           // (rows that are not ok have a = 0 in A, so Q' and V' are exactly 0)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) qn2 = fmaf(v[i], v[i], qn2);
+          for (int i = 0; i < 32; i += 4) {
+            qa = __ffma2_rn(make_float2(v[i], v[i + 1]), make_float2(v[i], v[i + 1]), qa);
+            qb = __ffma2_rn(make_float2(v[i + 2], v[i + 3]), make_float2(v[i + 2], v[i + 3]), qb);
+          }
           if (F16 && mapped) {  // s_rr = q'_r . a_r from this row's K (fp16 hi + lo parts)
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
@@ -517,6 +529,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
             tmem_st8(cA + 32 + 16 * h + 8 * c, lo);
           }
         }
+        qn2 = (qa.x + qa.y) + (qb.x + qb.y);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {  // V': (key r, d) at (r/8)*1024 + (d/8)*128 + (r%8)*16 + (d%8)*2
           tmem_ld32(lanebase + kCD + 64 + 32 * h, reinterpret_cast<uint32_t*>(v));

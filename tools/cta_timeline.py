@@ -71,9 +71,10 @@ if sel.any():
     for src in range(3):
         m = sel & (np.arange(len(rec_t)) % 3 == src) & (st_t > 0)
         if m.any():
+            em_t = t[7, 1]
             print(f"  source {src}: warps {m.sum()} total med {np.median(rec_t[m]) / 1e3:.2f} us, keys staged+scored "
                   f"med {np.median(st_t[m]) / 1e3:.2f} us, threshold found med {np.median(bi_t[m]) / 1e3:.2f} us, "
-                  f"n med {np.median(rec_n[m]):.0f}")
+                  f"emit counted med {np.median(em_t[m]) / 1e3:.2f} us, n med {np.median(rec_n[m]):.0f}")
 
 
 if "--detail" in sys.argv:  # the slowest CTAs of every kernel
