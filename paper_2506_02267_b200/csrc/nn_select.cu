@@ -153,10 +153,15 @@ __device__ __forceinline__ void bm_clear(uint32_t* bm, int words, int lane) {
 // prefix sum of the per-lane counts places its bits.
 __device__ __forceinline__ void emit_bitmap(const uint32_t* bm, int words, int k, int lane, int32_t* orow,
                                             double* srow, const KeySrc& ks, int dbg_slot = -1, long long t0 = 0) {
-  const int per = (words + 31) / 32;
+  const int per = (words + 31) / 32;    // <= 16 (kCaps0 positions)
   const int w_hi = words - per * lane;  // this lane's logical words: [w_hi - per, w_hi)
   int cnt = 0;
-  for (int j = 0; j < per && w_hi - 1 - j >= 0; ++j) cnt += __popc(bm[j * 32 + lane]);
+  uint32_t nz = 0u;  // this lane's nonzero words (bit j: logical word w_hi - 1 - j)
+  for (int j = 0; j < per && w_hi - 1 - j >= 0; ++j) {
+    const int c = __popc(bm[j * 32 + lane]);
+    cnt += c;
+    nz |= (c != 0 ? 1u : 0u) << j;
+  }
   int incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -165,29 +170,35 @@ __device__ __forceinline__ void emit_bitmap(const uint32_t* bm, int words, int k
   }
   int pos = incl - cnt;
   if (kDebug && dbg_slot >= 0 && lane == 0) sel_record_phase(dbg_slot, 2, gtimer() - t0);
-  for (int j = 0; j < per && w_hi - 1 - j >= 0; ++j) {
+  // only the nonzero words, descending storage index (j ascending, bits high
+  // to low); the reference scores in a second, lane-parallel pass
+  while (nz) {
+    const int j = __ffs(nz) - 1;
+    nz &= nz - 1;
     const int w = w_hi - 1 - j;
     uint32_t m = bm[j * 32 + lane];
     while (m) {
       const int b = 31 - __clz(m);
       m &= ~(1u << b);
-      const int t = 32 * w + b;
-      if (pos < k) {
-        orow[pos] = t;
-        if (srow) {
-          float4 r[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) r[q] = __ldg(reinterpret_cast<const float4*>(ks.tok + (size_t)t * kEmbed) + q);
-          srow[pos] = dot_exact(r, ks.uc);
-        }
-      }
+      if (pos < k) orow[pos] = 32 * w + b;
       ++pos;
     }
   }
   const int total = __shfl_sync(0xffffffffu, incl, 31);
-  for (int j = total + lane; j < k; j += 32) {
-    orow[j] = -1;
-    if (srow) srow[j] = 0.0;
+  for (int j = total + lane; j < k; j += 32) orow[j] = -1;
+  if (srow) {  // the exact f64 key of every winner (nnsearch.py:362-363)
+    __syncwarp();
+    for (int j = lane; j < k; j += 32) {
+      const int t = j < total ? orow[j] : -1;
+      double v = 0.0;
+      if (t >= 0) {
+        float4 r[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) r[q] = __ldg(reinterpret_cast<const float4*>(ks.tok + (size_t)t * kEmbed) + q);
+        v = dot_exact(r, ks.uc);
+      }
+      srow[j] = v;
+    }
   }
 }
 
