@@ -163,14 +163,14 @@ __device__ __forceinline__ void t3_layer_norm(const float* x, const float* g, co
 // addresses < 256 KB never carry out of the field).  (Building each
 // descriptor from the shared-window address instead cost an S2R + LDC +
 // address chain per k-step: the register-starved kernel rematerialises it.)
-template <int KSTEPS>
+template <int KSTEPS, bool ACC = false>  // ACC: accumulate onto D from the first k-step
 __device__ __forceinline__ void t3_mma3(uint32_t d, uint32_t a_col, uint32_t a_lo_off, uint64_t bh0,
                                         uint64_t bl0, uint32_t step16, uint32_t idesc) {
 #pragma unroll
   for (int j = 0; j < KSTEPS; ++j) {
     const uint64_t bh = bh0 + (uint64_t)(j * step16);
     const uint64_t bl = bl0 + (uint64_t)(j * step16);
-    mma_bf16_ts_w(d, a_col + 8 * j, bh, idesc, j > 0);
+    mma_bf16_ts_w(d, a_col + 8 * j, bh, idesc, ACC || j > 0);
     mma_bf16_ts_w(d, a_col + 8 * j, bl, idesc, 1);
     mma_bf16_ts_w(d, a_col + a_lo_off + 8 * j, bh, idesc, 1);
   }
@@ -185,8 +185,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   __shared__ uint32_t taddr_s;
   // B-operand descriptors of every GEMM at k-step 0: [2L, 2L+1] M1 (layer L
   // hi / lo), [4, 5] M2 keys, [6, 7] M3 V', [8 + 2L ..] M4, [12 + 2L ..] M5,
-  // [16, 17] pool
-  __shared__ uint64_t desc_s[18];
+  // [16, 17] pool, [18, 19] W2 W_out (the fused last-layer pool GEMM)
+  __shared__ uint64_t desc_s[20];
   __shared__ uint32_t valid_w[8];  // key-validity bitmask, bit r of word r/32
   __shared__ __align__(16) float lnp_s[2][4][kDModel];
   __shared__ float red_s[kT3Warps][kDModel];
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   const int S = nn.seq_len;
   const int S_pad = (S + 15) & ~15;
   const int NL = p.num_layers;
-  const int wbytes = NL * kW3Layer + kImg3WO;
+  const int wbytes = NL * kW3Layer + kImg3WO + kImg3W2O;
   uint8_t* Wsm = sm;
   uint8_t* Khi = sm + wbytes;
   uint8_t* Klo = Khi + S_pad * 128;
@@ -244,6 +244,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     desc_s[7] = sdesc(vlo, 1024, 128);
     desc_s[16] = sdesc(wsm + NL * kW3Layer, 64 * 16, 128);
     desc_s[17] = sdesc(wsm + NL * kW3Layer + 8192, 64 * 16, 128);
+    desc_s[18] = sdesc(wsm + NL * kW3Layer + kImg3WO, 64 * 16, 128);
+    desc_s[19] = sdesc(wsm + NL * kW3Layer + kImg3WO + 4096, 64 * 16, 128);
   }
   for (int i = tid; i < NL * 4 * kDModel; i += kT3Threads) {
     const int L = i / (4 * kDModel), w = (i / kDModel) % 4, j = i % kDModel;
@@ -258,6 +260,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     mbar_expect_tx(&t3.wfull, (uint32_t)wbytes);
     for (int L = 0; L < NL; ++L) bulk_g2s(Wsm + L * kW3Layer, img.w[L], kW3Layer, &t3.wfull);
     bulk_g2s(Wsm + NL * kW3Layer, img.wout, kImg3WO, &t3.wfull);
+    bulk_g2s(Wsm + NL * kW3Layer + kImg3WO, img.w2out, kImg3W2O, &t3.wfull);
   }
 
   const bool issuer = (tid & 127) == 0;  // debug stamps only
@@ -718,10 +721,29 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
 #pragma unroll
         for (int j = 0; j < kFfn; ++j) h[j] = t3_keep(fmaxf(h[j], 0.0f), okm);
         t3_st_split<32, F16>(lanebase + kCA2, h);
+#ifndef TAV2_POOL_UNFUSED
+        // last layer: x_mid -> A as well (M4 has consumed LN2's output): the
+        // pooled projection of the layer output x_mid + ReLU(H) W2 is
+        // x_mid W_out + ReLU(H) (W2 W_out) -- one GEMM, no M5 / P6 / pool store
+        if (L == NL - 1) t3_st_split<64, F16>(cA, x);  // invalid rows carry x = 0
+#endif
         tmem_st_wait();
         done();
       }
       stamp(15);
+#ifndef TAV2_POOL_UNFUSED
+      if (L == NL - 1) {
+        if (issue_warp) {  // pool: Y = A x_mid W_out + A2 ReLU(H) W2'  (N = 64, K = 64 + 32) -> D [64, 128)
+          issuer_wait_simt();
+          t3_mma3<4>(R + kCW2, R + kCA, 32, desc_s[16], desc_s[17], (2 * 64 * 16) >> 4, t3_idesc<F16>(128, 64));
+          t3_mma3<2, true>(R + kCW2, R + kCA2, 16, desc_s[18], desc_s[19], (2 * 64 * 16) >> 4,
+                           t3_idesc<F16>(128, 64));
+          commit_w(&t3.mma[t]);
+        }
+        stamp(16);
+        break;  // (the last layer ends here)
+      }
+#endif
       if (issue_warp) {  // M5: D2 = ReLU(H) W2   (N = 64, K = 32)
         issuer_wait_simt();
         t3_mma3<2>(R + kCW2, R + kCA2, 16, desc_s[12 + 2 * L], desc_s[13 + 2 * L], (2 * 64 * 16) >> 4, t3_idesc<F16>(128, 64));
@@ -745,7 +767,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       stamp(18);
     }
 
-    // ---- K5: y = x out_linear, masked max over rows, CTR head ----
+    // ---- K5: y = x out_linear, masked max over rows ----
+#ifdef TAV2_POOL_UNFUSED
     t3_st_split<64, F16>(cA, x);  // invalid rows carry x = 0
     tmem_st_wait();
     done();
@@ -756,12 +779,16 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
                  t3_idesc<F16>(128, 64));
       commit_w(&t3.mma[t]);
     }
+    constexpr uint32_t kCY = kCD;
+#else
+    constexpr uint32_t kCY = kCW2;  // issued in the last layer
+#endif
     stamp(20);
     wait_mma();
     stamp(21);
     {
       float y[kDModel];
-      t3_ld64(lanebase + kCD, y);
+      t3_ld64(lanebase + kCY, y);
       if (tid == 0) any_s = 0;
       named_bar_sync(1, kT3Threads);  // every row is past its last softmax (valid_w, kmax_s free)
       if (ok) any_s = 1;
@@ -817,7 +844,7 @@ cudaError_t launch_skut_tc3(const Params& p, const SkutImages3& img, const NNCfg
                             cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const int S_pad = (nn.seq_len + 15) & ~15;
-  const size_t smem = (size_t)p.num_layers * kW3Layer + kImg3WO + 4 * (size_t)S_pad * 128;
+  const size_t smem = (size_t)p.num_layers * kW3Layer + kImg3WO + kImg3W2O + 4 * (size_t)S_pad * 128;
   auto kern = f16 ? skut_tc3_kernel<true> : skut_tc3_kernel<false>;
   cudaError_t e = set_max_dyn_smem((const void*)kern, (int)smem);
   if (e != cudaSuccess) return e;

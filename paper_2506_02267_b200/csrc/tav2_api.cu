@@ -630,7 +630,7 @@ int tav2_load_params(tav2_ctx* c, int n, const char* const* names, const float* 
   c->cs_bound3 = c->cs_bound = 0.0;
   {
     const size_t lay = (size_t)kImg3WA + kImg3WB;
-    const size_t bytes3 = (size_t)L * lay + kImg3WO;
+    const size_t bytes3 = (size_t)L * lay + kImg3WO + kImg3W2O;
     std::vector<uint8_t> img3(bytes3, 0), img3h(bytes3, 0);
     std::vector<float> wqk(64 * 64), wvo(64 * 64);
     const double sc = 1.4426950408889634 / 8.0;
@@ -675,9 +675,23 @@ int tav2_load_params(tav2_ctx* c, int n, const char* const* names, const float* 
         put(base + kImg3WA + 8192, 64, 32, 0, host_of(P.w2[l]), 32, 64);
       }
     }
+    // W2' = W2 W_out of the last layer (f64): skut_tc3 computes the pooled
+    // projection y = x W_out of the last layer's output x = x_mid + ReLU(H) W2
+    // as x_mid W_out + ReLU(H) W2' -- one GEMM round trip instead of two
+    std::vector<float> w2o(32 * 64);
+    {
+      const float *w2 = host_of(P.w2[L - 1]), *wo = host_of(P.out_linear);
+      for (int i = 0; i < 32; ++i)
+        for (int j = 0; j < 64; ++j) {
+          double a = 0.0;
+          for (int m2 = 0; m2 < 64; ++m2) a += (double)w2[i * 64 + m2] * (double)wo[m2 * 64 + j];
+          w2o[i * 64 + j] = (float)a;
+        }
+    }
     for (int h16 = 0; h16 < 2; ++h16) {
       put_f16 = h16 != 0;
       put((h16 ? img3h : img3).data() + (size_t)L * lay, 64, 64, 0, host_of(P.out_linear), 64, 64);
+      put((h16 ? img3h : img3).data() + (size_t)L * lay + kImg3WO, 64, 32, 0, w2o.data(), 32, 64);
     }
     put_f16 = false;
     if (c->d_images3) cudaFree(c->d_images3);
@@ -691,6 +705,8 @@ int tav2_load_params(tav2_ctx* c, int n, const char* const* names, const float* 
     }
     c->images3.wout = c->d_images3 + (size_t)L * lay;
     c->images3h.wout = c->d_images3 + bytes3 + (size_t)L * lay;
+    c->images3.w2out = c->images3.wout + kImg3WO;
+    c->images3h.w2out = c->images3h.wout + kImg3WO;
   }
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);  // captured with the old parameters
   c->graphs.clear();

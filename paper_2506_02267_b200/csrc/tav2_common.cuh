@@ -134,10 +134,12 @@ constexpr int kImgWO = 2 * 64 * 64 * 2;   // 16384
 struct SkutImages3 {
   const uint8_t* w[kMaxLayers];
   const uint8_t* wout;
+  const uint8_t* w2out;  // W2 of the last layer times W_out (f64 product): the fused final FFN / pool GEMM
 };
 constexpr int kImg3WA = 2 * 128 * 64 * 2;  // 32768
 constexpr int kImg3WB = kImgWB - kImgWO;   // 16384 (W1 | W2)
 constexpr int kImg3WO = kImgWO;
+constexpr int kImg3W2O = 2 * 64 * 32 * 2;  // 8192 (W2 W_out, K = 32, N = 64)
 
 struct NNCfg {
   int32_t recent, k[3];       // k[0] = k_ll, k[1] = k_rt, k[2] = k_imp
