@@ -189,10 +189,14 @@ __device__ __forceinline__ void t4_layer_norm(const float* x, const float* g, co
 template <int KSTEPS>
 __device__ __forceinline__ void t4_mma3(uint32_t d, uint32_t a_col, uint32_t a_lo_off, uint32_t b_hi,
                                         uint32_t b_lo, uint32_t lbo, uint32_t idesc) {
+  // k-step-0 descriptors once; k-step j adds j * 2 lbo / 16 to the 14-bit
+  // start-address field (as skut_tc3: no per-k-step address rebuild)
+  const uint64_t bh0 = sdesc(b_hi, lbo, 128), bl0 = sdesc(b_lo, lbo, 128);
+  const uint32_t step16 = (2 * lbo) >> 4;
 #pragma unroll
   for (int j = 0; j < KSTEPS; ++j) {
-    const uint64_t bh = sdesc(b_hi + 2 * j * lbo, lbo, 128);
-    const uint64_t bl = sdesc(b_lo + 2 * j * lbo, lbo, 128);
+    const uint64_t bh = bh0 + (uint64_t)(j * step16);
+    const uint64_t bl = bl0 + (uint64_t)(j * step16);
     mma_bf16_ts_w(d, a_col + 8 * j, bh, idesc, j > 0);
     mma_bf16_ts_w(d, a_col + 8 * j, bl, idesc, 1);
     mma_bf16_ts_w(d, a_col + a_lo_off + 8 * j, bh, idesc, 1);
@@ -569,10 +573,11 @@ __global__ void __launch_bounds__(kT4Threads, 1) skut_tc4_kernel(Params p, SkutI
           issuer_wait_simt();
           const uint32_t id = t4_idesc<F16>(128, 64, 0, 1);
           const uint32_t sbo = (uint32_t)S_pad * 16;
+          // (16 keys = 2 groups of 8 keys x 128 B per k-step: +16 in the address field)
+          const uint64_t bh0 = sdesc(khi + (uint32_t)k0 * 16, 128, sbo), bl0 = sdesc(klo + (uint32_t)k0 * 16, 128, sbo);
           for (int j = 0; j < nch; ++j) {
-            const uint32_t koff = (uint32_t)(k0 + 16 * j) * 16;  // 2 groups of 8 keys x 128 B
-            const uint64_t bh = sdesc(khi + koff, 128, sbo);
-            const uint64_t bl = sdesc(klo + koff, 128, sbo);
+            const uint64_t bh = bh0 + (uint64_t)(16 * j);
+            const uint64_t bl = bl0 + (uint64_t)(16 * j);
             mma_bf16_ts_w(R + k4CO, R + k4CD + 16 * j, bh, id, (c > 0 || j > 0) ? 1u : 0u);
             mma_bf16_ts_w(R + k4CO, R + k4CD + 16 * j, bl, id, 1);
             mma_bf16_ts_w(R + k4CO, R + k4CD + 16 * j + 8, bh, id, 1);
