@@ -2,7 +2,7 @@
 #   bash tools/ab_bench.sh base pv
 for i in 1 2 3; do
   for v in "$@"; do
-    TAV2_LIB=${v#base} python bench.py --steps 300 --warmup 20 --no-cpu-baseline > gpurun_out/ab_$v.txt 2>&1
+    TAV2_LIB=${v#base} timeout 300 python bench.py --steps 300 --warmup 20 --no-cpu-baseline > gpurun_out/ab_$v.txt 2>&1
     python - "$v" <<'PY'
 import json, sys
 v = sys.argv[1]
