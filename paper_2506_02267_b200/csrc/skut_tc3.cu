@@ -804,8 +804,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     tok_pf = pf_idx >= 0 ? pf_off + pf_idx : -1;
 #endif
     {  // the next item's token row (tok_pf resolved in the last layer), under
-       // the head; always overwritten (row 0 for padding slots) so tfv is dead
-       // through the layers
+       // the pool barrier; always overwritten (row 0 for padding slots) so tfv
+       // is dead through the layers
       const size_t tr = (in_seq && tok_pf >= 0) ? (size_t)tok_pf : 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) ldg256(st.tok_feat + tr * kDModel + 8 * j, tfv + 8 * j);
