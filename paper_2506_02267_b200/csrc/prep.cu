@@ -31,7 +31,7 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
 // x[l + 4m]^2 in the unrolled-by-4 reverse order m = 3,2,1,0 then 7,6,5,4
 // (separately rounded products and additions), then (l0 + l1) + (l2 + l3).
 // Every thread of the quad gathers all 32 squares and returns the same value.
-__device__ __forceinline__ float quad_sumsq(const float* v, unsigned qm) {
+__device__ __forceinline__ float quad_sumsq(const float* v, unsigned qm) {  // (qm: the participating lanes)
   float s[32];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -125,17 +125,41 @@ __device__ __forceinline__ void prep_body(const Staged& st, int with_feat, const
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   int i = gt >> 2;
   const int g = gt & 3;
-  const unsigned qm = 0xfu << (threadIdx.x & 28);  // this quad's lanes (a quad is never split)
-  if (i < st.n_tok) {
-    const int8_t* q = reinterpret_cast<const int8_t*>(&raw);
-    float d[8];
+  // The quad's sum of squares at a point every lane of the warp reaches (a
+  // warp may hold token rows, candidate rows and padding): full-mask
+  // shuffles, not quad-masked ones inside the branches (each of which
+  // compiled to a divergence check)
+  const bool is_tok = i < st.n_tok;
+  const int8_t* q = reinterpret_cast<const int8_t*>(&raw);
+  float d[8];
+  if (is_tok) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) d[j] = deq_s[(int)q[j] + 128];  // core.py:54-57
-    float nrm = __fsqrt_rn(quad_sumsq(d, qm));
-    if (nrm == 0.0f) nrm = 1.0f;  // zero rows stay zero (core.py:69-74)
-    float u[8];
+  } else {
+    d[0] = v0.x; d[1] = v0.y; d[2] = v0.z; d[3] = v0.w; d[4] = v1.x; d[5] = v1.y; d[6] = v1.z; d[7] = v1.w;
+  }
+  const float ss = quad_sumsq(d, 0xffffffffu);
+  // unit rows of tokens and candidates alike (core.py:69-74, nnsearch.py:313-320;
+  // zero rows stay zero; padding lanes compute zeros and store nothing)
+  float nrm = __fsqrt_rn(ss);
+  if (nrm == 0.0f) nrm = 1.0f;
+  float u[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) u[j] = __fdiv_rn(d[j], nrm);
+  for (int j = 0; j < 8; ++j) u[j] = __fdiv_rn(d[j], nrm);
+  // features 0..31 of a token's Eq. 4 part = unit(q): thread g < 2 takes
+  // elements 16g..16g+15, held by threads 2g and 2g+1 (full-mask shuffles,
+  // every lane; g >= 2 and non-token lanes discard)
+  float fq[16];
+  if (with_feat) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float lo = __shfl_sync(0xffffffffu, u[j], 2 * (g & 1), 4);
+      const float hi = __shfl_sync(0xffffffffu, u[j], 2 * (g & 1) + 1, 4);
+      fq[j] = g < 2 ? lo : 0.0f;
+      fq[8 + j] = g < 2 ? hi : 0.0f;
+    }
+  }
+  if (is_tok) {
     float4* dst = reinterpret_cast<float4*>(st.tok_unit + (size_t)i * kEmbed + 8 * g);
     dst[0] = make_float4(u[0], u[1], u[2], u[3]);
     dst[1] = make_float4(u[4], u[5], u[6], u[7]);
@@ -147,18 +171,7 @@ __device__ __forceinline__ void prep_body(const Staged& st, int with_feat, const
     *reinterpret_cast<uint4*>(tile) = make_uint4(pack_h2(u[0], u[1]), pack_h2(u[2], u[3]), pack_h2(u[4], u[5]),
                                                  pack_h2(u[6], u[7]));
     if (with_feat) {  // token part of Eq. 4 (encoder.py:171-187): [unit(q) | 0] + bits @ action + surface
-      float f[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) f[j] = 0.0f;
-      // features 0..31 = unit(q): thread g < 2 takes elements 16g..16g+15,
-      // held by threads 2g and 2g+1 (all four shuffle, g >= 2 discard)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float lo = __shfl_sync(qm, u[j], 2 * (g & 1), 4);
-        const float hi = __shfl_sync(qm, u[j], 2 * (g & 1) + 1, 4);
-        f[j] = g < 2 ? lo : 0.0f;
-        f[8 + j] = g < 2 ? hi : 0.0f;
-      }
+      const float* f = fq;
       float asum[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) asum[j] = 0.0f;
@@ -185,12 +198,9 @@ __device__ __forceinline__ void prep_body(const Staged& st, int with_feat, const
   }
   i -= st.n_tok;
   if (i < st.n_items) {  // l2_normalize_rows of the candidates (nnsearch.py:313-320)
-    const float c[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-    float nrm = __fsqrt_rn(quad_sumsq(c, qm));
-    if (nrm == 0.0f) nrm = 1.0f;
     float4* dst = reinterpret_cast<float4*>(st.cand_unit + (size_t)i * kEmbed + 8 * g);
-    dst[0] = make_float4(__fdiv_rn(c[0], nrm), __fdiv_rn(c[1], nrm), __fdiv_rn(c[2], nrm), __fdiv_rn(c[3], nrm));
-    dst[1] = make_float4(__fdiv_rn(c[4], nrm), __fdiv_rn(c[5], nrm), __fdiv_rn(c[6], nrm), __fdiv_rn(c[7], nrm));
+    dst[0] = make_float4(u[0], u[1], u[2], u[3]);
+    dst[1] = make_float4(u[4], u[5], u[6], u[7]);
   }
 }
 
