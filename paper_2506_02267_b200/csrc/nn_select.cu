@@ -136,16 +136,23 @@ __device__ __forceinline__ void keys_staged(const KeySrc& ks, int n, int lane, f
 // 32w..32w+31) of a `words`-word bitmap lives at bm_phys(w): emitting lane l
 // owns logical words words-1-per*l-j (j = 0..per-1, descending) at physical
 // j*32 + l, so its reads are bank-conflict free.  (per*32 words.)
+// (per = words per lane, rounded up to a power of two: the mapping's
+// division and modulo become a shift and a mask -- an integer division by a
+// runtime divisor was ~20 instructions in every winner mark)
+__device__ __forceinline__ int bm_per_log(int words) {
+  const int per = (words + 31) >> 5;  // 1 .. 16
+  return 32 - __clz(per - 1);          // ceil(log2(per)) (0 for per = 1)
+}
 __device__ __forceinline__ int bm_phys(int w, int words) {
-  const int per = (words + 31) >> 5;
+  const int lg = bm_per_log(words);
   const int r = words - 1 - w;
-  return (r % per) * 32 + r / per;
+  return (r & ((1 << lg) - 1)) * 32 + (r >> lg);
 }
 __device__ __forceinline__ void bm_mark(uint32_t* bm, int words, int t) {
   atomicOr(bm + bm_phys(t >> 5, words), 1u << (t & 31));
 }
 __device__ __forceinline__ void bm_clear(uint32_t* bm, int words, int lane) {
-  for (int w = lane; w < ((words + 31) >> 5) * 32; w += 32) bm[w] = 0u;
+  for (int w = lane; w < (32 << bm_per_log(words)); w += 32) bm[w] = 0u;
 }
 
 // Emit the winners marked in the bitmap in descending storage index (the
@@ -153,7 +160,7 @@ __device__ __forceinline__ void bm_clear(uint32_t* bm, int words, int lane) {
 // prefix sum of the per-lane counts places its bits.
 __device__ __forceinline__ void emit_bitmap(const uint32_t* bm, int words, int k, int lane, int32_t* orow,
                                             double* srow, const KeySrc& ks, int dbg_slot = -1, long long t0 = 0) {
-  const int per = (words + 31) / 32;    // <= 16 (kCaps0 positions)
+  const int per = 1 << bm_per_log(words);  // <= 16 (kCaps0 positions), as bm_phys
   const int w_hi = words - per * lane;  // this lane's logical words: [w_hi - per, w_hi)
   int cnt = 0;
   uint32_t nz = 0u;  // this lane's nonzero words (bit j: logical word w_hi - 1 - j)
