@@ -426,15 +426,21 @@ __device__ __forceinline__ void nn_bound_body(const Staged& st, const NNCfg& nn,
   const int item = blockIdx.x * kBoundWarps + warp;
   const int s = blockIdx.y;
   griddep_launch();
+  // the request's source ranges come from the staged plan (copied before the
+  // chain started): read before the wait, their round trips overlap it
+  int lo = 0, hi = 0, glog = 0;
+  if (item < st.n_items) {
+    const ReqInfo& rq = st.req[st.item_req[item]];
+    lo = rq.tok_off[s] + (s == 1 ? min(nn.recent, rq.len[1]) : 0);
+    hi = rq.tok_off[s] + rq.len[s];
+    glog = rq.glog[s];
+  }
   griddep_wait();  // scan pass 1 complete (and the previous select is done with count)
   cta_stamp(kDbgBound, 2);
   if (item >= st.n_items) return;
   if (lane == 0) sc.count[(size_t)item * 3 + s] = 0u;
-  const ReqInfo& rq = st.req[st.item_req[item]];
   const int k = nn.k[s];
-  const int lo = rq.tok_off[s] + (s == 1 ? min(nn.recent, rq.len[1]) : 0), hi = rq.tok_off[s] + rq.len[s];
   if (!nn_scanned(hi - lo, k)) return;  // no scan (nn_select takes every token)
-  const int glog = rq.glog[s];
   const int ng = ((hi - 1) >> glog) - (lo >> glog) + 1;
   float* out = sc.bound + (size_t)item * 3 + s;
   const float* g = sc.gmax + ((size_t)item * 3 + s) * sc.gcap + ((lo >> glog) & 7);

@@ -655,6 +655,16 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = sel_item(warp);
   const int s = sel_source();
+  // the request's source offsets / lengths come from the staged plan (copied
+  // before the chain started): read before the wait, their round trips overlap it
+  int q_len1 = 0, q_lens = 0, q_off0 = 0, q_offs = 0;
+  if (item < st.n_items) {
+    const ReqInfo& rq0 = st.req[st.item_req[item]];
+    q_len1 = rq0.len[1];
+    q_lens = rq0.len[s];
+    q_off0 = rq0.tok_off[0];
+    q_offs = rq0.tok_off[s];
+  }
   griddep_wait();  // scan pass 2 complete
   // dependents launch only now: with SelFlags the SKUT kernel skips its
   // up-front griddep_wait, so it must not start before prep .. scan2 are
@@ -662,12 +672,11 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
   griddep_launch();
   cta_stamp(kDbgSelect, 2);
   if (item >= st.n_items) return;  // warp-uniform
-  const ReqInfo& rq = st.req[st.item_req[item]];
   const int S = nn.seq_len;
   const int k = nn.k[s];
 
   if (s == 1) {  // verbatim recent real-time segment RT[:r] reversed
-    const int n_recent = min(nn.recent, rq.len[1]);
+    const int n_recent = min(nn.recent, q_len1);
     for (int j = lane; j < nn.recent; j += 32) {
       idx[(size_t)item * S + nn.seg_start[1] + j] = j < n_recent ? n_recent - 1 - j : -1;
       if (scores) scores[(size_t)item * S + nn.seg_start[1] + j] = 0.0;
@@ -677,10 +686,10 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
   const int seg = s == 0 ? 0 : (s == 1 ? 2 : 3);
   int32_t* orow = idx + (size_t)item * S + nn.seg_start[seg];
   double* srow = scores ? scores + (size_t)item * S + nn.seg_start[seg] : nullptr;
-  const int lo = s == 1 ? min(nn.recent, rq.len[1]) : 0, hi = rq.len[s];
+  const int lo = s == 1 ? min(nn.recent, q_len1) : 0, hi = q_lens;
 
   if (hi - lo <= k) {  // 1. everything selected, descending storage index
-    const float* tok = st.tok_unit + (size_t)rq.tok_off[s] * kEmbed;
+    const float* tok = st.tok_unit + (size_t)q_offs * kEmbed;
     const float* cu = st.cand_unit + (size_t)item * kEmbed;
     for (int j = lane; j < k; j += 32) {
       const int t = hi - 1 - j;
@@ -701,9 +710,9 @@ __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn
   // 2./3. select over the survivors (all tokens of a source too small to scan)
   const bool scanned = nn_scanned(hi - lo, k);
   KeySrc ks;
-  ks.surv = scanned ? sc.surv + (size_t)item * sc.surv_stride + (rq.tok_off[s] - rq.tok_off[0]) : nullptr;
+  ks.surv = scanned ? sc.surv + (size_t)item * sc.surv_stride + (q_offs - q_off0) : nullptr;
   ks.first = lo;
-  ks.tok = st.tok_unit + (size_t)rq.tok_off[s] * kEmbed;
+  ks.tok = st.tok_unit + (size_t)q_offs * kEmbed;
   {
     const float4* cu = reinterpret_cast<const float4*>(st.cand_unit + (size_t)item * kEmbed);
 #pragma unroll
