@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(256) prep_kernel(Staged st, Params p, int with
   if (epoch_bump && blockIdx.x == 0 && threadIdx.x == 0) {
     const uint32_t e = *epoch_bump + 1u;
     *epoch_bump = e ? e : 1u;
+    epoch_bump[1] = 0u;  // the SKUT's dynamic item counter (SelFlags::next_item)
   }
   cta_stamp(kDbgPrep, 2);
   // this thread's global inputs, requested before the table staging so the

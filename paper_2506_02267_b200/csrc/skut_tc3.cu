@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   __shared__ __align__(16) float lnp_s[2][4][kDModel];
   __shared__ float red_s[kT3Warps][kDModel];
   __shared__ int any_s;
+  __shared__ int nx_s;  // the item after the next one (dynamic rounds)
   __shared__ unsigned kmax_s[2];
 
   const int S = nn.seq_len;
@@ -361,7 +362,14 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
 #pragma unroll
     for (int j = 0; j < 8; ++j) ldg256(st.tok_feat + tr * kDModel + 8 * j, tfv + 8 * j);
   }
-  for (int item = blockIdx.x; item < n; item += gridDim.x) {
+  // Items: the first two rounds round-robin, then a counter (sel.next_item,
+  // zeroed by prep): a CTA that started late or ran slow takes fewer of the
+  // last rounds' items.  The claim for item k+2 is made in item k's last
+  // layer and handed over in nx_s at its pool barrier; the next item is then
+  // known a whole layer ahead (its index chain is prefetched there).
+  int nx = 0;
+  uint32_t claim = 0u;
+  for (int item = blockIdx.x; item < n; item = nx) {
     if (kDebug && dbg) {
       dbg[31] += 1;
       t_last = clock64();
@@ -414,11 +422,13 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
 
     for (int L = 0; L < NL; ++L) {
       if (L == NL - 1) {
-        const int nx = item + gridDim.x;
         if (!sel_all) {
           griddep_wait();
           sel_all = true;
         }
+        // (nx_s was written by tid 0 before the previous item's pool barrier)
+        nx = (sel.next_item == nullptr || item < (int)gridDim.x) ? item + (int)gridDim.x : nx_s;
+        if (sel.next_item != nullptr && tid == 0) claim = atomicAdd(sel.next_item, 1u);  // consumed at the pool
 #ifdef TAV2_OLD_PF
         tok_pf = (in_seq && nx < n) ? slot_token(st, nn, idx, nx, r) : -1;
 #else
@@ -800,6 +810,9 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         if (lane == 0) red_s[warp][j] = v;
       }
     }
+    // (every thread read nx_s at this item's last-layer top, before its
+    // kvready arrival, which tid 0 has waited on since)
+    if (sel.next_item != nullptr && tid == 0) nx_s = 2 * (int)gridDim.x + (int)claim;
 #ifndef TAV2_OLD_PF
     tok_pf = pf_idx >= 0 ? pf_off + pf_idx : -1;
 #endif

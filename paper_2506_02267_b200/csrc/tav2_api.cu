@@ -463,8 +463,8 @@ int tav2_create(const tav2_config* cfg, const tav2_capacity* cap, int device, ta
       return bad(e, "scan survivors");
     if ((e = cudaMalloc(&d.sel_done, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "select flags");
     if ((e = cudaMemset(d.sel_done, 0, (size_t)N * 3 * 4)) != cudaSuccess) return bad(e, "select flags");
-    if ((e = cudaMalloc(&d.sel_epoch, 4)) != cudaSuccess) return bad(e, "select epoch");
-    if ((e = cudaMemset(d.sel_epoch, 0, 4)) != cudaSuccess) return bad(e, "select epoch");
+    if ((e = cudaMalloc(&d.sel_epoch, 8)) != cudaSuccess) return bad(e, "select epoch");  // + SKUT item counter
+    if ((e = cudaMemset(d.sel_epoch, 0, 8)) != cudaSuccess) return bad(e, "select epoch");
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if ((e = cudaMalloc(&d.skut_scratch, (size_t)sms * skut_simt_scratch_floats(S) * 4)) != cudaSuccess)
@@ -1060,7 +1060,7 @@ SelFlags next_sel(tav2_ctx* c) {
 #ifdef TAV2_NO_SELFLAGS
   return SelFlags{nullptr, nullptr, 0};
 #endif
-  return SelFlags{c->cur_dv().sel_done, c->cur_dv().sel_epoch, device_sms()};
+  return SelFlags{c->cur_dv().sel_done, c->cur_dv().sel_epoch, device_sms(), c->cur_dv().sel_epoch + 1};
 }
 
 // NN selection (both precision modes: the scan's survivors are re-scored with

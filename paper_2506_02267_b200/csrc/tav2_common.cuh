@@ -222,6 +222,9 @@ struct SelFlags {
   uint32_t* done;
   const uint32_t* epoch;  // device word: the current run's epoch (prep_kernel bumps it)
   int n_first;
+  // device word after the epoch: the SKUT's item counter from its third
+  // round on (prep_kernel zeroes it; null -> static round-robin items)
+  uint32_t* next_item = nullptr;
 };
 __device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
