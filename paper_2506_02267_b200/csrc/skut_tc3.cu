@@ -328,6 +328,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
   if (issue_warp) {
     mbar_wait(&t3.wfull, 0);
     fence_after();
+    cta_stamp(8, 2);  // (debug) weights landed
   }
   const float4* pos4 = reinterpret_cast<const float4*>(p.position_table + (size_t)(in_seq ? r : 0) * kDModel);
 
@@ -423,7 +424,9 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     for (int L = 0; L < NL; ++L) {
       if (L == NL - 1) {
         if (!sel_all) {
+          cta_stamp(9, 1);  // (debug) first item's last layer reached
           griddep_wait();
+          cta_stamp(9, 0);  // (debug) select grid complete
           sel_all = true;
         }
         // (nx_s was written by tid 0 before the previous item's pool barrier)
@@ -835,8 +838,10 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     }
     // (red_s is rewritten only after the next item's pool barrier)
     stamp(23);
+    if (item == (int)blockIdx.x) cta_stamp(8, 0);  // (debug) first item pooled
   }
   if (kDebug && dbg) dbg[27] += dbg_m3;
+  cta_stamp(8, 1);  // (debug) last item pooled
   fence_before();
   __syncthreads();
   if (warp == 0) tmem_free<512>(0u);

@@ -29,7 +29,7 @@ flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 for _ in range(5):
     eng.run_staged("bf16", logits)
 torch.cuda.synchronize()
-buf = torch.zeros(8 * 3 * 4096, dtype=torch.int64, device="cuda")
+buf = torch.zeros(10 * 3 * 4096, dtype=torch.int64, device="cuda")  # kernel ids 0-8 (8: SKUT item stamps)
 N.lib().tav2_debug_cta(buf.data_ptr())
 if "--flush" in sys.argv:
     flush.zero_()
