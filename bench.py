@@ -533,6 +533,12 @@ def _open_loop(eng, pool, mode, rate, seconds=2.0):
     b = S.DynamicBatcher(S.BatcherConfig(max_batch=n_item, max_wait=0.0005, workers=1), h)
     b.start()
     n = max(10, int(rate * seconds))
+    # a serving process's GIL hand-off interval: the submitter, batcher and
+    # completion threads each hold the GIL for microseconds, and CPython's
+    # 5 ms default forced-switch interval shows up in the tail
+    # (tools/open_loop_probe.py: p99 1.0-1.7 -> 0.95-1.05 ms at 50% load)
+    sw0 = sys.getswitchinterval()
+    sys.setswitchinterval(2e-4)
     try:
         for i in range(20):  # warm the loop
             b.submit(payloads[i % len(payloads)], n_item).done.wait(10)
@@ -565,6 +571,7 @@ def _open_loop(eng, pool, mode, rate, seconds=2.0):
             p.done.wait(30)
         wall = time.perf_counter() - t0
     finally:
+        sys.setswitchinterval(sw0)
         b.stop()
         h.close()
     errors = sum(p.error is not None for p in ps)

@@ -16,9 +16,12 @@ nn = P.NNConfig()
 model = P.RankingModel.init(P.ModelConfig.for_nn(nn), seed=0)
 eng = Engine(model, capacity=Capacity(1, 1000, 16896))
 pool = [[r] for r in P.synthetic_requests(4, 1000, 16384, 256, 256, seed=0)]
-for frac in (0.5, 0.5, 0.7, 0.85):
-    rate = frac * 4.6e6 / 1000
+sw0 = sys.getswitchinterval()
+for sw, frac in [(sw0, 0.5), (2e-4, 0.5), (sw0, 0.5), (2e-4, 0.5), (sw0, 0.7), (2e-4, 0.7), (2e-4, 0.85)]:
+    rate = frac * 5.5e6 / 1000
+    sys.setswitchinterval(sw)
     r = bench._open_loop(eng, pool, "bf16", rate, seconds=2.0)
-    print(f"rate {rate:.0f} req/s: p50 {r['p50_request_ms']} p99 {r['p99_request_ms']} ms, achieved "
+    sys.setswitchinterval(sw0)
+    print(f"switch {sw * 1e3:.1f} ms rate {rate:.0f} req/s: p50 {r['p50_request_ms']} p99 {r['p99_request_ms']} ms, achieved "
           f"{r['achieved_cand_s'] / 1e6:.2f}M cand/s; queueing p99 {r['stages_ms']['queueing']['p99']} "
           f"forward p99 {r['stages_ms']['forward']['p99']}", flush=True)
