@@ -621,9 +621,12 @@ __device__ __forceinline__ void select_direct(const KeySrc& ks, const float* ucf
 __device__ __forceinline__ void nn_select_body(const Staged& st, const NNCfg& nn, const NNScan& sc,
                                                int32_t* idx, double* scores);
 
-// CTA -> (candidate pair, source): source-major, so with the C2 shapes the
-// first candidate of every SKUT CTA (items < 148, SelFlags) is selected in
-// the first wave (a candidate-major order measured 1% slower)
+// CTA -> (candidate pair, source): source-major, the slowest source (0,
+// long-lifelong) first, so the second wave (6 CTAs per SM at C2: 888 of
+// 1,500 CTAs in the first) holds only short source-1/2 warps.  (A
+// candidate-major order measured 1% slower; an order that also moves the
+// source-1/2 warps of the SKUT CTAs' first candidates into the first wave
+// measured neutral: the SKUT's claimed last rounds absorb its start skew.)
 __device__ __forceinline__ int sel_item(int warp) { return blockIdx.x * kSelWarps + warp; }
 __device__ __forceinline__ int sel_source() { return blockIdx.y; }
 
