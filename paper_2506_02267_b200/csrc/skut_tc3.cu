@@ -27,7 +27,8 @@
 // the keys < S_pad/2 (half the score / P.V MMA work).  Two independent
 // tiles (warps 4t..4t+3), each with its own TMEM half (256 columns), its own
 // simt/mma barriers and issuing warp (warp 4t); they couple only through the
-// K/V operands (kvready / kvfree).  All weight images stay resident in
+// K/V operands (kready: every row's K and ||a||^2 after P1; kvready: every
+// row's V' after P2; kvfree).  All weight images stay resident in
 // shared memory for the CTA's lifetime (loaded once); the token features of
 // the gather come precomputed from prep_kernel (tok_feat).
 //
@@ -66,7 +67,7 @@ constexpr int kW3Layer = kImg3WA + kImg3WB;  // 48 KB per layer
 __device__ long long* g_dbg_skut3 = nullptr;
 
 struct T3Bars {
-  uint64_t simt[2], mma[2], kvready, kvfree, wfull, order;
+  uint64_t simt[2], mma[2], kready, kvready, kvfree, wfull, order;
 };
 __shared__ __align__(8) T3Bars t3;
 
@@ -220,6 +221,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
     mbar_init(&t3.simt[1], 128);
     mbar_init(&t3.mma[0], 1);
     mbar_init(&t3.mma[1], 1);
+    mbar_init(&t3.kready, kT3Threads);
     mbar_init(&t3.kvready, kT3Threads);
     mbar_init(&t3.kvfree, 2);
     mbar_init(&t3.wfull, 1);
@@ -417,7 +419,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       }
     }
     stamp(0);
-    // (no barrier: valid_w is read only in the softmax, after kvready -- every
+    // (no barrier: valid_w is read only in the softmax, after kready -- every
     // thread arrives there after its own validity bits)
     stamp(1);
 
@@ -488,6 +490,9 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         for (int o = 16; o > 0; o >>= 1) an2 = fmaxf(an2, __shfl_xor_sync(0xffffffffu, an2, o));
         if (lane == 0) atomicMax(&kmax_s[L], __float_as_uint(an2));
         tmem_st_wait();
+        fence_proxy_async();  // K (smem) -> the M2s of both tiles
+        fence_before();
+        mbar_arrive(&t3.kready);
         done();
       }
       stamp(3);
@@ -561,11 +566,15 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         tmem_st_wait();
         fence_proxy_async();
         fence_before();
-        mbar_arrive(&t3.kvready);  // this row's K, V' and Q' are in place
+        mbar_arrive(&t3.kvready);  // this row's V' is in place (the M3s)
+        done();                    // this tile's Q' is in place (its M2)
       }
       stamp(6);
       if (issue_warp) {  // M2: S = Q' K^T   (N = keys of this tile, K = 64)
-        mbar_wait(&t3.kvready, n_kv & 1);
+        // this tile's Q' plus every row's K (P1): the M2 no longer waits for
+        // the other tile's P2 (V' is needed only by the M3s)
+        issuer_wait_simt();
+        mbar_wait(&t3.kready, n_kv & 1);
         fence_after();
         if (t == 0) order_after_tile1();
         t3_mma3<4>(R + kCD, R + kCA, 32, desc_s[4], desc_s[5], 2 * S_pad, t3_idesc<F16>(128, NK));
@@ -585,7 +594,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
         const int nch = NK / 16;
         const int jlast = min(nch - 1, (rpw * kb + rpw - 1) / 16);  // warp-uniform causal bound
         float mb;
-        mbar_wait_sleep(&t3.kvready, n_kv & 1);  // kmax_s[L] complete (already passed)
+        mbar_wait_sleep(&t3.kready, n_kv & 1);  // kmax_s[L] complete (already passed)
         stamp(24);
         {  // Cauchy-Schwarz: >= every score of the row (up to the MUFU rsqrt's
            // ~2 ulp: any shift works, this one keeps exp2 in range)
@@ -675,6 +684,8 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       stamp(9);
       if (issue_warp) {  // M3: O' = P V'   (N = 64, K = keys; V' MN-major)
         issuer_wait_simt();
+        mbar_wait(&t3.kvready, n_kv & 1);  // every row's V' (tile 0's keys may reach into tile 1's rows)
+        fence_after();
         stamp(29);
         const uint32_t id = t3_idesc<F16>(128, 64, 0, 1);
         const int nk16 = NK / 16;  // <= 12 (S_pad <= 192); unrolled, warp-uniform bound
@@ -814,7 +825,7 @@ __global__ void __launch_bounds__(kT3Threads, 1) skut_tc3_kernel(
       }
     }
     // (every thread read nx_s at this item's last-layer top, before its
-    // kvready arrival, which tid 0 has waited on since)
+    // kready arrival, which tid 0 has waited on since)
     if (sel.next_item != nullptr && tid == 0) nx_s = 2 * (int)gridDim.x + (int)claim;
 #ifndef TAV2_OLD_PF
     tok_pf = pf_idx >= 0 ? pf_off + pf_idx : -1;
