@@ -37,7 +37,7 @@ torch.cuda.synchronize()
 eng.run_staged("bf16", logits)
 torch.cuda.synchronize()
 N.lib().tav2_debug_cta(None)
-t = buf.cpu().numpy().reshape(8, 3, 4096)
+t = buf.cpu().numpy().reshape(10, 3, 4096)
 t0 = min(int(t[k, 0][t[k, 0] > 0].min()) for k in range(6) if (t[k, 0] > 0).any())
 for k, name in enumerate(KERNELS):
     n = int((t[k, 0] > 0).sum())

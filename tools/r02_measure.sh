@@ -2,6 +2,7 @@
 # (outputs under gpurun_out/r02_*; copied into profiles/ afterwards).
 set -x
 python -m paper_2506_02267_b200.build
+python -m paper_2506_02267_b200.build --debug
 python bench.py > gpurun_out/r02_bench.json 2> gpurun_out/r02_bench.err
 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/r02_bench_reference.json 2>&1
 python bench.py --config c3 --no-cpu-baseline > gpurun_out/r02_c3.json 2>&1
