@@ -394,11 +394,21 @@ __device__ __forceinline__ float bisect_kth(const float* g, int ng, int k, int l
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
   }
+  // four independent counters: one counter compiled to a PER-long chain of
+  // dependent predicated increments per bisection step (step 0.2062 ->
+  // 0.2060 ms; a CTA of 4 warps per (candidate, source) instead, 3000 CTAs,
+  // was slower: 0.2067 ms, the CTA launches of the grid set the bound's end)
+  static_assert(PER % 4 == 0, "PER must be a multiple of 4");
   auto count_ge = [&](float x) {
-    int c = 0;
+    int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
 #pragma unroll
-    for (int j = 0; j < PER; ++j) c += v[j] >= x ? 1 : 0;
-    return (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
+    for (int j = 0; j < PER; j += 4) {
+      c0 += v[j] >= x ? 1 : 0;
+      c1 += v[j + 1] >= x ? 1 : 0;
+      c2 += v[j + 2] >= x ? 1 : 0;
+      c3 += v[j + 3] >= x ? 1 : 0;
+    }
+    return (int)__reduce_add_sync(0xffffffffu, (unsigned)((c0 + c1) + (c2 + c3)));
   };
   if (count_ge(mx) >= k) return mx;
   // T only has to stay <= the k-th largest maximum: stop once the bracket is
