@@ -516,7 +516,7 @@ def run_gpu(args, rank, world, local_rank):
     return out
 
 
-def _open_loop(eng, pool, mode, rate, seconds=2.0):
+def _open_loop(eng, pool, mode, rate, seconds=2.0, per_batch=1):
     """Fixed-rate arrivals of the pool's requests (payload (user id,
     candidates)) through serving.DynamicBatcher + serving.PipelinedHandler."""
     from paper_2506_02267_b200 import serving as S
@@ -530,7 +530,7 @@ def _open_loop(eng, pool, mode, rate, seconds=2.0):
     n_item = len(payloads[0][1])
     stats = S.LatencyStats(window=3600.0)
     h = S.PipelinedHandler(eng, users, mode=mode, stats=stats)
-    b = S.DynamicBatcher(S.BatcherConfig(max_batch=n_item, max_wait=0.0005, workers=1), h)
+    b = S.DynamicBatcher(S.BatcherConfig(max_batch=per_batch * n_item, max_wait=0.0005, workers=1), h)
     b.start()
     n = max(10, int(rate * seconds))
     # a serving process's GIL hand-off interval: the submitter, batcher and

@@ -492,8 +492,9 @@ class Engine:
     @_locked
     def submit(self, requests, mode: str = "bf16", want_idx: bool = False) -> tuple[int, int, object]:
         """tav2_rank_submit: stage into the next free slot and enqueue the
-        whole rank; returns (slot, items, keep-alive).  At most two submits
-        may be outstanding: ``wait`` + ``collect`` a slot before it is reused."""
+        whole rank; returns (slot, items, keep-alive).  At most
+        tav2_stage_slots() submits may be outstanding: ``wait`` + ``collect``
+        a slot before it is reused."""
         if self.model is None:
             raise ValidationError("no model loaded")
         pack = _Pack(requests)
