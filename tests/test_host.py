@@ -92,6 +92,23 @@ def test_sigmoid_and_final_score():
     np.testing.assert_allclose(r.final, orc.final_score(r.probs))
 
 
+def test_sigmoid_bit_identical_to_the_split_form():
+    """serving.sigmoid computes both branches from one exp(-|x|); the
+    reference's split form (trainer.py:230-236, oracle.sigmoid) must come out
+    bit for bit, in f32 and f64, at every array length (SIMD tails)."""
+    rng = np.random.default_rng(11)
+    for dt in (np.float32, np.float64):
+        for shape in [(), (1,), (3, 4), (17, 4), (1000, 4), (8192, 4)]:
+            x = (rng.standard_normal(shape) * 12).astype(dt)
+            if x.size >= 4:
+                x.flat[:4] = [0.0, -0.0, -110.0, 110.0]
+            a, b = serving.sigmoid(x), orc.sigmoid(x)
+            assert a.dtype == b.dtype and a.shape == b.shape
+            assert a.tobytes() == b.tobytes(), (dt, shape)
+    nan = serving.sigmoid(np.array([np.nan, 1.0], np.float32))
+    assert np.isnan(nan[0]) and nan[1] == orc.sigmoid(np.array([1.0], np.float32))[0]
+
+
 def test_synthetic_requests_are_valid():
     for r in P.generate_requests(3, 50, 2000, 256, 256, seed=5):
         r.user.validate()
