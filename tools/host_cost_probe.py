@@ -58,3 +58,34 @@ t("_response", lambda: S._response(np.arange(1000, dtype=np.uint64), logits, mod
 st = S.LatencyStats(window=3600.0)
 t("stats.record", lambda: st.record("forward", 1e-4))
 t("time.monotonic", time.monotonic)
+
+# the copy tav2_stage does: the request's columns into a pinned arena
+import torch  # noqa: E402
+
+cols = [b.embeddings for b in (r.user.lifelong, r.user.realtime, r.user.impression)] + [r.candidates]
+cols += [b.actions for b in (r.user.lifelong, r.user.realtime, r.user.impression)]
+cols += [b.surfaces for b in (r.user.lifelong, r.user.realtime, r.user.impression)]
+nbytes = sum(c.nbytes for c in cols)
+pinned = torch.empty(nbytes + 4096, dtype=torch.uint8, pin_memory=True).numpy()
+plain = np.empty_like(pinned)
+
+
+def copy_into(dst):
+    o = 0
+    for c in cols:
+        b = c.reshape(-1).view(np.uint8)
+        dst[o:o + b.size] = b
+        o += b.size
+
+
+t(f"numpy copy {nbytes >> 10} KB -> pinned", lambda: copy_into(pinned))
+t(f"numpy copy {nbytes >> 10} KB -> pageable", lambda: copy_into(plain))
+t("eng.stage (tav2_stage)", lambda: eng.stage(req))
+
+import ctypes  # noqa: E402
+
+pk = _Pack(req)
+nn_ = ctypes.c_int32()
+sid = eng.stream()
+t("raw tav2_stage (ctypes)", lambda: eng._lib.tav2_stage(eng._ctx, pk.arr, 1, sid, ctypes.byref(nn_)))
+t("eng.stage again", lambda: eng.stage(req))
